@@ -1,0 +1,119 @@
+/* qt_sse.h — C ABI of libqtsse.so, the B200 (sm_100a) electron-phonon scattering
+ * self-energy (SSE) hot path of Ziogas et al., SC19 (arXiv 1912.10024).
+ *
+ * The library evaluates, for X ∈ {<,>} and Y the other one:
+ *   Σ^X_aa(kz,E)  — Eq. 3, PAPER.md P:355-365 (electron SSE, diagonal atom blocks)
+ *   Π^X_ab(ω,qz)  — Eq. 4, PAPER.md P:366-375 (phonon SSE, self + N_b neighbour blocks)
+ * from the tensors of PAPER.md P:386-397, with the readings R1-R19 of DESIGN.md §3:
+ *   Σ^X[kz][E][a] = scale_Σ · Σ_{s,qz,m} Σ_{i,j} ∇_iH_{ab} ·
+ *        ( Dc^X_{ij}(qz,m) G^X_b(kz-qz, E-s_m) + Dc^Y_{ji}(qz,m) G^X_b(kz-qz, E+s_m) ) · ∇_jH_{ba}
+ *   Dc^X_{ij}(qz,m) = D^X[qz][m][b][r+1] - D^X[qz][m][b][0] - D^X[qz][m][a][0] + D^X[qz][m][a][s+1]
+ *   Π^X[qz][m][a][s+1]_{ij} = scale_Π · Σ_{kz,E} tr{ ∇_iH_{ba} G^X_a(kz+qz, E+s_m) ∇_jH_{ab} G^Y_b(kz,E) }
+ *   Π^X[qz][m][a][0] = Σ_s Π^X[qz][m][a][s+1]
+ * where b = nbr[a][s], r = the slot of a in nbr[b], s_m = shift0 + m·shift_step (ħω_m/ΔE),
+ * kz-qz ↦ (kz-qz+h) mod Nkz, kz+qz ↦ (kz+qz-h) mod Nkz, h = Nkz/2, and energies
+ * outside [0,NE) contribute nothing (zero extension, never clamped).
+ *
+ * Tensors (all complex128, interleaved (re,im), row-major, 16-byte aligned):
+ *   G≷, Σ≷ : [Nkz][NE][Na][Norb][Norb]
+ *   D≷, Π≷ : [Nqz][Nw][Na][Nb+1][3][3]      (slot 0 = self, slot s+1 = neighbour s)
+ *   dH     : [Na][Nb][3][Norb][Norb]        dH[a][s][i] = ∇_i H_{a, nbr[a][s]}
+ *   neighbors (host, int32): [Na][Nb], -1 = empty slot; must be symmetric.
+ * With nranks > 1 (QT_SHARD_ATOM) the G/D/Σ/Π/dH pointers hold the rank's LOCAL atom
+ * window described by qt_sse_info (see qt_sse_query): atoms [w_lo, w_hi) for inputs
+ * (owned atoms + neighbour halo), atoms [a_lo, a_hi) for outputs.
+ *
+ * Ownership: the caller owns every tensor; outputs are OVERWRITTEN (never accumulated);
+ * inputs are never modified. The plan owns its device workspace, work lists and
+ * (nranks > 1) its NCCL communicator.
+ * Execution: calls are stream-ordered and asynchronous on `stream`; argument and
+ * launch errors are returned synchronously; asynchronous device faults surface as
+ * QT_ERR_CUDA on a later call. No exceptions cross the ABI. One plan per host thread.
+ * A plan is reusable with new tensor pointers of the same dimensions.
+ */
+#ifndef QT_SSE_H
+#define QT_SSE_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QT_OK = 0,
+  QT_ERR_INVALID_ARG = 1,   /* bad dims, neighbour table, null/misaligned/aliased pointer */
+  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12, shift_step != 1, FP32 mode, ...                */
+  QT_ERR_OUT_OF_MEMORY = 3,
+  QT_ERR_CUDA = 4,
+  QT_ERR_NCCL = 5,
+  QT_ERR_INTERNAL = 6
+} qt_status;
+
+typedef enum { QT_PREC_FP64 = 0, QT_PREC_FP32_MIXED = 1 } qt_precision;
+typedef enum { QT_SHARD_NONE = 0, QT_SHARD_ENERGY = 1, QT_SHARD_ATOM = 2 } qt_shard;
+
+typedef struct {
+  int64_t Na, Nb, Norb, N3D, NE, Nw, Nkz, Nqz; /* paper symbols; N3D must be 3; Nkz == Nqz          */
+  int32_t shift0, shift_step;                  /* ħω_m/ΔE = shift0 + m·shift_step; shift0 ≥ 1        */
+  qt_precision precision;                      /* QT_PREC_FP64 only (FP32 mode: not yet)            */
+  qt_shard shard;                              /* QT_SHARD_NONE, or QT_SHARD_ATOM with nranks > 1   */
+  int32_t rank, nranks;
+  const void* nccl_unique_id;                  /* host ptr to a 128-byte ncclUniqueId (nranks > 1)  */
+  size_t workspace_limit;                      /* bytes of device scratch the plan may use; 0 = auto */
+} qt_sse_desc;
+
+typedef struct qt_sse_plan_s* qt_sse_plan_t;
+
+typedef struct {
+  int64_t a_lo, a_hi;       /* atoms whose Σ/Π this rank computes (outputs)               */
+  int64_t w_lo, w_hi;       /* atom window of this rank's input tensors (owned + halo)    */
+  int64_t npairs;           /* valid (a,s) pairs with a in [a_lo,a_hi)                      */
+  size_t workspace_bytes;   /* device bytes owned by the plan                               */
+  double flops_sigma;       /* algorithmic FP64 flops of one qt_sse_sigma call (both X)     */
+  double flops_pi;          /* algorithmic FP64 flops of one qt_sse_pi call (both X)        */
+  double halo_bytes;        /* bytes received per call pair in the atom-halo exchange       */
+} qt_sse_info;
+
+/* Validates desc + neighbours, builds the work lists, allocates the workspace. */
+qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* neighbors_host, void* cuda_stream,
+                      qt_sse_plan_t* plan_out);
+
+/* Σ^<, Σ^> (Eq. 3). scale = complex ∫dħω/2π weight (default i·ΔE/2π, R8). */
+qt_status qt_sse_sigma(qt_sse_plan_t plan, const void* dH, const void* G_less, const void* G_gtr,
+                       const void* D_less, const void* D_gtr, double scale_re, double scale_im,
+                       void* Sig_less, void* Sig_gtr, void* cuda_stream);
+
+/* Π^<, Π^> (Eq. 4). scale = complex ∫dE/2π weight (default -i·ΔE/2π, R8). */
+qt_status qt_sse_pi(qt_sse_plan_t plan, const void* dH, const void* G_less, const void* G_gtr,
+                    double scale_re, double scale_im, void* Pi_less, void* Pi_gtr, void* cuda_stream);
+
+/* End-to-end call on HOST buffers (pinned or pageable): copies inputs to device
+ * buffers owned by the plan, runs qt_sse_sigma + qt_sse_pi, copies Σ≷, Π≷ back,
+ * and synchronizes `cuda_stream` before returning. */
+qt_status qt_sse_execute_host(qt_sse_plan_t plan, const void* dH, const void* G_less, const void* G_gtr,
+                              const void* D_less, const void* D_gtr, double sig_scale_re, double sig_scale_im,
+                              double pi_scale_re, double pi_scale_im, void* Sig_less, void* Sig_gtr,
+                              void* Pi_less, void* Pi_gtr, void* cuda_stream);
+
+qt_status qt_sse_query(qt_sse_plan_t plan, qt_sse_info* out);
+
+/* Halo exchange (nranks > 1): fills the halo atoms of the local input window from their
+ * owners over NCCL. In-place on the caller's G≷, D≷ buffers (halo part only). */
+qt_status qt_sse_halo_exchange(qt_sse_plan_t plan, void* G_less, void* G_gtr, void* D_less, void* D_gtr,
+                               void* cuda_stream);
+
+void qt_sse_destroy(qt_sse_plan_t plan);   /* NULL-safe; frees workspace (+ NCCL comm) */
+const char* qt_sse_status_string(qt_status s);
+
+/* Host-only (no device needed): algorithmic flop counts for desc + neighbours:
+ * out[0] Σ contraction, out[1] Σ sandwich, out[2] Π sandwich, out[3] Π contraction
+ * (both X, 8 real flops per complex multiply-add, in-window valid-pair work only). */
+qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* neighbors_host, double out[4]);
+
+/* Number of this library's kernel launches issued since load (for bench accounting). */
+uint64_t qt_sse_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

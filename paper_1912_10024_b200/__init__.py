@@ -1,0 +1,164 @@
+"""B200-native electron-phonon scattering self-energy (SSE) hot path of
+Ziogas et al., SC19 (arXiv 1912.10024): Σ≷ (Eq. 3) and Π≷ (Eq. 4).
+
+Thin ctypes binding over the C ABI of libqtsse.so (include/qt_sse.h): argument
+marshalling only — every step of the path runs in the library's sm_100a kernels.
+There is no CPU fallback: importing fails loudly when the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "libqtsse.so"
+
+QT_OK, QT_ERR_INVALID_ARG, QT_ERR_UNSUPPORTED, QT_ERR_OUT_OF_MEMORY, QT_ERR_CUDA, QT_ERR_NCCL, QT_ERR_INTERNAL = range(7)
+QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM = range(3)
+EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
+            "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
+            "qt_sse_launch_count"]
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [("Na", ctypes.c_int64), ("Nb", ctypes.c_int64), ("Norb", ctypes.c_int64), ("N3D", ctypes.c_int64),
+                ("NE", ctypes.c_int64), ("Nw", ctypes.c_int64), ("Nkz", ctypes.c_int64), ("Nqz", ctypes.c_int64),
+                ("shift0", ctypes.c_int32), ("shift_step", ctypes.c_int32), ("precision", ctypes.c_int),
+                ("shard", ctypes.c_int), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("workspace_limit", ctypes.c_size_t)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("a_lo", ctypes.c_int64), ("a_hi", ctypes.c_int64), ("w_lo", ctypes.c_int64),
+                ("w_hi", ctypes.c_int64), ("npairs", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t),
+                ("flops_sigma", ctypes.c_double), ("flops_pi", ctypes.c_double), ("halo_bytes", ctypes.c_double)]
+
+
+class QTError(RuntimeError):
+    pass
+
+
+def _load():
+    if not _LIB_PATH.exists():
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_1912_10024_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(_LIB_PATH))
+    P, D, I = ctypes.c_void_p, ctypes.c_double, ctypes.c_int
+    lib.qt_sse_plan.argtypes = [ctypes.POINTER(Desc), P, P, ctypes.POINTER(P)]
+    lib.qt_sse_sigma.argtypes = [P, P, P, P, P, P, D, D, P, P, P]
+    lib.qt_sse_pi.argtypes = [P, P, P, P, D, D, P, P, P]
+    lib.qt_sse_execute_host.argtypes = [P, P, P, P, P, P, D, D, D, D, P, P, P, P, P]
+    lib.qt_sse_query.argtypes = [P, ctypes.POINTER(Info)]
+    lib.qt_sse_halo_exchange.argtypes = [P, P, P, P, P, P]
+    lib.qt_sse_destroy.argtypes = [P]
+    lib.qt_sse_destroy.restype = None
+    lib.qt_sse_status_string.argtypes = [I]
+    lib.qt_sse_status_string.restype = ctypes.c_char_p
+    lib.qt_sse_count_flops.argtypes = [ctypes.POINTER(Desc), P, ctypes.POINTER(ctypes.c_double)]
+    lib.qt_sse_launch_count.argtypes = []
+    lib.qt_sse_launch_count.restype = ctypes.c_uint64
+    for f in ("qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
+              "qt_sse_halo_exchange", "qt_sse_count_flops"):
+        getattr(lib, f).restype = I
+    return lib
+
+
+lib = _load()
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != QT_OK:
+        raise QTError(f"{what}: {lib.qt_sse_status_string(rc).decode()} (status {rc})")
+
+
+def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0) -> Desc:
+    """Desc from a qtgen.Problem-like object (Na, Nb, Norb, NE, Nw, Nkz, Nqz, shift0, shift_step)."""
+    return Desc(p.Na, p.Nb, p.Norb, 3, p.NE, p.Nw, p.Nkz, p.Nqz, p.shift0, p.shift_step, 0, shard, rank, nranks,
+                None, workspace_limit)
+
+
+def count_flops(p) -> dict:
+    d = make_desc(p)
+    out = (ctypes.c_double * 4)()
+    nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
+    _check(lib.qt_sse_count_flops(ctypes.byref(d), nbr.ctypes.data, out), "qt_sse_count_flops")
+    return dict(sigma_contraction=out[0], sigma_sandwich=out[1], pi_sandwich=out[2], pi_contraction=out[3],
+                total=sum(out))
+
+
+def launch_count() -> int:
+    return int(lib.qt_sse_launch_count())
+
+
+def _ptr(t):
+    return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+class Plan:
+    """Owns a qt_sse_plan_t (workspace, work lists) for one problem shape."""
+
+    def __init__(self, p, stream=None, workspace_limit=0):
+        self.desc = make_desc(p, workspace_limit=workspace_limit)
+        self._nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(lib.qt_sse_plan(ctypes.byref(self.desc), self._nbr.ctypes.data, _stream(stream), ctypes.byref(h)),
+               "qt_sse_plan")
+        self.h = h
+
+    def info(self) -> dict:
+        i = Info()
+        _check(lib.qt_sse_query(self.h, ctypes.byref(i)), "qt_sse_query")
+        return {k: getattr(i, k) for k, _ in Info._fields_}
+
+    def sigma(self, dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, scale=1j, stream=None):
+        _check(lib.qt_sse_sigma(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
+                                scale.real, scale.imag, _ptr(S_less), _ptr(S_gtr), _stream(stream)), "qt_sse_sigma")
+
+    def pi(self, dH, G_less, G_gtr, P_less, P_gtr, scale=-1j, stream=None):
+        _check(lib.qt_sse_pi(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), scale.real, scale.imag, _ptr(P_less),
+                             _ptr(P_gtr), _stream(stream)), "qt_sse_pi")
+
+    def execute_host(self, dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr, sig_scale=1j,
+                     pi_scale=-1j, stream=None):
+        """End-to-end on host buffers (numpy / pinned torch CPU tensors)."""
+        _check(lib.qt_sse_execute_host(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
+                                       sig_scale.real, sig_scale.imag, pi_scale.real, pi_scale.imag, _ptr(S_less),
+                                       _ptr(S_gtr), _ptr(P_less), _ptr(P_gtr), _stream(stream)),
+               "qt_sse_execute_host")
+
+    def close(self):
+        if self.h:
+            lib.qt_sse_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run(p, t: dict, sig_scale=1j, pi_scale=-1j, plan: Plan | None = None):
+    """Σ≷, Π≷ for device inputs t (dict of complex128 CUDA tensors as made by qtgen.dev_inputs)."""
+    import torch
+    own = plan is None
+    plan = Plan(p) if own else plan
+    sh = p.shapes()
+    out = dict(S_less=torch.empty(sh["G"], dtype=torch.complex128, device="cuda"),
+               S_gtr=torch.empty(sh["G"], dtype=torch.complex128, device="cuda"),
+               P_less=torch.empty(sh["D"], dtype=torch.complex128, device="cuda"),
+               P_gtr=torch.empty(sh["D"], dtype=torch.complex128, device="cuda"))
+    plan.sigma(t["dH"], t["G_less"], t["G_gtr"], t["D_less"], t["D_gtr"], out["S_less"], out["S_gtr"], sig_scale)
+    plan.pi(t["dH"], t["G_less"], t["G_gtr"], out["P_less"], out["P_gtr"], pi_scale)
+    if own:
+        torch.cuda.synchronize()
+        plan.close()
+    return out

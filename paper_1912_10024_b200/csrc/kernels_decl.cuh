@@ -1,0 +1,64 @@
+// kernels_decl.cuh — launcher declarations (definitions in kernels_sigma.cu / kernels_pi.cu).
+#pragma once
+#include "common.cuh"
+
+namespace qt {
+
+struct CoefArgs {
+  const double2* DX;
+  const double2* DY;
+  const SigPair* pairs;
+  const SigItem* items;
+  const int32_t* pair_item;
+  double2* coef;
+  int64_t npairs, Nw, Nwin, Nb, Nqz, DWp;
+  int Dmax, shift0;
+};
+
+struct SigmaArgs {
+  const double2* G;
+  const double2* coef;
+  const double2* dH;
+  const SigItem* items;
+  const SigPair* pairs;
+  double2* Sig;
+  double2 scale;
+  int64_t Nwin, Nout, Nb, DWp;
+  int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin;
+};
+
+struct PiWArgs {
+  const double2* GY;
+  const double2* dH;
+  const PiPair* pairs;
+  double2* W;
+  int64_t p0, Nwin, Nb;
+  int NE, Nkz, Norb, NN, nEB;
+};
+
+struct PiCArgs {
+  const double2* GX;
+  const double2* W;
+  const PiItem* items;
+  const PiPair* pairs;
+  double2* Pi;
+  double2 scale;
+  int64_t p0, i0, Nwin, Nout, Nb;
+  int NE, Nkz, Nqz, h, NN, Nw, NWP, shift0, nring, ring_rows;
+};
+
+struct PiSelfArgs {
+  double2* Pi;
+  const int32_t* nbr;
+  int64_t Nout, Nb, Nqz, Nw, a_off;
+};
+
+constexpr int kEB = 4;
+
+cudaError_t launch_sigma_coef(const CoefArgs& a, cudaStream_t st);
+cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
+cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st);
+cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st);
+cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st);
+
+}  // namespace qt

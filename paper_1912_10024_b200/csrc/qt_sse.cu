@@ -1,0 +1,544 @@
+// qt_sse.cu — C ABI of libqtsse.so (include/qt_sse.h): plan validation, work lists,
+// workspace, and the stream-ordered kernel sequence for Σ≷ (Eq. 3) and Π≷ (Eq. 4).
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "qt_sse.h"
+
+#include "kernels_decl.cuh"
+
+using namespace qt;
+
+static std::atomic<uint64_t> g_launches{0};
+
+struct qt_sse_plan_s {
+  qt_sse_desc d{};
+  int64_t NN = 0, h = 0, Dmax = 0, Dwin = 0, DWp = 0, NWP = 0;
+  int64_t a_lo = 0, a_hi = 0, w_lo = 0, w_hi = 0, Nwin = 0, Nout = 0;
+  std::vector<int32_t> nbr;          // global [Na][Nb]
+  std::vector<int32_t> nbr_win;      // window [Nwin][Nb] (local indices, -1 outside/empty)
+  // device
+  int32_t* d_nbr_win = nullptr;
+  SigItem* d_sig_items = nullptr;
+  SigPair* d_sig_pairs = nullptr;
+  int32_t* d_sig_pair_item = nullptr;
+  PiItem* d_pi_items = nullptr;
+  PiPair* d_pi_pairs = nullptr;
+  std::vector<SigItem> sig_items;
+  std::vector<PiItem> pi_items;
+  int64_t n_sig_pairs = 0, n_pi_pairs = 0;
+  // chunks: item ranges [lo, hi) and their pair ranges
+  std::vector<int64_t> sig_chunks, pi_chunks;   // item boundaries
+  double2* ws = nullptr;
+  size_t ws_bytes = 0;
+  int pi_nring = 2;
+  double flops[4] = {0, 0, 0, 0};
+  // host-execute staging
+  void* h_dev = nullptr;
+  size_t h_dev_bytes = 0;
+};
+
+namespace {
+
+qt_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return QT_OK;
+  if (e == cudaErrorMemoryAllocation) return QT_ERR_OUT_OF_MEMORY;
+  return QT_ERR_CUDA;
+}
+#define QT_CUDA(call)                           \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
+#define QT_LAUNCH(call)                         \
+  do {                                          \
+    g_launches.fetch_add(1);                    \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
+
+bool aligned16(const void* p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+qt_status validate_desc(const qt_sse_desc* d) {
+  if (!d) return QT_ERR_INVALID_ARG;
+  if (d->Na <= 0 || d->Nb <= 0 || d->Norb <= 0 || d->NE <= 0 || d->Nw <= 0 || d->Nkz <= 0 || d->Nqz <= 0)
+    return QT_ERR_INVALID_ARG;
+  if (d->N3D != 3 || d->Nkz != d->Nqz) return QT_ERR_INVALID_ARG;
+  if (d->shift0 < 1 || d->shift_step < 1) return QT_ERR_INVALID_ARG;     // S:287 grid alignment
+  if (d->Na > (1LL << 30) || d->Nb > 4096) return QT_ERR_INVALID_ARG;
+  if (d->precision != QT_PREC_FP64) return QT_ERR_UNSUPPORTED;
+  if (d->Norb > 12 || d->shift_step != 1 || d->Nw > 128) return QT_ERR_UNSUPPORTED;
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return QT_ERR_INVALID_ARG;
+  if (d->nranks > 1 && d->shard != QT_SHARD_ATOM) return QT_ERR_UNSUPPORTED;
+  return QT_OK;
+}
+
+// neighbour table: in range, no self, no duplicates, symmetric
+qt_status validate_nbr(const qt_sse_desc* d, const int32_t* nbr) {
+  if (!nbr) return QT_ERR_INVALID_ARG;
+  const int64_t Na = d->Na, Nb = d->Nb;
+  for (int64_t a = 0; a < Na; ++a)
+    for (int64_t s = 0; s < Nb; ++s) {
+      int32_t b = nbr[a * Nb + s];
+      if (b < -1 || b >= Na || b == a) return QT_ERR_INVALID_ARG;
+      if (b < 0) continue;
+      int cnt = 0, back = 0;
+      for (int64_t t = 0; t < Nb; ++t) {
+        if (nbr[a * Nb + t] == b) ++cnt;
+        if (nbr[(int64_t)b * Nb + t] == a) ++back;
+      }
+      if (cnt != 1 || back != 1) return QT_ERR_INVALID_ARG;
+    }
+  return QT_OK;
+}
+
+int64_t rev_slot(const int32_t* nbr, int64_t Nb, int64_t b, int64_t a) {
+  for (int64_t t = 0; t < Nb; ++t)
+    if (nbr[b * Nb + t] == a) return t;
+  return -1;
+}
+
+// valid (E, m) counts: V- = #{E - s_m >= 0}, V+ = #{E + s_m < NE}
+void window_counts(const qt_sse_desc* d, double* vm, double* vp) {
+  double a = 0, b = 0;
+  for (int64_t e = 0; e < d->NE; ++e)
+    for (int64_t m = 0; m < d->Nw; ++m) {
+      int64_t sm = d->shift0 + m * d->shift_step;
+      if (e - sm >= 0) a += 1;
+      if (e + sm < d->NE) b += 1;
+    }
+  *vm = a;
+  *vp = b;
+}
+
+void count_flops(const qt_sse_desc* d, double npairs, double out[4]) {
+  double vm, vp;
+  window_counts(d, &vm, &vp);
+  const double NN = (double)d->Norb * d->Norb, No3 = NN * d->Norb;
+  out[0] = 2.0 * d->Nkz * d->Nqz * npairs * (vm + vp) * 9.0 * NN * 8.0;
+  out[1] = 2.0 * d->Nkz * d->NE * npairs * 12.0 * No3 * 8.0;
+  out[2] = out[1];
+  out[3] = 2.0 * d->Nkz * d->Nqz * npairs * vp * 9.0 * NN * 8.0;
+}
+
+// Atom ranges of a rank for atom sharding: contiguous owned slabs balanced by valid-pair count.
+void owned_range(const qt_sse_desc* d, const int32_t* nbr, int64_t* lo, int64_t* hi) {
+  if (d->nranks == 1) {
+    *lo = 0;
+    *hi = d->Na;
+    return;
+  }
+  std::vector<double> cum(d->Na + 1, 0.0);
+  for (int64_t a = 0; a < d->Na; ++a) {
+    int c = 0;
+    for (int64_t s = 0; s < d->Nb; ++s) c += nbr[a * d->Nb + s] >= 0;
+    cum[a + 1] = cum[a] + c + 1;
+  }
+  auto cut = [&](int r) -> int64_t {
+    double target = cum[d->Na] * r / d->nranks;
+    return (int64_t)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+  };
+  *lo = d->rank == 0 ? 0 : cut(d->rank);
+  *hi = d->rank == d->nranks - 1 ? d->Na : cut(d->rank + 1);
+}
+
+}  // namespace
+
+extern "C" const char* qt_sse_status_string(qt_status s) {
+  switch (s) {
+    case QT_OK: return "ok";
+    case QT_ERR_INVALID_ARG: return "invalid argument";
+    case QT_ERR_UNSUPPORTED: return "unsupported configuration";
+    case QT_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case QT_ERR_CUDA: return "CUDA error";
+    case QT_ERR_NCCL: return "NCCL error";
+    case QT_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+extern "C" uint64_t qt_sse_launch_count(void) { return g_launches.load(); }
+
+extern "C" qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* nbr, double out[4]) {
+  qt_status st = validate_desc(desc);
+  if (st == QT_ERR_UNSUPPORTED) st = QT_OK;   // counting does not depend on kernel limits
+  if (st != QT_OK) return st;
+  if (!out) return QT_ERR_INVALID_ARG;
+  if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
+  int64_t lo, hi;
+  owned_range(desc, nbr, &lo, &hi);
+  double np = 0;
+  for (int64_t a = lo; a < hi; ++a)
+    for (int64_t s = 0; s < desc->Nb; ++s) np += nbr[a * desc->Nb + s] >= 0;
+  count_flops(desc, np, out);
+  return QT_OK;
+}
+
+extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
+  if (!p) return;
+  cudaFree(p->d_nbr_win);
+  cudaFree(p->d_sig_items);
+  cudaFree(p->d_sig_pairs);
+  cudaFree(p->d_sig_pair_item);
+  cudaFree(p->d_pi_items);
+  cudaFree(p->d_pi_pairs);
+  cudaFree(p->ws);
+  cudaFree(p->h_dev);
+  delete p;
+}
+
+template <typename T>
+static qt_status upload(T** dst, const std::vector<T>& v, cudaStream_t st) {
+  if (v.empty()) return QT_OK;
+  QT_CUDA(cudaMalloc(dst, v.size() * sizeof(T)));
+  QT_CUDA(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return QT_OK;
+}
+
+extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, void* stream, qt_sse_plan_t* out) {
+  if (!out) return QT_ERR_INVALID_ARG;
+  *out = nullptr;
+  qt_status st = validate_desc(desc);
+  if (st != QT_OK) return st;
+  if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
+  if (desc->nranks > 1 && desc->nccl_unique_id != nullptr) return QT_ERR_UNSUPPORTED;  // NCCL halo: NEXT
+  cudaStream_t cs = (cudaStream_t)stream;
+  qt_sse_plan_s* p = new (std::nothrow) qt_sse_plan_s();
+  if (!p) return QT_ERR_OUT_OF_MEMORY;
+  p->d = *desc;
+  const qt_sse_desc& d = p->d;
+  p->NN = d.Norb * d.Norb;
+  p->h = d.Nkz / 2;
+  p->Dmax = d.shift0 + (d.Nw - 1) * d.shift_step;
+  p->Dwin = 2 * p->Dmax + 1;
+  p->DWp = (p->Dwin + 3) & ~3LL;
+  p->NWP = (d.Nw + 7) & ~7LL;
+  p->nbr.assign(nbr, nbr + d.Na * d.Nb);
+  owned_range(&d, nbr, &p->a_lo, &p->a_hi);
+  // input window: owned atoms + every neighbour (contiguous hull)
+  p->w_lo = p->a_lo;
+  p->w_hi = p->a_hi;
+  for (int64_t a = p->a_lo; a < p->a_hi; ++a)
+    for (int64_t s = 0; s < d.Nb; ++s) {
+      int32_t b = nbr[a * d.Nb + s];
+      if (b < 0) continue;
+      p->w_lo = std::min<int64_t>(p->w_lo, b);
+      p->w_hi = std::max<int64_t>(p->w_hi, b + 1);
+    }
+  p->Nwin = p->w_hi - p->w_lo;
+  p->Nout = p->a_hi - p->a_lo;
+  p->nbr_win.assign(p->Nwin * d.Nb, -1);
+  for (int64_t a = p->w_lo; a < p->w_hi; ++a)
+    for (int64_t s = 0; s < d.Nb; ++s) {
+      int32_t b = nbr[a * d.Nb + s];
+      if (b >= p->w_lo && b < p->w_hi) p->nbr_win[(a - p->w_lo) * d.Nb + s] = (int32_t)(b - p->w_lo);
+    }
+
+  // Σ work list: source-organized. For each source atom b, its reverse pairs (a,s) with a owned.
+  std::vector<SigPair> sp;
+  std::vector<int32_t> sp_item;
+  for (int64_t b = p->w_lo; b < p->w_hi; ++b) {
+    std::vector<SigPair> mine;
+    for (int64_t r = 0; r < d.Nb; ++r) {
+      int32_t a = nbr[b * d.Nb + r];
+      if (a < 0 || a < p->a_lo || a >= p->a_hi) continue;
+      SigPair q;
+      q.a = (int32_t)(a - p->a_lo);
+      q.a_in = (int32_t)(a - p->w_lo);
+      q.s = (int32_t)rev_slot(nbr, d.Nb, a, b);
+      q.r = (int32_t)r;
+      mine.push_back(q);
+    }
+    for (size_t k = 0; k < mine.size(); k += kMaxPairs) {
+      SigItem it;
+      it.b_in = (int32_t)(b - p->w_lo);
+      it.b = (int32_t)b;
+      it.npair = (int32_t)std::min<size_t>(kMaxPairs, mine.size() - k);
+      it.pair0 = (int32_t)sp.size();
+      for (int t = 0; t < it.npair; ++t) {
+        sp.push_back(mine[k + t]);
+        sp_item.push_back((int32_t)p->sig_items.size());
+      }
+      p->sig_items.push_back(it);
+    }
+  }
+  p->n_sig_pairs = (int64_t)sp.size();
+  // Π work list: destination-organized. For each owned atom a, its valid slots in chunks of 8.
+  std::vector<PiPair> pp;
+  for (int64_t a = p->a_lo; a < p->a_hi; ++a) {
+    std::vector<PiPair> mine;
+    for (int64_t s = 0; s < d.Nb; ++s) {
+      int32_t b = nbr[a * d.Nb + s];
+      if (b < 0) continue;
+      PiPair q;
+      q.s = (int32_t)s;
+      q.b_in = (int32_t)(b - p->w_lo);
+      q.r = (int32_t)rev_slot(nbr, d.Nb, b, a);
+      q.a_in = (int32_t)(a - p->w_lo);
+      mine.push_back(q);
+    }
+    for (size_t k = 0; k < mine.size(); k += kMaxPairs) {
+      PiItem it;
+      it.a_out = (int32_t)(a - p->a_lo);
+      it.a_in = (int32_t)(a - p->w_lo);
+      it.npair = (int32_t)std::min<size_t>(kMaxPairs, mine.size() - k);
+      it.pair0 = (int32_t)pp.size();
+      for (int t = 0; t < it.npair; ++t) pp.push_back(mine[k + t]);
+      p->pi_items.push_back(it);
+    }
+  }
+  p->n_pi_pairs = (int64_t)pp.size();
+  count_flops(&d, (double)p->n_pi_pairs, p->flops);
+
+  // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
+  const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
+  const size_t w_per_pair = (size_t)d.Nkz * d.NE * 9 * p->NN * sizeof(double2);
+  size_t budget = d.workspace_limit;
+  if (budget == 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      qt_sse_destroy(p);
+      return QT_ERR_CUDA;
+    }
+    budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
+  }
+  const size_t need_min = std::max(coef_per_pair, w_per_pair) * kMaxPairs;
+  if (budget < need_min) budget = need_min;
+  const size_t full = std::max(coef_per_pair * p->n_sig_pairs, w_per_pair * p->n_pi_pairs);
+  p->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
+  // chunk item ranges so that each chunk's pairs fit the workspace
+  auto make_chunks = [&](auto& items, size_t per_pair, std::vector<int64_t>& bounds) {
+    const int64_t cap = (int64_t)(p->ws_bytes / per_pair);
+    bounds.clear();
+    bounds.push_back(0);
+    int64_t acc = 0;
+    for (size_t i = 0; i < items.size(); ++i) {
+      if (acc + items[i].npair > cap) {
+        bounds.push_back((int64_t)i);
+        acc = 0;
+      }
+      acc += items[i].npair;
+    }
+    bounds.push_back((int64_t)items.size());
+  };
+  make_chunks(p->sig_items, coef_per_pair, p->sig_chunks);
+  make_chunks(p->pi_items, w_per_pair, p->pi_chunks);
+  const int64_t e_end = d.NE - d.shift0;
+  p->pi_nring = e_end >= 3 ? 2 : 4;
+
+  qt_status s2;
+  if ((s2 = upload(&p->d_nbr_win, p->nbr_win, cs)) != QT_OK || (s2 = upload(&p->d_sig_items, p->sig_items, cs)) != QT_OK ||
+      (s2 = upload(&p->d_sig_pairs, sp, cs)) != QT_OK || (s2 = upload(&p->d_sig_pair_item, sp_item, cs)) != QT_OK ||
+      (s2 = upload(&p->d_pi_items, p->pi_items, cs)) != QT_OK || (s2 = upload(&p->d_pi_pairs, pp, cs)) != QT_OK) {
+    qt_sse_destroy(p);
+    return s2;
+  }
+  if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) {
+    qt_sse_destroy(p);
+    return QT_ERR_OUT_OF_MEMORY;
+  }
+  if (cudaStreamSynchronize(cs) != cudaSuccess) {
+    qt_sse_destroy(p);
+    return QT_ERR_CUDA;
+  }
+  *out = p;
+  return QT_OK;
+}
+
+extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
+  if (!p || !o) return QT_ERR_INVALID_ARG;
+  o->a_lo = p->a_lo;
+  o->a_hi = p->a_hi;
+  o->w_lo = p->w_lo;
+  o->w_hi = p->w_hi;
+  o->npairs = p->n_pi_pairs;
+  o->workspace_bytes = p->ws_bytes;
+  o->flops_sigma = p->flops[0] + p->flops[1];
+  o->flops_pi = p->flops[2] + p->flops[3];
+  o->halo_bytes = 0;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? QT_OK : cuda_status(e);
+}
+
+extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* GL, const void* GG, const void* DL,
+                                  const void* DG, double sre, double sim, void* SL, void* SG, void* stream) {
+  if (!p) return QT_ERR_INVALID_ARG;
+  const void* ins[] = {dH, GL, GG, DL, DG};
+  for (const void* q : ins)
+    if (!aligned16(q)) return QT_ERR_INVALID_ARG;
+  if (!aligned16(SL) || !aligned16(SG) || SL == SG) return QT_ERR_INVALID_ARG;
+  for (const void* q : ins)
+    if (q == SL || q == SG) return QT_ERR_INVALID_ARG;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const qt_sse_desc& d = p->d;
+  const size_t sig_bytes = (size_t)d.Nkz * d.NE * p->Nout * p->NN * sizeof(double2);
+  const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp;
+  for (int X = 0; X < 2; ++X) {
+    void* S = X == 0 ? SL : SG;
+    QT_CUDA(cudaMemsetAsync(S, 0, sig_bytes, cs));
+    for (size_t c = 0; c + 1 < p->sig_chunks.size(); ++c) {
+      const int64_t i0 = p->sig_chunks[c], i1 = p->sig_chunks[c + 1];
+      if (i1 <= i0) continue;
+      const int64_t pp0 = p->sig_items[i0].pair0;
+      const int64_t pp1 = p->sig_items[i1 - 1].pair0 + p->sig_items[i1 - 1].npair;
+      CoefArgs ca;
+      ca.DX = (const double2*)(X == 0 ? DL : DG);
+      ca.DY = (const double2*)(X == 0 ? DG : DL);
+      ca.pairs = p->d_sig_pairs + pp0;
+      ca.items = p->d_sig_items;
+      ca.pair_item = p->d_sig_pair_item + pp0;
+      ca.coef = p->ws;
+      ca.npairs = pp1 - pp0;
+      ca.Nw = d.Nw;
+      ca.Nwin = p->Nwin;
+      ca.Nb = d.Nb;
+      ca.Nqz = d.Nqz;
+      ca.DWp = p->DWp;
+      ca.Dmax = (int)p->Dmax;
+      ca.shift0 = d.shift0;
+      QT_LAUNCH(launch_sigma_coef(ca, cs));
+      SigmaArgs sa;
+      sa.G = (const double2*)(X == 0 ? GL : GG);
+      sa.coef = p->ws - (ptrdiff_t)(pp0 * coef_per_pair);
+      sa.dH = (const double2*)dH;
+      sa.items = p->d_sig_items + i0;
+      sa.pairs = p->d_sig_pairs;
+      sa.Sig = (double2*)S;
+      sa.scale = make_double2(sre, sim);
+      sa.Nwin = p->Nwin;
+      sa.Nout = p->Nout;
+      sa.Nb = d.Nb;
+      sa.DWp = p->DWp;
+      sa.NE = (int)d.NE;
+      sa.Nkz = (int)d.Nkz;
+      sa.Nqz = (int)d.Nqz;
+      sa.h = (int)p->h;
+      sa.Norb = (int)d.Norb;
+      sa.NN = (int)p->NN;
+      sa.Dmax = (int)p->Dmax;
+      sa.Dwin = (int)p->Dwin;
+      QT_LAUNCH(launch_sigma(sa, i1 - i0, cs));
+    }
+  }
+  return QT_OK;
+}
+
+extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, const void* GG, double sre,
+                               double sim, void* PL, void* PG, void* stream) {
+  if (!p) return QT_ERR_INVALID_ARG;
+  const void* ins[] = {dH, GL, GG};
+  for (const void* q : ins)
+    if (!aligned16(q)) return QT_ERR_INVALID_ARG;
+  if (!aligned16(PL) || !aligned16(PG) || PL == PG) return QT_ERR_INVALID_ARG;
+  for (const void* q : ins)
+    if (q == PL || q == PG) return QT_ERR_INVALID_ARG;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const qt_sse_desc& d = p->d;
+  for (int X = 0; X < 2; ++X) {
+    const double2* GX = (const double2*)(X == 0 ? GL : GG);
+    const double2* GY = (const double2*)(X == 0 ? GG : GL);
+    double2* P = (double2*)(X == 0 ? PL : PG);
+    for (size_t c = 0; c + 1 < p->pi_chunks.size(); ++c) {
+      const int64_t i0 = p->pi_chunks[c], i1 = p->pi_chunks[c + 1];
+      if (i1 <= i0) continue;
+      const int64_t pp0 = p->pi_items[i0].pair0;
+      const int64_t pp1 = p->pi_items[i1 - 1].pair0 + p->pi_items[i1 - 1].npair;
+      PiWArgs wa;
+      wa.GY = GY;
+      wa.dH = (const double2*)dH;
+      wa.pairs = p->d_pi_pairs;
+      wa.W = p->ws;
+      wa.p0 = pp0;
+      wa.Nwin = p->Nwin;
+      wa.Nb = d.Nb;
+      wa.NE = (int)d.NE;
+      wa.Nkz = (int)d.Nkz;
+      wa.Norb = (int)d.Norb;
+      wa.NN = (int)p->NN;
+      wa.nEB = (int)((d.NE + kEB - 1) / kEB);
+      QT_LAUNCH(launch_pi_w(wa, pp1 - pp0, cs));
+      PiCArgs ca;
+      ca.GX = GX;
+      ca.W = p->ws;
+      ca.items = p->d_pi_items;
+      ca.pairs = p->d_pi_pairs;
+      ca.Pi = P;
+      ca.scale = make_double2(sre, sim);
+      ca.p0 = pp0;
+      ca.i0 = i0;
+      ca.Nwin = p->Nwin;
+      ca.Nout = p->Nout;
+      ca.Nb = d.Nb;
+      ca.NE = (int)d.NE;
+      ca.Nkz = (int)d.Nkz;
+      ca.Nqz = (int)d.Nqz;
+      ca.h = (int)p->h;
+      ca.NN = (int)p->NN;
+      ca.Nw = (int)d.Nw;
+      ca.NWP = (int)p->NWP;
+      ca.shift0 = d.shift0;
+      ca.nring = p->pi_nring;
+      ca.ring_rows = (int)(p->NWP + 3);
+      QT_LAUNCH(launch_pi_contract(ca, i1 - i0, cs));
+    }
+    PiSelfArgs sa;
+    sa.Pi = P;
+    sa.nbr = p->d_nbr_win;
+    sa.Nout = p->Nout;
+    sa.Nb = d.Nb;
+    sa.Nqz = d.Nqz;
+    sa.Nw = d.Nw;
+    sa.a_off = p->a_lo - p->w_lo;
+    QT_LAUNCH(launch_pi_self(sa, cs));
+  }
+  return QT_OK;
+}
+
+extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const void* GL, const void* GG,
+                                         const void* DL, const void* DG, double ssre, double ssim, double psre,
+                                         double psim, void* SL, void* SG, void* PL, void* PG, void* stream) {
+  if (!p || !dH || !GL || !GG || !DL || !DG || !SL || !SG || !PL || !PG) return QT_ERR_INVALID_ARG;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const qt_sse_desc& d = p->d;
+  const size_t b_dH = (size_t)p->Nwin * d.Nb * 3 * p->NN * 16;
+  const size_t b_G = (size_t)d.Nkz * d.NE * p->Nwin * p->NN * 16;
+  const size_t b_D = (size_t)d.Nqz * d.Nw * p->Nwin * (d.Nb + 1) * 9 * 16;
+  const size_t b_S = (size_t)d.Nkz * d.NE * p->Nout * p->NN * 16;
+  const size_t b_P = (size_t)d.Nqz * d.Nw * p->Nout * (d.Nb + 1) * 9 * 16;
+  const size_t total = b_dH + 2 * b_G + 2 * b_D + 2 * b_S + 2 * b_P;
+  if (p->h_dev_bytes < total) {
+    cudaFree(p->h_dev);
+    p->h_dev = nullptr;
+    p->h_dev_bytes = 0;
+    QT_CUDA(cudaMalloc(&p->h_dev, total));
+    p->h_dev_bytes = total;
+  }
+  char* base = (char*)p->h_dev;
+  char *ddH = base, *dGL = ddH + b_dH, *dGG = dGL + b_G, *dDL = dGG + b_G, *dDG = dDL + b_D;
+  char *dSL = dDG + b_D, *dSG = dSL + b_S, *dPL = dSG + b_S, *dPG = dPL + b_P;
+  QT_CUDA(cudaMemcpyAsync(ddH, dH, b_dH, cudaMemcpyHostToDevice, cs));
+  QT_CUDA(cudaMemcpyAsync(dGL, GL, b_G, cudaMemcpyHostToDevice, cs));
+  QT_CUDA(cudaMemcpyAsync(dGG, GG, b_G, cudaMemcpyHostToDevice, cs));
+  QT_CUDA(cudaMemcpyAsync(dDL, DL, b_D, cudaMemcpyHostToDevice, cs));
+  QT_CUDA(cudaMemcpyAsync(dDG, DG, b_D, cudaMemcpyHostToDevice, cs));
+  qt_status st = qt_sse_sigma(p, ddH, dGL, dGG, dDL, dDG, ssre, ssim, dSL, dSG, stream);
+  if (st != QT_OK) return st;
+  st = qt_sse_pi(p, ddH, dGL, dGG, psre, psim, dPL, dPG, stream);
+  if (st != QT_OK) return st;
+  QT_CUDA(cudaMemcpyAsync(SL, dSL, b_S, cudaMemcpyDeviceToHost, cs));
+  QT_CUDA(cudaMemcpyAsync(SG, dSG, b_S, cudaMemcpyDeviceToHost, cs));
+  QT_CUDA(cudaMemcpyAsync(PL, dPL, b_P, cudaMemcpyDeviceToHost, cs));
+  QT_CUDA(cudaMemcpyAsync(PG, dPG, b_P, cudaMemcpyDeviceToHost, cs));
+  QT_CUDA(cudaStreamSynchronize(cs));
+  return QT_OK;
+}
+
+extern "C" qt_status qt_sse_halo_exchange(qt_sse_plan_t p, void*, void*, void*, void*, void*) {
+  if (!p) return QT_ERR_INVALID_ARG;
+  if (p->d.nranks == 1) return QT_OK;
+  return QT_ERR_UNSUPPORTED;
+}
