@@ -1,0 +1,347 @@
+"""Benchmark: SSE Σ≷+Π≷ FP64 Tflop/s and % of the FP64 roofline on B200 (BASELINE.json `metric`).
+
+One step = one pass of the whole hot path — Σ^<, Σ^> (Eq. 3) and Π^<, Π^> (Eq. 4) — over the
+workload (default cfg3: Si FinFET slice, 4,864 atoms, Nb=34, Norb=10, NE=176, Nω=70, Nkz=Nqz=3).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU). Ranks own contiguous atom slabs (atom sharding,
+the paper's Ta tiling) with their neighbour halo resident in HBM; every rank
+computes Σ/Π for its own atoms, so the timed region has no data-path collective. `value` is the
+total algorithmic flops of all ranks ÷ the max over ranks of the device time (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 sustained, profiles/r01_fp64_peak.jsonl (nominal 37.2)
+METRIC = "SSE Σ+Π FP64 Tflop/s and % of FP64 roofline at 1/2/4/8 B200 vs CPU oracle"
+THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks sampler (nvidia-smi during the timed region)
+class Clocks:
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 4:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            try:
+                bits = int(r[3], 16)
+            except ValueError:
+                continue
+            for b, n in THROTTLE_BITS.items():
+                if bits & b and n != "gpu_idle":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle sample (cpu_baseline / --impl reference)
+def block_flops(p, sig_blocks, pi_blocks):
+    """Algorithmic flops (F_alg units) of sampled Σ blocks (X,kz,e,a) and Π blocks (X,qz,m,a,slot>0)."""
+    NN, No3 = p.Norb ** 2, p.Norb ** 3
+    deg = (p.nbr >= 0).sum(1)
+    sm = p.shift0 + np.arange(p.Nw) * p.shift_step
+    f = 0.0
+    for _, _, e, a in sig_blocks:
+        valid = int(((e - sm) >= 0).sum() + ((e + sm) < p.NE).sum())
+        f += deg[a] * (p.Nqz * valid * 9 * NN + 12 * No3) * 8.0
+    vplus = np.array([int(((np.arange(p.NE) + s) < p.NE).sum()) for s in sm])
+    for _, _, m, a, slot in pi_blocks:
+        f += (p.Nkz * vplus[m] * 9 * NN + p.Nkz * p.NE * 12 * No3 / (p.Nqz * p.Nw)) * 8.0
+    return f
+
+
+def oracle_sample(p, host, n_sig, n_pi, seed):
+    import oracle
+    rng = np.random.default_rng(seed)
+    sb = np.stack([rng.integers(0, 2, n_sig), rng.integers(0, p.Nkz, n_sig), rng.integers(0, p.NE, n_sig),
+                   rng.integers(0, p.Na, n_sig)], 1)
+    pa = rng.integers(0, p.Na, n_pi)
+    pslot = np.array([1 + rng.choice(np.nonzero(p.nbr[a] >= 0)[0]) if (p.nbr[a] >= 0).any() else 0 for a in pa])
+    pb = np.stack([rng.integers(0, 2, n_pi), rng.integers(0, p.Nqz, n_pi), rng.integers(0, p.Nw, n_pi), pa, pslot], 1)
+    pb = pb[pb[:, 4] > 0]
+    t0 = time.perf_counter()
+    oracle.sigma_blocks(p, host, sb)
+    oracle.pi_blocks(p, host, pb)
+    dt = time.perf_counter() - t0
+    return block_flops(p, sb, pb), dt, len(sb), len(pb)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def calibrated_oracle(p, host, target_s, seed=7):
+    """Oracle timed on a bounded sample sized for ~target_s seconds (as it stands: no tuning)."""
+    n_sig, n_pi = 2 * host_cores(), 8 * host_cores()
+    f, dt, ns, npi = oracle_sample(p, host, n_sig, n_pi, seed)
+    scale = max(1.0, min(64.0, target_s / max(dt, 1e-3)))
+    if dt < target_s / 2:
+        f, dt, ns, npi = oracle_sample(p, host, int(n_sig * scale), int(n_pi * scale), seed + 1)
+    return f, dt, ns, npi
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-oracle sample time")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import qtgen
+    p = qtgen.problem(args.config)
+
+    if args.impl == "reference":
+        return run_reference(args, p, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1912_10024_b200 as qt
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # ---- plan (atom shard of this rank) and resident inputs for its window
+    total_mem = torch.cuda.get_device_properties(local).total_memory
+    desc_kw = dict(rank=rank, nranks=world, shard=qt.QT_SHARD_ATOM if world > 1 else qt.QT_SHARD_NONE,
+                   workspace_limit=int(min(48 << 30, 0.3 * total_mem)))
+    plan = qt.Plan(p, stream=stream, **desc_kw)
+    info = plan.info()
+    w_lo, w_hi, a_lo, a_hi = info["w_lo"], info["w_hi"], info["a_lo"], info["a_hi"]
+    nwin, nout = w_hi - w_lo, a_hi - a_lo
+    NN = p.Norb ** 2
+    c128 = torch.complex128
+    nbr_dev = torch.from_numpy(p.nbr).to(dev)
+    G_less = torch.empty((p.Nkz, p.NE, nwin, p.Norb, p.Norb), dtype=c128, device=dev)
+    G_gtr = torch.empty_like(G_less)
+    D_less = torch.empty((p.Nqz, p.Nw, nwin, p.Nb + 1, 3, 3), dtype=c128, device=dev)
+    D_gtr = torch.empty_like(D_less)
+    dH_full = torch.empty((p.Na, p.Nb, 3, p.Norb, p.Norb), dtype=c128, device=dev)
+    qtgen.dev_G(p, qtgen.ID_GL, G_less, a_lo=w_lo, a_hi=w_hi)
+    qtgen.dev_G(p, qtgen.ID_GG, G_gtr, a_lo=w_lo, a_hi=w_hi)
+    qtgen.dev_D(p, qtgen.ID_DL, D_less, nbr_dev, a_lo=w_lo, a_hi=w_hi)
+    qtgen.dev_D(p, qtgen.ID_DG, D_gtr, nbr_dev, a_lo=w_lo, a_hi=w_hi)
+    qtgen.dev_dH(p, dH_full, nbr_dev)
+    dH = dH_full[w_lo:w_hi].contiguous()
+    del dH_full
+    S_less = torch.empty((p.Nkz, p.NE, nout, p.Norb, p.Norb), dtype=c128, device=dev)
+    S_gtr = torch.empty_like(S_less)
+    P_less = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
+    P_gtr = torch.empty_like(P_less)
+    torch.cuda.synchronize()
+    in_bytes = sum(t.numel() * 16 for t in (G_less, G_gtr, D_less, D_gtr, dH))
+    out_bytes = sum(t.numel() * 16 for t in (S_less, S_gtr, P_less, P_gtr))
+
+    def step():
+        plan.sigma(dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, 1j, stream)
+        plan.pi(dH, G_less, G_gtr, P_less, P_gtr, -1j, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the launching stream
+    clocks = Clocks(local)
+    plan.timing(True)
+    plan.timing_read()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    n0 = qt.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = qt.launch_count() - n0
+    ms_total = ev0.elapsed_time(ev1)
+    kern = plan.timing_read()
+    plan.timing(False)
+
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    f_local = torch.tensor([info["flops_sigma"] + info["flops_pi"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(f_local, op=dist.ReduceOp.SUM)
+    ms_step = float(t_local.item()) / args.steps
+    flops_step = float(f_local.item())
+    value = flops_step / (ms_step * 1e-3) / 1e12
+
+    # ---- roofline: dominant kernel (k_sigma), algorithmic flops per launch ÷ its average launch time
+    f = qt.count_flops(p) if world == 1 else None
+    sig_ms, sig_n = kern["k_sigma"]
+    sig_flops_step = info["flops_sigma"]                 # k_sigma fuses the Σ contraction + sandwich (both X)
+    achieved = (sig_flops_step * args.steps / max(sig_n, 1)) / (sig_ms / max(sig_n, 1) * 1e-3) / 1e12
+    prof_traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        prof_traffic = json.loads(tf.read_text()).get(args.config, {}).get("k_sigma")
+    roofline = {"bound": "tensor", "kernel": "k_sigma (DMMA.8x8x4, FP64)", "achieved": round(achieved, 3),
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
+                "traffic": prof_traffic,
+                "peak_source": "measured FP64 DMMA m8n8k4 sustained (profiles/r01_fp64_peak.jsonl); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "share_of_step": round(sig_ms / ms_total, 4),
+                "kernels_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kern.items()}}
+
+    # ---- e2e through the public C-ABI call on pinned HOST buffers (H2D + compute + D2H every step)
+    e2e = None
+    if not args.no_e2e:
+        hin = {k: torch.empty(v.shape, dtype=c128, pin_memory=True)
+               for k, v in (("dH", dH), ("G_less", G_less), ("G_gtr", G_gtr), ("D_less", D_less), ("D_gtr", D_gtr))}
+        for k, v in (("dH", dH), ("G_less", G_less), ("G_gtr", G_gtr), ("D_less", D_less), ("D_gtr", D_gtr)):
+            hin[k].copy_(v)
+        # free the device-resident copies: execute_host stages through plan-owned buffers
+        del G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr
+        torch.cuda.empty_cache()
+        hout = {k: torch.empty(s, dtype=c128, pin_memory=True) for k, s in
+                (("S_less", (p.Nkz, p.NE, nout, p.Norb, p.Norb)), ("S_gtr", (p.Nkz, p.NE, nout, p.Norb, p.Norb)),
+                 ("P_less", (p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3)),
+                 ("P_gtr", (p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3)))}
+        args_h = (hin["dH"], hin["G_less"], hin["G_gtr"], hin["D_less"], hin["D_gtr"],
+                  hout["S_less"], hout["S_gtr"], hout["P_less"], hout["P_gtr"])
+        plan.execute_host(*args_h, stream=stream)       # warm (allocates the plan's staging buffers)
+        e2e_steps = max(1, min(args.steps, 2))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            plan.execute_host(*args_h, stream=stream)
+        t_e2e = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(flops_step / float(t_e2e.item()) / 1e12, 3), "unit": "Tflop/s",
+               "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(out_bytes), "steps": e2e_steps,
+               "api": "qt_sse_execute_host (pinned host buffers)"}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only), bounded sample of the same workload
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        host = hin if e2e is not None else None
+        if host is None:
+            host = qtgen.host_inputs(p)
+        hnp = {k: (v.numpy() if hasattr(v, "numpy") else v) for k, v in host.items()}
+        os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+        fs, dt, ns, npi = calibrated_oracle(p, hnp, args.cpu_seconds)
+        cpu = {"value": round(fs / dt / 1e12, 6), "unit": "Tflop/s", "cores": host_cores(), "kind": "oracle",
+               "sample": f"{ns} Σ blocks + {npi} Π blocks of {args.config} (random (X,kz,E,a) / (X,qz,m,a,s)), "
+                         f"{dt:.1f} s, F_alg of the sampled blocks ÷ wall time",
+               "seconds": round(dt, 2)}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 3), "unit": "Tflop/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
+                                      f"NE={p.NE}, Nω={p.Nw}, Nkz=Nqz={p.Nkz}",
+                          "flops_per_step": flops_step, "parallelism": f"atom-shard x{world}",
+                          "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (in_bytes / 1e9)},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+               "clocks": clk, "pct_fp64_peak": round(value / (FP64_PEAK_TFLOPS * world) * 100, 2)}
+        print(json.dumps(out), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, p, rank, world):
+    """--impl reference: the CPU oracle as it stands on the host cores, bounded sample per step."""
+    if rank != 0:
+        return
+    import qtgen
+    host = qtgen.host_inputs(p)
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    _, dt0, ns0, npi0 = oracle_sample(p, host, 2 * host_cores(), 8 * host_cores(), 1)
+    k = max(1.0, per_step / max(dt0, 1e-3))
+    ns, npi = int(2 * host_cores() * k), int(8 * host_cores() * k)
+    for w in range(args.warmup):
+        oracle_sample(p, host, max(1, ns // 4), max(1, npi // 4), 100 + w)
+    fl, tt, nsig, npis = 0.0, 0.0, 0, 0
+    for s in range(args.steps):
+        f, dt, a, b = oracle_sample(p, host, ns, npi, 200 + s)
+        fl, tt, nsig, npis = fl + f, tt + dt, nsig + a, npis + b
+    v = fl / tt / 1e12
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "Tflop/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tt / args.steps * 1e3, 1),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
+                                  f"NE={p.NE}, Nω={p.Nw}, Nkz=Nqz={p.Nkz}"},
+           "cpu_baseline": {"value": round(v, 6), "unit": "Tflop/s", "kind": "oracle", "cores": host_cores(),
+                            "sample": f"per step {ns} Σ blocks + ~{npi} Π blocks (random); "
+                                      f"{nsig} + {npis} blocks in {tt:.1f} s total"},
+           "e2e": {"value": round(v, 6), "unit": "Tflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

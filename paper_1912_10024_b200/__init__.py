@@ -19,7 +19,8 @@ QT_OK, QT_ERR_INVALID_ARG, QT_ERR_UNSUPPORTED, QT_ERR_OUT_OF_MEMORY, QT_ERR_CUDA
 QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM = range(3)
 EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
-            "qt_sse_launch_count"]
+            "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read"]
+KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self"]
 
 
 class Desc(ctypes.Structure):
@@ -59,18 +60,34 @@ def _load():
     lib.qt_sse_count_flops.argtypes = [ctypes.POINTER(Desc), P, ctypes.POINTER(ctypes.c_double)]
     lib.qt_sse_launch_count.argtypes = []
     lib.qt_sse_launch_count.restype = ctypes.c_uint64
+    lib.qt_sse_timing_enable.argtypes = [P, I]
+    lib.qt_sse_timing_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     for f in ("qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
-              "qt_sse_halo_exchange", "qt_sse_count_flops"):
+              "qt_sse_halo_exchange", "qt_sse_count_flops", "qt_sse_timing_enable", "qt_sse_timing_read"):
         getattr(lib, f).restype = I
     return lib
 
 
-lib = _load()
+_lib = None
+
+
+def _get_lib():
+    """Load libqtsse.so on first use (so the in-tree build can run before it exists)."""
+    global _lib
+    if _lib is None:
+        _lib = _load()
+    return _lib
+
+
+def __getattr__(name):   # PEP 562: `paper_1912_10024_b200.lib` is the loaded C library
+    if name == "lib":
+        return _get_lib()
+    raise AttributeError(name)
 
 
 def _check(rc: int, what: str) -> None:
     if rc != QT_OK:
-        raise QTError(f"{what}: {lib.qt_sse_status_string(rc).decode()} (status {rc})")
+        raise QTError(f"{what}: {_get_lib().qt_sse_status_string(rc).decode()} (status {rc})")
 
 
 def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0) -> Desc:
@@ -83,13 +100,13 @@ def count_flops(p) -> dict:
     d = make_desc(p)
     out = (ctypes.c_double * 4)()
     nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
-    _check(lib.qt_sse_count_flops(ctypes.byref(d), nbr.ctypes.data, out), "qt_sse_count_flops")
+    _check(_get_lib().qt_sse_count_flops(ctypes.byref(d), nbr.ctypes.data, out), "qt_sse_count_flops")
     return dict(sigma_contraction=out[0], sigma_sandwich=out[1], pi_sandwich=out[2], pi_contraction=out[3],
                 total=sum(out))
 
 
 def launch_count() -> int:
-    return int(lib.qt_sse_launch_count())
+    return int(_get_lib().qt_sse_launch_count())
 
 
 def _ptr(t):
@@ -105,38 +122,48 @@ def _stream(stream):
 class Plan:
     """Owns a qt_sse_plan_t (workspace, work lists) for one problem shape."""
 
-    def __init__(self, p, stream=None, workspace_limit=0):
-        self.desc = make_desc(p, workspace_limit=workspace_limit)
+    def __init__(self, p, stream=None, workspace_limit=0, rank=0, nranks=1, shard=QT_SHARD_NONE):
+        self.desc = make_desc(p, rank=rank, nranks=nranks, shard=shard, workspace_limit=workspace_limit)
         self._nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
         h = ctypes.c_void_p()
-        _check(lib.qt_sse_plan(ctypes.byref(self.desc), self._nbr.ctypes.data, _stream(stream), ctypes.byref(h)),
+        _check(_get_lib().qt_sse_plan(ctypes.byref(self.desc), self._nbr.ctypes.data, _stream(stream), ctypes.byref(h)),
                "qt_sse_plan")
         self.h = h
 
     def info(self) -> dict:
         i = Info()
-        _check(lib.qt_sse_query(self.h, ctypes.byref(i)), "qt_sse_query")
+        _check(_get_lib().qt_sse_query(self.h, ctypes.byref(i)), "qt_sse_query")
         return {k: getattr(i, k) for k, _ in Info._fields_}
 
     def sigma(self, dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, scale=1j, stream=None):
-        _check(lib.qt_sse_sigma(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
+        _check(_get_lib().qt_sse_sigma(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
                                 scale.real, scale.imag, _ptr(S_less), _ptr(S_gtr), _stream(stream)), "qt_sse_sigma")
 
     def pi(self, dH, G_less, G_gtr, P_less, P_gtr, scale=-1j, stream=None):
-        _check(lib.qt_sse_pi(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), scale.real, scale.imag, _ptr(P_less),
+        _check(_get_lib().qt_sse_pi(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), scale.real, scale.imag, _ptr(P_less),
                              _ptr(P_gtr), _stream(stream)), "qt_sse_pi")
 
     def execute_host(self, dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr, sig_scale=1j,
                      pi_scale=-1j, stream=None):
         """End-to-end on host buffers (numpy / pinned torch CPU tensors)."""
-        _check(lib.qt_sse_execute_host(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
+        _check(_get_lib().qt_sse_execute_host(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
                                        sig_scale.real, sig_scale.imag, pi_scale.real, pi_scale.imag, _ptr(S_less),
                                        _ptr(S_gtr), _ptr(P_less), _ptr(P_gtr), _stream(stream)),
                "qt_sse_execute_host")
 
+    def timing(self, enable: bool = True):
+        _check(_get_lib().qt_sse_timing_enable(self.h, int(enable)), "qt_sse_timing_enable")
+
+    def timing_read(self) -> dict:
+        """{kernel: (ms_total, launches)} since the last read (synchronizes the recorded events)."""
+        ms = (ctypes.c_double * len(KERNEL_KINDS))()
+        n = (ctypes.c_int64 * len(KERNEL_KINDS))()
+        _check(_get_lib().qt_sse_timing_read(self.h, ms, n), "qt_sse_timing_read")
+        return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_KINDS)}
+
     def close(self):
         if self.h:
-            lib.qt_sse_destroy(self.h)
+            _get_lib().qt_sse_destroy(self.h)
             self.h = None
 
     def __del__(self):

@@ -206,6 +206,10 @@ cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st)
   int64_t nblk = npairs_chunk * a.Nkz * a.nEB;
   if (nblk == 0) return cudaSuccess;
   size_t smem = (size_t)(kEB * a.NN + 6 * a.NN + kEB * 3 * a.NN) * sizeof(double2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_pi_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   k_pi_w<<<(unsigned)nblk, 256, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -40,6 +40,12 @@ struct qt_sse_plan_s {
   // host-execute staging
   void* h_dev = nullptr;
   size_t h_dev_bytes = 0;
+  // per-kernel timing (qt_sse_timing_*)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -54,11 +60,29 @@ qt_status cuda_status(cudaError_t e) {
     cudaError_t e_ = (call);                    \
     if (e_ != cudaSuccess) return cuda_status(e_); \
   } while (0)
-#define QT_LAUNCH(call)                         \
-  do {                                          \
-    g_launches.fetch_add(1);                    \
-    cudaError_t e_ = (call);                    \
-    if (e_ != cudaSuccess) return cuda_status(e_); \
+cudaEvent_t take_event(qt_sse_plan_s* p) {
+  if (p->ev_used == p->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    p->ev_pool.push_back(e);
+  }
+  return p->ev_pool[p->ev_used++];
+}
+#define QT_LAUNCH(kind, call)                                            \
+  do {                                                                   \
+    g_launches.fetch_add(1);                                             \
+    cudaEvent_t ea_ = nullptr, eb_ = nullptr;                            \
+    if (p->timing) {                                                     \
+      ea_ = take_event(p);                                               \
+      eb_ = take_event(p);                                               \
+      if (ea_ && eb_) cudaEventRecord(ea_, cs);                          \
+    }                                                                    \
+    cudaError_t e_ = (call);                                             \
+    if (e_ != cudaSuccess) return cuda_status(e_);                       \
+    if (ea_ && eb_) {                                                    \
+      cudaEventRecord(eb_, cs);                                          \
+      p->recs.push_back({kind, ea_, eb_});                               \
+    }                                                                    \
   } while (0)
 
 bool aligned16(const void* p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -188,6 +212,7 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_pi_pairs);
   cudaFree(p->ws);
   cudaFree(p->h_dev);
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
 }
 
@@ -400,7 +425,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       ca.DWp = p->DWp;
       ca.Dmax = (int)p->Dmax;
       ca.shift0 = d.shift0;
-      QT_LAUNCH(launch_sigma_coef(ca, cs));
+      QT_LAUNCH(QT_K_SIGMA_COEF, launch_sigma_coef(ca, cs));
       SigmaArgs sa;
       sa.G = (const double2*)(X == 0 ? GL : GG);
       sa.coef = p->ws - (ptrdiff_t)(pp0 * coef_per_pair);
@@ -421,7 +446,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.NN = (int)p->NN;
       sa.Dmax = (int)p->Dmax;
       sa.Dwin = (int)p->Dwin;
-      QT_LAUNCH(launch_sigma(sa, i1 - i0, cs));
+      QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
     }
   }
   return QT_OK;
@@ -460,7 +485,7 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       wa.Norb = (int)d.Norb;
       wa.NN = (int)p->NN;
       wa.nEB = (int)((d.NE + kEB - 1) / kEB);
-      QT_LAUNCH(launch_pi_w(wa, pp1 - pp0, cs));
+      QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, pp1 - pp0, cs));
       PiCArgs ca;
       ca.GX = GX;
       ca.W = p->ws;
@@ -483,7 +508,7 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       ca.shift0 = d.shift0;
       ca.nring = p->pi_nring;
       ca.ring_rows = (int)(p->NWP + 3);
-      QT_LAUNCH(launch_pi_contract(ca, i1 - i0, cs));
+      QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
     }
     PiSelfArgs sa;
     sa.Pi = P;
@@ -493,7 +518,7 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
     sa.Nqz = d.Nqz;
     sa.Nw = d.Nw;
     sa.a_off = p->a_lo - p->w_lo;
-    QT_LAUNCH(launch_pi_self(sa, cs));
+    QT_LAUNCH(QT_K_PI_SELF, launch_pi_self(sa, cs));
   }
   return QT_OK;
 }
@@ -541,4 +566,28 @@ extern "C" qt_status qt_sse_halo_exchange(qt_sse_plan_t p, void*, void*, void*, 
   if (!p) return QT_ERR_INVALID_ARG;
   if (p->d.nranks == 1) return QT_OK;
   return QT_ERR_UNSUPPORTED;
+}
+
+extern "C" qt_status qt_sse_timing_enable(qt_sse_plan_t p, int enable) {
+  if (!p) return QT_ERR_INVALID_ARG;
+  p->timing = enable != 0;
+  return QT_OK;
+}
+
+extern "C" qt_status qt_sse_timing_read(qt_sse_plan_t p, double ms[QT_K_NKINDS], int64_t launches[QT_K_NKINDS]) {
+  if (!p || !ms || !launches) return QT_ERR_INVALID_ARG;
+  for (int k = 0; k < QT_K_NKINDS; ++k) {
+    ms[k] = 0.0;
+    launches[k] = 0;
+  }
+  for (const auto& r : p->recs) {
+    QT_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    QT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.kind] += t;
+    launches[r.kind] += 1;
+  }
+  p->recs.clear();
+  p->ev_used = 0;
+  return QT_OK;
 }
