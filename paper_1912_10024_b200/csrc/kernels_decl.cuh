@@ -17,13 +17,13 @@ struct CoefArgs {
 
 struct SigmaArgs {
   const double2* G;
-  const double2* coef;
+  const double2* coef;   // coefficient table of the current chunk: pair index p - cp0
   const double2* dH;
   const SigItem* items;
   const SigPair* pairs;
   double2* Sig;
   double2 scale;
-  int64_t Nwin, Nout, Nb, DWp;
+  int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk;
   int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin;
 };
 
@@ -57,6 +57,7 @@ constexpr int kEB = 4;
 
 cudaError_t launch_sigma_coef(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
+cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st);
 cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st);

@@ -61,10 +61,11 @@ struct SigmaCfg {
   static constexpr size_t SMEM = (size_t)(REGION1 + VS) * sizeof(double2);
 };
 
+// cp.async variant, used for Norb = 11, 12 (Norb² rows too wide for one TMA box; see kernels_sigma_tma.cu).
 // One CTA = (item: source atom b + ≤8 pairs, kz, E). 9 warps; warp w owns m-fragment w (rows 8w..8w+7)
 // and all NF n-fragments.
 template <int NF>
-__global__ void __launch_bounds__(kThreads, 1) k_sigma(SigmaArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) k_sigma_cp(SigmaArgs A) {
   using C = SigmaCfg<NF>;
   extern __shared__ __align__(16) double2 smem[];
   double2* Gs = smem;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sigma(SigmaArgs A) {
     for (int idx = threadIdx.x; idx < 9 * P * kc; idx += kThreads) {
       const int row = idx / kc, kk = idx - row * kc;
       const int t = row / 9, ij = row - 9 * t;
-      const double2* src = A.coef + (((int64_t)(item.pair0 + t) * 9 + ij) * A.Nqz + q) * A.DWp + dd0 + kk;
+      const double2* src = A.coef + (((int64_t)(item.pair0 - A.cp0 + t) * 9 + ij) * A.Nqz + q) * A.DWp + dd0 + kk;
       cp_async16(cs + row * C::KCP + kk, src, true);
     }
   };
@@ -214,27 +215,19 @@ static cudaError_t launch_sigma_nf(const SigmaArgs& a, int64_t nitems, cudaStrea
   using C = SigmaCfg<NF>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sigma<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_sigma_cp<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   int64_t nblk = nitems * a.NE * a.Nkz;
   if (nblk == 0) return cudaSuccess;
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  k_sigma<NF><<<(unsigned)nblk, kThreads, C::SMEM, st>>>(a);
+  k_sigma_cp<NF><<<(unsigned)nblk, kThreads, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
+cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
   switch ((a.NN + 7) / 8) {
-    case 1: return launch_sigma_nf<1>(a, nitems, st);
-    case 2: return launch_sigma_nf<2>(a, nitems, st);
-    case 4: return launch_sigma_nf<4>(a, nitems, st);
-    case 5: return launch_sigma_nf<5>(a, nitems, st);
-    case 7: return launch_sigma_nf<7>(a, nitems, st);
-    case 8: return launch_sigma_nf<8>(a, nitems, st);
-    case 11: return launch_sigma_nf<11>(a, nitems, st);
-    case 13: return launch_sigma_nf<13>(a, nitems, st);
     case 16: return launch_sigma_nf<16>(a, nitems, st);
     case 18: return launch_sigma_nf<18>(a, nitems, st);
     default: return cudaErrorInvalidValue;

@@ -428,7 +428,9 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       QT_LAUNCH(QT_K_SIGMA_COEF, launch_sigma_coef(ca, cs));
       SigmaArgs sa;
       sa.G = (const double2*)(X == 0 ? GL : GG);
-      sa.coef = p->ws - (ptrdiff_t)(pp0 * coef_per_pair);
+      sa.coef = p->ws;
+      sa.cp0 = pp0;
+      sa.npairs_chunk = pp1 - pp0;
       sa.dH = (const double2*)dH;
       sa.items = p->d_sig_items + i0;
       sa.pairs = p->d_sig_pairs;
