@@ -31,8 +31,10 @@ struct PiWArgs {
   const double2* GY;
   const double2* dH;
   const PiPair* pairs;
-  double2* W;
-  int64_t p0, Nwin, Nb;
+  const PiItem* items;
+  const int32_t* pair_item;   // pair -> item
+  double2* W;                 // [item - i0][Nkz][NE][72 rows (t,ij)][NN]
+  int64_t p0, i0, Nwin, Nb;
   int NE, Nkz, Norb, NN, nEB;
 };
 
@@ -43,8 +45,8 @@ struct PiCArgs {
   const PiPair* pairs;
   double2* Pi;
   double2 scale;
-  int64_t p0, i0, Nwin, Nout, Nb;
-  int NE, Nkz, Nqz, h, NN, Nw, NWP, shift0, nring, ring_rows;
+  int64_t i0, nitems, Nwin, Nout, Nb;
+  int NE, Nkz, Nqz, h, NN, Nw, NWP, shift0;
 };
 
 struct PiSelfArgs {

@@ -9,6 +9,7 @@
 // window (rows E+s_m), held in a shared-memory ring buffer that advances one row per E.
 // Π_{a,0} = Σ_s Π_{a,s+1} (R9) is formed by k_pi_self.
 #include "kernels_decl.cuh"
+#include "tma.cuh"
 
 namespace qt {
 
@@ -23,8 +24,11 @@ __global__ void __launch_bounds__(256) k_pi_w(PiWArgs A) {
   const int64_t blk = blockIdx.x;
   const int eb = (int)(blk % A.nEB);
   const int kz = (int)((blk / A.nEB) % A.Nkz);
-  const int64_t pl = blk / ((int64_t)A.nEB * A.Nkz);
-  const PiPair pr = A.pairs[A.p0 + pl];
+  const int64_t p = A.p0 + blk / ((int64_t)A.nEB * A.Nkz);
+  const PiPair pr = A.pairs[p];
+  const int item = A.pair_item[p];
+  const int t = (int)(p - A.items[item].pair0);
+  const int64_t il = item - A.i0;
   const int e0 = eb * kEB;
   const int ne = min(kEB, A.NE - e0);
   for (int idx = threadIdx.x; idx < kEB * NN; idx += blockDim.x) {
@@ -46,137 +50,253 @@ __global__ void __launch_bounds__(256) k_pi_w(PiWArgs A) {
     T[idx] = s;
   }
   __syncthreads();
-  double2* out = A.W + (((pl * A.Nkz + kz) * A.NE) + e0) * 9 * NN;
+  double2* out = A.W + (((il * A.Nkz + kz) * A.NE) + e0) * kRows * NN + t * 9 * NN;
   for (int idx = threadIdx.x; idx < ne * 9 * NN; idx += blockDim.x) {
     const int e = idx / (9 * NN), rem = idx - e * 9 * NN, ij = rem / NN, xy = rem - ij * NN;
     const int i = ij / 3, j = ij - 3 * i, x = xy / No, y = xy - x * No;
     double2 s = make_double2(0.0, 0.0);
     const double2* hl = Hl + j * NN + y * No;
-    const double2* t = T + (e * 3 + i) * NN + x;
-    for (int q = 0; q < No; ++q) cfma(s, hl[q], t[q * No]);
-    out[idx] = s;
+    const double2* tt = T + (e * 3 + i) * NN + x;
+    for (int q = 0; q < No; ++q) cfma(s, hl[q], tt[q * No]);
+    out[(int64_t)e * kRows * NN + rem] = s;
   }
 }
 
+// ---------------------------------------------------------------- Π correlation: TMA / mbarrier pipeline
+// Stage = (kz, E0..E0+EC-1, xy0..xy0+XC-1): the W tile [EC][72][XC] (5-D TMA box) and the G_a window
+// rows E0+s_0 .. E0+EC-1+s_{NWP-1} (4-D TMA box; rows >= NE zero-filled: reading R7). Warp 18 produces;
+// warps 0..17 consume (warp w: m-fragment w%9 of the rows (t,ij), half of the m-column fragments).
 struct PiCfg {
-  static constexpr int XC = 20;       // xy values per step (5 DMMA k-steps)
-  static constexpr int XCP = 20;      // row stride (conflict-free fragment LDS.128)
-  static constexpr int STAGES = 4;
-  static constexpr int A_STAGE = kRows * XCP;
+  static constexpr int XC = 20;      // xy per stage: 5 DMMA k-steps; row stride 80 words ≡ 16 (mod 32)
+  static constexpr int EC = 2;       // energies per stage
+  static constexpr int STAGES = 3;
+  static constexpr int W_STAGE = EC * kRows * XC;
+  static constexpr int NCONS = 18;
+  static constexpr int THREADS = (NCONS + 1) * 32;
 };
 
-// One CTA = (item: destination atom a + ≤8 pairs, qz). Warp w owns m-fragment w and all m columns.
 template <int NFM>
-__global__ void __launch_bounds__(kThreads, 1) k_pi_contract(PiCArgs A) {
-  using C = PiCfg;
-  extern __shared__ __align__(16) double2 smem[];
-  double2* As = smem;                                   // [STAGES][72][XCP]
-  double2* rings = smem + C::STAGES * C::A_STAGE;       // [nring][ring_rows][XCP]
-  __shared__ PiPair pairs_s[kMaxPairs];
+struct PiTma {
+  static constexpr int NWP = NFM * 8;
+  static constexpr int GROWS = PiCfg::EC + NWP - 1;
+  static constexpr int G_STAGE = ((GROWS * PiCfg::XC) + 7) & ~7;   // 128-byte multiple
+  static constexpr int STAGE = PiCfg::W_STAGE + G_STAGE;
+  static constexpr uint32_t STAGE_BYTES = (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 16;
+  static constexpr int NF0 = (NFM + 1) / 2, NF1 = NFM / 2;
+  static constexpr size_t SMEM = (size_t)PiCfg::STAGES * STAGE * 16 + 2 * PiCfg::STAGES * 8 + 128;
+};
 
+// DMMA work of one stage for one warp (NFW column fragments starting at f0).
+// Complex k-step over N column fragments (compile-time N): (re·re, re·im) for fragment f, then
+// (-im·im, im·re) for fragment f-1, so the two DMMAs on one accumulator are never adjacent.
+template <int N>
+__device__ __forceinline__ void pi_kstep(CAcc* acc, double2 a, const double2* gb) {
+  double2 bp = gb[0];
+  dmma(acc[0].r0, acc[0].r1, a.x, bp.x);
+  dmma(acc[0].i0, acc[0].i1, a.x, bp.y);
+#pragma unroll
+  for (int f = 1; f < N; ++f) {
+    const double2 b = gb[f * 8 * PiCfg::XC];
+    dmma(acc[f].r0, acc[f].r1, a.x, b.x);
+    dmma(acc[f].i0, acc[f].i1, a.x, b.y);
+    dmma(acc[f - 1].r0, acc[f - 1].r1, -a.y, bp.y);
+    dmma(acc[f - 1].i0, acc[f - 1].i1, a.y, bp.x);
+    bp = b;
+  }
+  dmma(acc[N - 1].r0, acc[N - 1].r1, -a.y, bp.y);
+  dmma(acc[N - 1].i0, acc[N - 1].i1, a.y, bp.x);
+}
+
+template <int N>
+__device__ __forceinline__ void pi_energy(CAcc* acc, const double2* ws, const double2* gs) {
+#pragma unroll
+  for (int k4 = 0; k4 < PiCfg::XC; k4 += 4) pi_kstep<N>(acc, ws[k4], gs + k4);
+}
+
+// DMMA work of one stage for one warp. rem = NE - E0 - shift0: energy E0+el has in-window columns
+// m < rem - el; only the column fragments that contain such m are computed (warp-uniform switch).
+template <int NFW>
+__device__ __forceinline__ void pi_stage(CAcc* acc, const double2* ws, const double2* gs, int rem, int f0) {
+  using C = PiCfg;
+#pragma unroll
+  for (int el = 0; el < C::EC; ++el) {
+    const int nfe = min(NFW, ((rem - el + 7) >> 3) - f0);
+    const double2* w = ws + el * kRows * C::XC;
+    const double2* g = gs + el * C::XC;
+    switch (nfe) {
+      case 8: if (NFW >= 8) pi_energy<(NFW >= 8 ? 8 : 1)>(acc, w, g); break;
+      case 7: if (NFW >= 7) pi_energy<(NFW >= 7 ? 7 : 1)>(acc, w, g); break;
+      case 6: if (NFW >= 6) pi_energy<(NFW >= 6 ? 6 : 1)>(acc, w, g); break;
+      case 5: if (NFW >= 5) pi_energy<(NFW >= 5 ? 5 : 1)>(acc, w, g); break;
+      case 4: if (NFW >= 4) pi_energy<(NFW >= 4 ? 4 : 1)>(acc, w, g); break;
+      case 3: if (NFW >= 3) pi_energy<(NFW >= 3 ? 3 : 1)>(acc, w, g); break;
+      case 2: if (NFW >= 2) pi_energy<(NFW >= 2 ? 2 : 1)>(acc, w, g); break;
+      case 1: pi_energy<1>(acc, w, g); break;
+      default: break;
+    }
+  }
+}
+
+template <int NFM>
+__global__ void __launch_bounds__(PiCfg::THREADS, 1)
+    k_pi_contract(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmG, PiCArgs A) {
+  using C = PiCfg;
+  using T = PiTma<NFM>;
+  extern __shared__ uint8_t smem_raw[];
+  double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * T::STAGE);
+  uint64_t* empty = full + C::STAGES;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t blk = blockIdx.x;
   const int qz = (int)(blk % A.Nqz);
-  const PiItem item = A.items[A.i0 + blk / A.Nqz];
+  const int il = (int)(blk / A.Nqz);
+  const PiItem item = A.items[A.i0 + il];
   const int P = item.npair;
-  if (threadIdx.x < P) pairs_s[threadIdx.x] = A.pairs[item.pair0 + threadIdx.x];
+  const int NN = A.NN;
+  const int nxc = (NN + C::XC - 1) / C::XC;
+  const int e_end = A.NE - A.shift0;                    // E with at least one in-window E + s_m (R7)
+  const int nec = e_end > 0 ? (e_end + C::EC - 1) / C::EC : 0;
+  const int nst = A.Nkz * nxc * nec;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCONS);
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
 
-  const int NN = A.NN, R = A.ring_rows;
-  const int nxc = (NN + C::XC - 1) / C::XC;
-  const int e_end = A.NE - A.shift0;   // E with at least one in-window E + s_m (R7)
-  const int64_t nsteps = e_end > 0 ? (int64_t)A.Nkz * nxc * e_end : 0;
-
-  auto load_step = [&](int slot, int64_t g) {
-    const int64_t seg = g / e_end;
-    const int e = (int)(g - seg * e_end);
-    const int kz = (int)(seg / nxc), xc = (int)(seg - (int64_t)kz * nxc);
-    const int xy0 = xc * C::XC;
-    double2* as = As + slot * C::A_STAGE;
-    for (int idx = threadIdx.x; idx < 9 * P * C::XC; idx += kThreads) {
-      const int row = idx / C::XC, c = idx - row * C::XC;
-      const int t = row / 9, ij = row - 9 * t;
-      const bool v = xy0 + c < NN;
-      const int64_t pl = item.pair0 + t - A.p0;
-      const double2* src = v ? A.W + (((pl * A.Nkz + kz) * A.NE + e) * 9 + ij) * NN + xy0 + c : A.W;
-      cp_async16(as + row * C::XCP + c, src, v);
-    }
-    const int k2 = (int)imod(kz + qz - A.h, A.Nkz);     // kz + qz (R5)
-    double2* ring = rings + (int)(seg % A.nring) * R * C::XCP;
-    const int m_lo = e == 0 ? 0 : A.NWP - 1;              // prime the window, then one new row per E
-    const int nrow = A.NWP - m_lo;
-    for (int idx = threadIdx.x; idx < nrow * C::XC; idx += kThreads) {
-      const int mr = idx / C::XC, c = idx - mr * C::XC;
-      const int ep = e + A.shift0 + m_lo + mr;
-      const bool v = (ep < A.NE) && (xy0 + c < NN);
-      const double2* src = v ? A.GX + (((int64_t)k2 * A.NE + ep) * A.Nwin + item.a_in) * NN + xy0 + c : A.GX;
-      cp_async16(ring + (ep % R) * C::XCP + c, src, v);
-    }
-  };
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool active = warp * 8 < 9 * P;
-  CAcc acc[NFM];
+  const int mi = warp % 9;
+  const bool upper = warp >= 9;
+  const int f0 = upper ? T::NF0 : 0;
+  CAcc acc[T::NF0];
 #pragma unroll
-  for (int f = 0; f < NFM; ++f) acc[f] = CAcc{0.0, 0.0, 0.0, 0.0};
+  for (int f = 0; f < T::NF0; ++f) acc[f] = CAcc{0.0, 0.0, 0.0, 0.0};
 
-#pragma unroll
-  for (int s = 0; s < C::STAGES - 1; ++s) {
-    if (s < nsteps) load_step(s, s);
-    cp_async_commit();
-  }
-  for (int64_t g = 0; g < nsteps; ++g) {
-    cp_async_wait<C::STAGES - 2>();
-    __syncthreads();
-    {
-      const int64_t nx = g + C::STAGES - 1;
-      if (nx < nsteps) load_step((int)(nx % C::STAGES), nx);
-      cp_async_commit();
+  if (warp == C::NCONS) {
+    if (lane == 0) {
+      prefetch_tmap(&tmW);
+      prefetch_tmap(&tmG);
+      int kz = 0, xc = 0, ec = 0;
+      for (int st = 0; st < nst; ++st) {
+        const int slot = st % C::STAGES;
+        if (st >= C::STAGES) mbar_wait(&empty[slot], ((st / C::STAGES) - 1) & 1);
+        mbar_arrive_expect_tx(&full[slot], T::STAGE_BYTES);
+        double2* ws = smem + slot * T::STAGE;
+        const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
+        tma_load_5d(ws, &tmW, 2 * xc * C::XC, 0, ec * C::EC, kz, il, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, item.a_in, ec * C::EC + A.shift0, k2, &full[slot]);
+        if (++ec == nec) {
+          ec = 0;
+          if (++xc == nxc) {
+            xc = 0;
+            ++kz;
+          }
+        }
+      }
+    }
+  } else {
+    const bool active = mi * 8 < 9 * P;
+    int ec = 0;
+    for (int st = 0; st < nst; ++st) {
+      const int slot = st % C::STAGES;
+      mbar_wait(&full[slot], (st / C::STAGES) & 1);
+      if (active) {
+        const double2* ws = smem + slot * T::STAGE + (mi * 8 + (lane >> 2)) * C::XC + (lane & 3);
+        const double2* gs = smem + slot * T::STAGE + C::W_STAGE + (f0 * 8 + (lane >> 2)) * C::XC + (lane & 3);
+        const int rem = A.NE - ec * C::EC - A.shift0;
+        if (upper)
+          pi_stage<T::NF1>(acc, ws, gs, rem, f0);
+        else
+          pi_stage<T::NF0>(acc, ws, gs, rem, f0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++ec == nec) ec = 0;
     }
     if (active) {
-      const int64_t seg = g / e_end;
-      const int e = (int)(g - seg * e_end);
-      const int slot = (int)(g % C::STAGES);
-      const double2* ring = rings + (int)(seg % A.nring) * R * C::XCP;
-      const double2* as = As + slot * C::A_STAGE + (warp * 8 + (lane >> 2)) * C::XCP + (lane & 3);
-      // column fragments with at least one in-window E + s_m
-      const int nf = min(NFM, (A.NE - e - A.shift0 + 7) >> 3);
-      int rowoff[NFM];
+      const int row = mi * 8 + (lane >> 2);
+      const int t = row / 9, ij = row - 9 * t;
+      const int nfw = upper ? T::NF1 : T::NF0;
+      if (t < P) {
+        const int slot = A.pairs[item.pair0 + t].s + 1;
+        const int64_t base = (int64_t)item.a_out * (A.Nb + 1) * 9 + slot * 9 + ij;
 #pragma unroll
-      for (int f = 0; f < NFM; ++f) rowoff[f] = ((e + A.shift0 + f * 8 + (lane >> 2)) % R) * C::XCP + (lane & 3);
-#pragma unroll
-      for (int k4 = 0; k4 < C::XC; k4 += 4) {
-        const double2 a = as[k4];
-        const double na = -a.y;
-#pragma unroll
-        for (int f = 0; f < NFM; ++f) {
-          if (f < nf) {
-            const double2 b = ring[rowoff[f] + k4];
-            cmma(acc[f], a.x, a.y, na, b.x, b.y);
+        for (int f = 0; f < T::NF0; ++f) {
+          if (f < nfw) {
+            const int m0 = (f0 + f) * 8 + 2 * (lane & 3);
+            if (m0 < A.Nw)
+              A.Pi[((int64_t)qz * A.Nw + m0) * A.Nout * (A.Nb + 1) * 9 + base] =
+                  cmul(A.scale, make_double2(acc[f].r0, acc[f].i0));
+            if (m0 + 1 < A.Nw)
+              A.Pi[((int64_t)qz * A.Nw + m0 + 1) * A.Nout * (A.Nb + 1) * 9 + base] =
+                  cmul(A.scale, make_double2(acc[f].r1, acc[f].i1));
           }
         }
       }
     }
   }
-  cp_async_wait<0>();
+}
 
-  if (active) {
-    const int row = warp * 8 + (lane >> 2);
-    const int t = row / 9, ij = row - 9 * t;
-    if (t < P) {
-      const int slot = pairs_s[t].s + 1;
-#pragma unroll
-      for (int f = 0; f < NFM; ++f) {
-        const int m0 = f * 8 + 2 * (lane & 3);
-        if (m0 < A.Nw)
-          A.Pi[(((int64_t)qz * A.Nw + m0) * A.Nout + item.a_out) * (A.Nb + 1) * 9 + slot * 9 + ij] =
-              cmul(A.scale, make_double2(acc[f].r0, acc[f].i0));
-        if (m0 + 1 < A.Nw)
-          A.Pi[(((int64_t)qz * A.Nw + m0 + 1) * A.Nout + item.a_out) * (A.Nb + 1) * 9 + slot * 9 + ij] =
-              cmul(A.scale, make_double2(acc[f].r1, acc[f].i1));
-      }
-    }
+cudaError_t make_tmap_f64(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                          const uint32_t* box);
+
+template <int NFM>
+static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
+  using T = PiTma<NFM>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_pi_contract<NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const uint64_t NN = (uint64_t)a.NN;
+  CUtensorMap tmW, tmG;
+  {
+    const uint64_t dims[5] = {2 * NN, (uint64_t)kRows, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.nitems};
+    const uint64_t s1 = NN * 16, s2 = s1 * kRows, s3 = s2 * a.NE, s4 = s3 * a.Nkz;
+    const uint64_t strides[4] = {s1, s2, s3, s4};
+    const uint32_t box[5] = {2 * PiCfg::XC, (uint32_t)kRows, PiCfg::EC, 1, 1};
+    cudaError_t e = make_tmap_f64(&tmW, a.W, 5, dims, strides, box);
+    if (e != cudaSuccess) return e;
+  }
+  {
+    const uint64_t dims[4] = {2 * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
+    const uint64_t strides[3] = {NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
+    const uint32_t box[4] = {2 * PiCfg::XC, 1, (uint32_t)T::GROWS, 1};
+    cudaError_t e = make_tmap_f64(&tmG, a.GX, 4, dims, strides, box);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t nblk = a.nitems * a.Nqz;
+  if (nblk == 0) return cudaSuccess;
+  k_pi_contract<NFM><<<(unsigned)nblk, PiCfg::THREADS, T::SMEM, st>>>(tmW, tmG, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pi_contract(const PiCArgs& a, int64_t /*nitems*/, cudaStream_t st) {
+  switch (a.NWP / 8) {
+    case 1: return launch_pi_nfm<1>(a, st);
+    case 2: return launch_pi_nfm<2>(a, st);
+    case 3: return launch_pi_nfm<3>(a, st);
+    case 4: return launch_pi_nfm<4>(a, st);
+    case 5: return launch_pi_nfm<5>(a, st);
+    case 6: return launch_pi_nfm<6>(a, st);
+    case 7: return launch_pi_nfm<7>(a, st);
+    case 8: return launch_pi_nfm<8>(a, st);
+    case 9: return launch_pi_nfm<9>(a, st);
+    case 10: return launch_pi_nfm<10>(a, st);
+    case 11: return launch_pi_nfm<11>(a, st);
+    case 12: return launch_pi_nfm<12>(a, st);
+    case 13: return launch_pi_nfm<13>(a, st);
+    case 14: return launch_pi_nfm<14>(a, st);
+    case 15: return launch_pi_nfm<15>(a, st);
+    case 16: return launch_pi_nfm<16>(a, st);
+    default: return cudaErrorInvalidValue;
   }
 }
+
 
 // Π_{a,0} = Σ_{valid s} Π_{a,s+1} (reading R9); empty slots are set to 0 (R12).
 __global__ void k_pi_self(PiSelfArgs A) {
@@ -212,43 +332,6 @@ cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st)
   }
   k_pi_w<<<(unsigned)nblk, 256, smem, st>>>(a);
   return cudaGetLastError();
-}
-
-size_t pi_contract_smem(int nring, int ring_rows) {
-  return (size_t)(PiCfg::STAGES * PiCfg::A_STAGE + nring * ring_rows * PiCfg::XCP) * sizeof(double2);
-}
-
-template <int NFM>
-static cudaError_t launch_pi_nfm(const PiCArgs& a, int64_t nitems, cudaStream_t st) {
-  size_t smem = pi_contract_smem(a.nring, a.ring_rows);
-  cudaError_t e = cudaFuncSetAttribute(k_pi_contract<NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int64_t nblk = nitems * a.Nqz;
-  if (nblk == 0) return cudaSuccess;
-  k_pi_contract<NFM><<<(unsigned)nblk, kThreads, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st) {
-  switch (a.NWP / 8) {
-    case 1: return launch_pi_nfm<1>(a, nitems, st);
-    case 2: return launch_pi_nfm<2>(a, nitems, st);
-    case 3: return launch_pi_nfm<3>(a, nitems, st);
-    case 4: return launch_pi_nfm<4>(a, nitems, st);
-    case 5: return launch_pi_nfm<5>(a, nitems, st);
-    case 6: return launch_pi_nfm<6>(a, nitems, st);
-    case 7: return launch_pi_nfm<7>(a, nitems, st);
-    case 8: return launch_pi_nfm<8>(a, nitems, st);
-    case 9: return launch_pi_nfm<9>(a, nitems, st);
-    case 10: return launch_pi_nfm<10>(a, nitems, st);
-    case 11: return launch_pi_nfm<11>(a, nitems, st);
-    case 12: return launch_pi_nfm<12>(a, nitems, st);
-    case 13: return launch_pi_nfm<13>(a, nitems, st);
-    case 14: return launch_pi_nfm<14>(a, nitems, st);
-    case 15: return launch_pi_nfm<15>(a, nitems, st);
-    case 16: return launch_pi_nfm<16>(a, nitems, st);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st) {

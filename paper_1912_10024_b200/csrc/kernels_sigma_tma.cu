@@ -225,13 +225,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// FP64 4-D tiled map; dims/box innermost first, strides in bytes for dims 1..3.
-cudaError_t make_tmap_f64_4d(CUtensorMap* m, const void* base, const uint64_t dims[4], const uint64_t strides[3],
-                             const uint32_t box[4]) {
+// FP64 tiled map of rank 1..5; dims/box innermost first, strides in bytes for dims 1..rank-1.
+cudaError_t make_tmap_f64(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                          const uint32_t* box) {
   auto fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
-  const uint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
+  const uint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -252,7 +252,7 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     const uint64_t dims[4] = {2 * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
     const uint64_t strides[3] = {NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
     const uint32_t box[4] = {2 * C::NPS, 1, C::KC, 1};
-    cudaError_t e = make_tmap_f64_4d(&tmG, a.G, dims, strides, box);
+    cudaError_t e = make_tmap_f64(&tmG, a.G, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
   {
@@ -260,7 +260,7 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     const uint64_t dims[4] = {2 * D, (uint64_t)a.Nqz, 9, (uint64_t)a.npairs_chunk};
     const uint64_t strides[3] = {D * 16, (uint64_t)a.Nqz * D * 16, 9ull * a.Nqz * D * 16};
     const uint32_t box[4] = {2 * C::KCP, 1, 9, kMaxPairs};
-    cudaError_t e = make_tmap_f64_4d(&tmC, a.coef, dims, strides, box);
+    cudaError_t e = make_tmap_f64(&tmC, a.coef, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
   const int64_t nblk = nitems * a.NE * a.Nkz;

@@ -28,6 +28,7 @@ struct qt_sse_plan_s {
   int32_t* d_sig_pair_item = nullptr;
   PiItem* d_pi_items = nullptr;
   PiPair* d_pi_pairs = nullptr;
+  int32_t* d_pi_pair_item = nullptr;
   std::vector<SigItem> sig_items;
   std::vector<PiItem> pi_items;
   int64_t n_sig_pairs = 0, n_pi_pairs = 0;
@@ -35,7 +36,6 @@ struct qt_sse_plan_s {
   std::vector<int64_t> sig_chunks, pi_chunks;   // item boundaries
   double2* ws = nullptr;
   size_t ws_bytes = 0;
-  int pi_nring = 2;
   double flops[4] = {0, 0, 0, 0};
   // host-execute staging
   void* h_dev = nullptr;
@@ -210,6 +210,7 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_sig_pair_item);
   cudaFree(p->d_pi_items);
   cudaFree(p->d_pi_pairs);
+  cudaFree(p->d_pi_pair_item);
   cudaFree(p->ws);
   cudaFree(p->h_dev);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -294,6 +295,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   p->n_sig_pairs = (int64_t)sp.size();
   // Π work list: destination-organized. For each owned atom a, its valid slots in chunks of 8.
   std::vector<PiPair> pp;
+  std::vector<int32_t> pp_item;
   for (int64_t a = p->a_lo; a < p->a_hi; ++a) {
     std::vector<PiPair> mine;
     for (int64_t s = 0; s < d.Nb; ++s) {
@@ -312,7 +314,10 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
       it.a_in = (int32_t)(a - p->w_lo);
       it.npair = (int32_t)std::min<size_t>(kMaxPairs, mine.size() - k);
       it.pair0 = (int32_t)pp.size();
-      for (int t = 0; t < it.npair; ++t) pp.push_back(mine[k + t]);
+      for (int t = 0; t < it.npair; ++t) {
+        pp.push_back(mine[k + t]);
+        pp_item.push_back((int32_t)p->pi_items.size());
+      }
       p->pi_items.push_back(it);
     }
   }
@@ -321,7 +326,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
 
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
-  const size_t w_per_pair = (size_t)d.Nkz * d.NE * 9 * p->NN * sizeof(double2);
+  const size_t w_per_item = (size_t)d.Nkz * d.NE * kRows * p->NN * sizeof(double2);
   size_t budget = d.workspace_limit;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
@@ -331,34 +336,35 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
     budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
   }
-  const size_t need_min = std::max(coef_per_pair, w_per_pair) * kMaxPairs;
+  const size_t need_min = std::max(coef_per_pair * kMaxPairs, w_per_item);
   if (budget < need_min) budget = need_min;
-  const size_t full = std::max(coef_per_pair * p->n_sig_pairs, w_per_pair * p->n_pi_pairs);
+  const size_t full = std::max(coef_per_pair * p->n_sig_pairs, w_per_item * p->pi_items.size());
   p->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
   // chunk item ranges so that each chunk's pairs fit the workspace
-  auto make_chunks = [&](auto& items, size_t per_pair, std::vector<int64_t>& bounds) {
-    const int64_t cap = (int64_t)(p->ws_bytes / per_pair);
+  // chunk item ranges so that each chunk's scratch fits the workspace (Σ: per pair; Π: per item)
+  auto make_chunks = [&](auto& items, size_t per_unit, bool per_pair, std::vector<int64_t>& bounds) {
+    const int64_t cap = (int64_t)(p->ws_bytes / per_unit);
     bounds.clear();
     bounds.push_back(0);
     int64_t acc = 0;
     for (size_t i = 0; i < items.size(); ++i) {
-      if (acc + items[i].npair > cap) {
+      const int64_t u = per_pair ? items[i].npair : 1;
+      if (acc + u > cap) {
         bounds.push_back((int64_t)i);
         acc = 0;
       }
-      acc += items[i].npair;
+      acc += u;
     }
     bounds.push_back((int64_t)items.size());
   };
-  make_chunks(p->sig_items, coef_per_pair, p->sig_chunks);
-  make_chunks(p->pi_items, w_per_pair, p->pi_chunks);
-  const int64_t e_end = d.NE - d.shift0;
-  p->pi_nring = e_end >= 3 ? 2 : 4;
+  make_chunks(p->sig_items, coef_per_pair, true, p->sig_chunks);
+  make_chunks(p->pi_items, w_per_item, false, p->pi_chunks);
 
   qt_status s2;
   if ((s2 = upload(&p->d_nbr_win, p->nbr_win, cs)) != QT_OK || (s2 = upload(&p->d_sig_items, p->sig_items, cs)) != QT_OK ||
       (s2 = upload(&p->d_sig_pairs, sp, cs)) != QT_OK || (s2 = upload(&p->d_sig_pair_item, sp_item, cs)) != QT_OK ||
-      (s2 = upload(&p->d_pi_items, p->pi_items, cs)) != QT_OK || (s2 = upload(&p->d_pi_pairs, pp, cs)) != QT_OK) {
+      (s2 = upload(&p->d_pi_items, p->pi_items, cs)) != QT_OK || (s2 = upload(&p->d_pi_pairs, pp, cs)) != QT_OK ||
+      (s2 = upload(&p->d_pi_pair_item, pp_item, cs)) != QT_OK) {
     qt_sse_destroy(p);
     return s2;
   }
@@ -478,8 +484,11 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       wa.GY = GY;
       wa.dH = (const double2*)dH;
       wa.pairs = p->d_pi_pairs;
+      wa.items = p->d_pi_items;
+      wa.pair_item = p->d_pi_pair_item;
       wa.W = p->ws;
       wa.p0 = pp0;
+      wa.i0 = i0;
       wa.Nwin = p->Nwin;
       wa.Nb = d.Nb;
       wa.NE = (int)d.NE;
@@ -495,8 +504,8 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       ca.pairs = p->d_pi_pairs;
       ca.Pi = P;
       ca.scale = make_double2(sre, sim);
-      ca.p0 = pp0;
       ca.i0 = i0;
+      ca.nitems = i1 - i0;
       ca.Nwin = p->Nwin;
       ca.Nout = p->Nout;
       ca.Nb = d.Nb;
@@ -508,8 +517,6 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       ca.Nw = (int)d.Nw;
       ca.NWP = (int)p->NWP;
       ca.shift0 = d.shift0;
-      ca.nring = p->pi_nring;
-      ca.ring_rows = (int)(p->NWP + 3);
       QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
     }
     PiSelfArgs sa;
