@@ -114,25 +114,33 @@ __device__ __forceinline__ void pi_energy(CAcc* acc, const double2* ws, const do
 }
 
 // DMMA work of one stage for one warp. rem = NE - E0 - shift0: energy E0+el has in-window columns
-// m < rem - el; only the column fragments that contain such m are computed (warp-uniform switch).
+// m < rem - el; column fragments without any are skipped (fast path: all NFW fragments live).
 template <int NFW>
 __device__ __forceinline__ void pi_stage(CAcc* acc, const double2* ws, const double2* gs, int rem, int f0) {
+  static_assert(NFW > 0, "empty fragment range");
   using C = PiCfg;
 #pragma unroll
   for (int el = 0; el < C::EC; ++el) {
     const int nfe = min(NFW, ((rem - el + 7) >> 3) - f0);
     const double2* w = ws + el * kRows * C::XC;
     const double2* g = gs + el * C::XC;
-    switch (nfe) {
-      case 8: if (NFW >= 8) pi_energy<(NFW >= 8 ? 8 : 1)>(acc, w, g); break;
-      case 7: if (NFW >= 7) pi_energy<(NFW >= 7 ? 7 : 1)>(acc, w, g); break;
-      case 6: if (NFW >= 6) pi_energy<(NFW >= 6 ? 6 : 1)>(acc, w, g); break;
-      case 5: if (NFW >= 5) pi_energy<(NFW >= 5 ? 5 : 1)>(acc, w, g); break;
-      case 4: if (NFW >= 4) pi_energy<(NFW >= 4 ? 4 : 1)>(acc, w, g); break;
-      case 3: if (NFW >= 3) pi_energy<(NFW >= 3 ? 3 : 1)>(acc, w, g); break;
-      case 2: if (NFW >= 2) pi_energy<(NFW >= 2 ? 2 : 1)>(acc, w, g); break;
-      case 1: pi_energy<1>(acc, w, g); break;
-      default: break;
+    if (nfe == NFW) {
+      pi_energy<NFW>(acc, w, g);
+    } else if (nfe > 0) {
+#pragma unroll
+      for (int k4 = 0; k4 < C::XC; k4 += 4) {
+        const double2 a = w[k4];
+#pragma unroll
+        for (int f = 0; f < NFW; ++f) {
+          if (f < nfe) {
+            const double2 b = g[k4 + f * 8 * C::XC];
+            dmma(acc[f].r0, acc[f].r1, a.x, b.x);
+            dmma(acc[f].i0, acc[f].i1, a.x, b.y);
+            dmma(acc[f].r0, acc[f].r1, -a.y, b.y);
+            dmma(acc[f].i0, acc[f].i1, a.y, b.x);
+          }
+        }
+      }
     }
   }
 }
@@ -207,10 +215,11 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const double2* ws = smem + slot * T::STAGE + (mi * 8 + (lane >> 2)) * C::XC + (lane & 3);
         const double2* gs = smem + slot * T::STAGE + C::W_STAGE + (f0 * 8 + (lane >> 2)) * C::XC + (lane & 3);
         const int rem = A.NE - ec * C::EC - A.shift0;
-        if (upper)
-          pi_stage<T::NF1>(acc, ws, gs, rem, f0);
-        else
+        if (upper) {
+          if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, gs, rem, f0);
+        } else {
           pi_stage<T::NF0>(acc, ws, gs, rem, f0);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);

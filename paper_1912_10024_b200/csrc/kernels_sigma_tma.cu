@@ -21,9 +21,9 @@ template <int NF>
 struct SigTmaCfg {
   static constexpr int NP = 8 * NF;
   static constexpr int NPS = NP + 2;        // ≡ 2 (mod 8): conflict-free B-fragment LDS.128
-  static constexpr int KC = 32;             // d values per stage (8 DMMA k-steps)
-  static constexpr int KCP = 36;            // ≡ 4 (mod 8): conflict-free A-fragment LDS.128
-  static constexpr int STAGES = 2;
+  static constexpr int KC = 16;             // d values per stage (4 DMMA k-steps)
+  static constexpr int KCP = 20;            // ≡ 4 (mod 8): conflict-free A-fragment LDS.128
+  static constexpr int STAGES = 4;
   static constexpr int G_STAGE = KC * NPS;  // complex elements
   static constexpr int C_STAGE = kRows * KCP;
   static constexpr int STAGE = G_STAGE + C_STAGE;
@@ -48,6 +48,7 @@ struct SigTmaCfg {
 // two B fragments are live: (re·re, re·im) for fragment f, then (-im·im, im·re) for fragment f-1.
 template <int NFW, int NPS, int KC>
 __device__ __forceinline__ void sigma_stage(CAcc* acc, const double2* gs, const double2* cs, int kc) {
+  static_assert(NFW > 0, "empty fragment range");
 #pragma unroll
   for (int k4 = 0; k4 < KC; k4 += 4) {
     if (k4 < kc) {
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       for (int st = 0; st < nst; ++st) {
         const int slot = st & (C::STAGES - 1);
         if (st >= C::STAGES) mbar_wait(&empty[slot], ((st / C::STAGES) - 1) & 1);
+        static_assert((C::STAGES & (C::STAGES - 1)) == 0, "power-of-two stage count");
         mbar_arrive_expect_tx(&full[slot], C::STAGE_BYTES);
         const int dd0 = dd_lo + c * C::KC;
         const int kp = (int)imod(kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
@@ -144,10 +146,11 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
         const int kc = min(C::KC, dd_hi - (dd_lo + c * C::KC));
         const double2* gs = smem + slot * C::STAGE + (lane & 3) * C::NPS + (lane >> 2) + f0 * 8;
         const double2* cs = smem + slot * C::STAGE + C::G_STAGE + (mi * 8 + (lane >> 2)) * C::KCP + (lane & 3);
-        if (upper)
-          sigma_stage<C::NF1, C::NPS, C::KC>(acc, gs, cs, kc);
-        else
+        if (upper) {
+          if constexpr (C::NF1 > 0) sigma_stage<C::NF1, C::NPS, C::KC>(acc, gs, cs, kc);
+        } else {
           sigma_stage<C::NF0, C::NPS, C::KC>(acc, gs, cs, kc);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -179,36 +182,81 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
   }
   __syncthreads();
 
+  // Register-blocked sandwich: each thread owns a 2 x YB output block (rows x, x+1; columns y0..y0+YB-1).
+  constexpr int YB = 5;
+  const int nxb = (No + 1) >> 1, nyb = (No + YB - 1) / YB;
   // ---- epilogue 2: V^i_t = Σ_j Gt^{ij}_t · ∇_jH_{b r_t}
-  for (int idx = tid; idx < P * 3 * NN; idx += C::THREADS) {
-    const int t = idx / (3 * NN), rem = idx - t * 3 * NN, i = rem / NN, xy = rem - i * NN;
-    const int x = xy / No, y = xy - x * No;
-    double2 s = make_double2(0.0, 0.0);
+  for (int idx = tid; idx < P * 3 * nxb * nyb; idx += C::THREADS) {
+    const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, ti = r1 / nxb;   // ti = t*3 + i
+    const int t = ti / 3, i = ti - 3 * t, x0 = 2 * xb, y0 = yb * YB;
+    double2 s[2][YB];
 #pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int w = 0; w < YB; ++w) s[u][w] = make_double2(0.0, 0.0);
     for (int j = 0; j < 3; ++j) {
-      const double2* g = Gt + (t * 9 + i * 3 + j) * C::NPS + x * No;
-      const double2* hr = Hr + t * 3 * C::NP + j * NN + y;
-      for (int v = 0; v < No; ++v) cfma(s, g[v], hr[v * No]);
+      const double2* g0 = Gt + (t * 9 + i * 3 + j) * C::NPS + x0 * No;
+      const double2* hr = Hr + t * 3 * C::NP + j * NN + y0;
+      for (int v = 0; v < No; ++v) {
+        const double2 ga = g0[v], gb = (x0 + 1 < No) ? g0[No + v] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int w = 0; w < YB; ++w) {
+          const double2 h = (y0 + w < No) ? hr[v * No + w] : make_double2(0.0, 0.0);
+          cfma(s[0][w], ga, h);
+          cfma(s[1][w], gb, h);
+        }
+      }
     }
-    Vs[(t * 3 + i) * C::NP + xy] = s;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int w = 0; w < YB; ++w)
+        if (x0 + u < No && y0 + w < No) Vs[ti * C::NP + (x0 + u) * No + y0 + w] = s[u][w];
+  }
+  __syncthreads();
+  // ∇_iH_{a_t s_t} -> shared memory (reuses the Gt region)
+  double2* Hl = smem;
+  for (int idx = tid; idx < P * 3 * NN; idx += C::THREADS) {
+    const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
+    const SigPair pr = pairs_s[t];
+    Hl[t * 3 * C::NP + rem] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
   }
   __syncthreads();
 
   // ---- epilogue 3: S_t = Σ_i ∇_iH_{a_t s_t} · V^i_t; Σ_a += scale · S_t (R8)
-  for (int idx = tid; idx < P * NN; idx += C::THREADS) {
-    const int t = idx / NN, xy = idx - t * NN, x = xy / No, y = xy - x * No;
-    const SigPair pr = pairs_s[t];
-    double2 s = make_double2(0.0, 0.0);
+  for (int idx = tid; idx < P * nxb * nyb; idx += C::THREADS) {
+    const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, t = r1 / nxb;
+    const int x0 = 2 * xb, y0 = yb * YB;
+    double2 s[2][YB];
 #pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int w = 0; w < YB; ++w) s[u][w] = make_double2(0.0, 0.0);
     for (int i = 0; i < 3; ++i) {
-      const double2* hl = A.dH + (((int64_t)pr.a_in * A.Nb + pr.s) * 3 + i) * NN + x * No;
-      const double2* v = Vs + (t * 3 + i) * C::NP + y;
-      for (int u = 0; u < No; ++u) cfma(s, __ldg(hl + u), v[u * No]);
+      const double2* hl = Hl + t * 3 * C::NP + i * NN + x0 * No;
+      const double2* v = Vs + (t * 3 + i) * C::NP + y0;
+      for (int u = 0; u < No; ++u) {
+        const double2 ha = hl[u], hb = (x0 + 1 < No) ? hl[No + u] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int w = 0; w < YB; ++w) {
+          const double2 vv = (y0 + w < No) ? v[u * No + w] : make_double2(0.0, 0.0);
+          cfma(s[0][w], ha, vv);
+          cfma(s[1][w], hb, vv);
+        }
+      }
     }
-    const double2 r = cmul(A.scale, s);
-    double* dst = reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NE + E) * A.Nout + pr.a) * NN + xy);
-    atomicAdd(dst, r.x);
-    atomicAdd(dst + 1, r.y);
+    const SigPair pr = pairs_s[t];
+    double2* out = A.Sig + (((int64_t)kz * A.NE + E) * A.Nout + pr.a) * NN;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int w = 0; w < YB; ++w)
+        if (x0 + u < No && y0 + w < No) {
+          const double2 r = cmul(A.scale, s[u][w]);
+          double* dst = reinterpret_cast<double*>(out + (x0 + u) * No + y0 + w);
+          atomicAdd(dst, r.x);
+          atomicAdd(dst + 1, r.y);
+        }
   }
 }
 
