@@ -20,7 +20,7 @@ QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM = range(3)
 EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
             "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read"]
-KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self"]
+KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout"]
 
 
 class Desc(ctypes.Structure):

@@ -16,7 +16,8 @@ struct CoefArgs {
 };
 
 struct SigmaArgs {
-  const double2* G;
+  const double2* G;      // G^X, paper layout [Nkz][NE][Nwin][NN]
+  const double2* Gam;    // G^X, atom-major copy [Nwin][Nkz][NE][NN] (TMA path)
   const double2* coef;   // coefficient table of the current chunk: pair index p - cp0
   const double2* dH;
   const SigItem* items;
@@ -29,6 +30,7 @@ struct SigmaArgs {
 
 struct PiWArgs {
   const double2* GY;
+  const double2* GYam;        // G^Y atom-major [Nwin][Nkz][NE][NN]
   const double2* dH;
   const PiPair* pairs;
   const PiItem* items;
@@ -39,7 +41,7 @@ struct PiWArgs {
 };
 
 struct PiCArgs {
-  const double2* GX;
+  const double2* GX;     // G^X atom-major [Nwin][Nkz][NE][NN]
   const double2* W;
   const PiItem* items;
   const PiPair* pairs;
@@ -63,5 +65,8 @@ cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st)
 cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st);
 cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st);
+// G [Nkz][NE][Nwin][NN] (paper layout) -> [Nwin][Nkz][NE][NN] (atom-major: every TMA box contiguous)
+cudaError_t launch_relayout(const double2* in, double2* out, int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN,
+                            cudaStream_t st);
 
 }  // namespace qt

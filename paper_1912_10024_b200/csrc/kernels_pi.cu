@@ -13,52 +13,95 @@
 
 namespace qt {
 
-// W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] · T_i[q][x],  T_i = G^Y_b · ∇_iH_{br}
+// W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] · T_i[q][x],  T_i = G^Y_b · ∇_iH_{br}   (the Π sandwich)
+// One CTA per (pair, kz); loops over energy chunks of kEB. ∇H blocks stay in shared memory; both
+// products are register-blocked 5x5 (2.5 complex MACs per shared-memory load); W is staged in shared
+// memory and written with contiguous 16-byte stores into the item's 72-row block.
+constexpr int kWB = 5;   // register block edge
+
+template <bool ROWS_X>
+__device__ __forceinline__ void block_mm(const double2* __restrict__ L, int ldl, const double2* __restrict__ R, int ldr,
+                                         int r0, int c0, int n, int No, double2 (&acc)[kWB][kWB]) {
+  // acc[u][w] += Σ_k L[(r0+u)*ldl + k] * R[k*ldr + c0 + w], rows/cols < No
+  for (int k = 0; k < n; ++k) {
+    double2 l[kWB], r[kWB];
+#pragma unroll
+    for (int u = 0; u < kWB; ++u) l[u] = (r0 + u < No) ? L[(r0 + u) * ldl + k] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < kWB; ++w) r[w] = (c0 + w < No) ? R[k * ldr + c0 + w] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kWB; ++u)
+#pragma unroll
+      for (int w = 0; w < kWB; ++w) cfma(acc[u][w], l[u], r[w]);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_pi_w(PiWArgs A) {
+  // One CTA per (work item = ≤8 pairs of one destination atom, kz); energy chunks of kWE (1 or 2).
+  const int kWE = A.nEB;
   extern __shared__ __align__(16) double2 sm[];
   const int NN = A.NN, No = A.Norb;
-  double2* Gb = sm;                 // [kEB][NN]
-  double2* Hl = Gb + kEB * NN;      // [3][NN]  ∇_jH_{as}
-  double2* Hr = Hl + 3 * NN;        // [3][NN]  ∇_iH_{br}
-  double2* T = Hr + 3 * NN;         // [kEB][3][NN]
-  const int64_t blk = blockIdx.x;
-  const int eb = (int)(blk % A.nEB);
-  const int kz = (int)((blk / A.nEB) % A.Nkz);
-  const int64_t p = A.p0 + blk / ((int64_t)A.nEB * A.Nkz);
-  const PiPair pr = A.pairs[p];
-  const int item = A.pair_item[p];
-  const int t = (int)(p - A.items[item].pair0);
-  const int64_t il = item - A.i0;
-  const int e0 = eb * kEB;
-  const int ne = min(kEB, A.NE - e0);
-  for (int idx = threadIdx.x; idx < kEB * NN; idx += blockDim.x) {
-    const int e = idx / NN, uv = idx - e * NN;
-    Gb[idx] = e < ne ? A.GY[(((int64_t)kz * A.NE + e0 + e) * A.Nwin + pr.b_in) * NN + uv] : make_double2(0.0, 0.0);
+  const int kz = (int)(blockIdx.x % A.Nkz);
+  const int64_t item = A.i0 + blockIdx.x / A.Nkz;
+  const PiItem it = A.items[item];
+  const int P = it.npair;
+  double2* Hl = sm;                          // [P][3][NN]  ∇_jH_{as}
+  double2* Hr = Hl + kMaxPairs * 3 * NN;     // [P][3][NN]  ∇_iH_{br}
+  double2* Gb = Hr + kMaxPairs * 3 * NN;     // [P][kWE][NN]
+  double2* T = Gb + kMaxPairs * kWE * NN;    // [P][kWE][3][NN]
+  for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
+    const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
+    const PiPair pr = A.pairs[it.pair0 + t];
+    Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
+    Hr[idx] = A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + rem];
   }
-  for (int idx = threadIdx.x; idx < 3 * NN; idx += blockDim.x) {
-    Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + idx];
-    Hr[idx] = A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + idx];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < ne * 3 * NN; idx += blockDim.x) {
-    const int e = idx / (3 * NN), rem = idx - e * 3 * NN, i = rem / NN, qx = rem - i * NN;
-    const int q = qx / No, x = qx - q * No;
-    double2 s = make_double2(0.0, 0.0);
-    const double2* g = Gb + e * NN + q * No;
-    const double2* h = Hr + i * NN + x;
-    for (int p = 0; p < No; ++p) cfma(s, g[p], h[p * No]);
-    T[idx] = s;
-  }
-  __syncthreads();
-  double2* out = A.W + (((il * A.Nkz + kz) * A.NE) + e0) * kRows * NN + t * 9 * NN;
-  for (int idx = threadIdx.x; idx < ne * 9 * NN; idx += blockDim.x) {
-    const int e = idx / (9 * NN), rem = idx - e * 9 * NN, ij = rem / NN, xy = rem - ij * NN;
-    const int i = ij / 3, j = ij - 3 * i, x = xy / No, y = xy - x * No;
-    double2 s = make_double2(0.0, 0.0);
-    const double2* hl = Hl + j * NN + y * No;
-    const double2* tt = T + (e * 3 + i) * NN + x;
-    for (int q = 0; q < No; ++q) cfma(s, hl[q], tt[q * No]);
-    out[(int64_t)e * kRows * NN + rem] = s;
+  const int nb1 = (No + kWB - 1) / kWB, nb = nb1 * nb1;
+  double2* Wdst = A.W + ((item - A.i0) * A.Nkz + kz) * (int64_t)A.NE * kRows * NN;
+  for (int e0 = 0; e0 < A.NE; e0 += kWE) {
+    const int ne = min(kWE, A.NE - e0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
+      const int t = idx / (ne * NN), rem = idx - t * ne * NN;
+      const int b_in = A.pairs[it.pair0 + t].b_in;
+      Gb[t * kWE * NN + rem] = A.GYam[(((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem];
+    }
+    __syncthreads();
+    // T_i(t, e) = G_b(e) · ∇_iH_{br}
+    for (int u = threadIdx.x; u < P * ne * 3 * nb; u += blockDim.x) {
+      const int bl = u % nb, r = u / nb, i = r % 3, te = r / 3, e = te % ne, t = te / ne;
+      const int r0 = (bl / nb1) * kWB, c0 = (bl % nb1) * kWB;
+      double2 acc[kWB][kWB];
+#pragma unroll
+      for (int x = 0; x < kWB; ++x)
+#pragma unroll
+        for (int y = 0; y < kWB; ++y) acc[x][y] = make_double2(0.0, 0.0);
+      block_mm<true>(Gb + (t * kWE + e) * NN, No, Hr + (t * 3 + i) * NN, No, r0, c0, No, No, acc);
+      double2* o = T + ((t * kWE + e) * 3 + i) * NN;
+#pragma unroll
+      for (int x = 0; x < kWB; ++x)
+#pragma unroll
+        for (int y = 0; y < kWB; ++y)
+          if (r0 + x < No && c0 + y < No) o[(r0 + x) * No + c0 + y] = acc[x][y];
+    }
+    __syncthreads();
+    // W^{ij}(t, e)[x][y] = (∇_jH_{as} · T_i)[y][x] -> rows t*9 + ij of the item's block (L2 merges lines)
+    for (int u = threadIdx.x; u < P * ne * 9 * nb; u += blockDim.x) {
+      const int bl = u % nb, r = u / nb, ij = r % 9, te = r / 9, e = te % ne, t = te / ne;
+      const int i = ij / 3, j = ij - 3 * i;
+      const int y0 = (bl / nb1) * kWB, x0 = (bl % nb1) * kWB;
+      double2 acc[kWB][kWB];
+#pragma unroll
+      for (int x = 0; x < kWB; ++x)
+#pragma unroll
+        for (int y = 0; y < kWB; ++y) acc[x][y] = make_double2(0.0, 0.0);
+      block_mm<true>(Hl + (t * 3 + j) * NN, No, T + ((t * kWE + e) * 3 + i) * NN, No, y0, x0, No, No, acc);
+      double2* o = Wdst + ((int64_t)(e0 + e) * kRows + t * 9 + ij) * NN;
+#pragma unroll
+      for (int xx = 0; xx < kWB; ++xx)
+#pragma unroll
+        for (int yy = 0; yy < kWB; ++yy)
+          if (y0 + yy < No && x0 + xx < No) o[(x0 + xx) * No + y0 + yy] = acc[yy][xx];
+    }
   }
 }
 
@@ -195,7 +238,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         double2* ws = smem + slot * T::STAGE;
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
         tma_load_5d(ws, &tmW, 2 * xc * C::XC, 0, ec * C::EC, kz, il, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, item.a_in, ec * C::EC + A.shift0, k2, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
         if (++ec == nec) {
           ec = 0;
           if (++xc == nxc) {
@@ -272,9 +315,9 @@ static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   {
-    const uint64_t dims[4] = {2 * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
-    const uint64_t strides[3] = {NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
-    const uint32_t box[4] = {2 * PiCfg::XC, 1, (uint32_t)T::GROWS, 1};
+    const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+    const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
+    const uint32_t box[4] = {2 * PiCfg::XC, (uint32_t)T::GROWS, 1, 1};
     cudaError_t e = make_tmap_f64(&tmG, a.GX, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
@@ -331,15 +374,37 @@ __global__ void k_pi_self(PiSelfArgs A) {
 }
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st) {
-  int64_t nblk = npairs_chunk * a.Nkz * a.nEB;
+cudaError_t launch_pi_w(const PiWArgs& a, int64_t nitems_chunk, cudaStream_t st) {
+  int64_t nblk = nitems_chunk * a.Nkz;
   if (nblk == 0) return cudaSuccess;
-  size_t smem = (size_t)(kEB * a.NN + 6 * a.NN + kEB * 3 * a.NN) * sizeof(double2);
+  PiWArgs b = a;
+  b.nEB = (size_t)kMaxPairs * (6 + 2 + 6) * a.NN * sizeof(double2) <= 220 * 1024 ? 2 : 1;
+  size_t smem = (size_t)kMaxPairs * (6 + 4 * b.nEB) * a.NN * sizeof(double2);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_pi_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k_pi_w<<<(unsigned)nblk, 256, smem, st>>>(a);
+  k_pi_w<<<(unsigned)nblk, 256, smem, st>>>(b);
+  return cudaGetLastError();
+}
+
+// one CTA per (atom, kz): copies the NE x NN block of that atom into its contiguous atom-major slot
+__global__ void __launch_bounds__(256) k_relayout(const double2* __restrict__ in, double2* __restrict__ out,
+                                                  int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN) {
+  const int64_t a = blockIdx.x / Nkz, kz = blockIdx.x % Nkz;
+  double2* o = out + (a * Nkz + kz) * NE * NN;
+  const double2* src = in + (kz * NE * Nwin + a) * NN;
+  const int64_t n = NE * NN;
+  for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int64_t e = idx / NN, uv = idx - e * NN;
+    o[idx] = __ldg(src + e * Nwin * NN + uv);
+  }
+}
+
+cudaError_t launch_relayout(const double2* in, double2* out, int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN,
+                            cudaStream_t st) {
+  if (Nkz * Nwin == 0) return cudaSuccess;
+  k_relayout<<<(unsigned)(Nkz * Nwin), 256, 0, st>>>(in, out, Nkz, NE, Nwin, NN);
   return cudaGetLastError();
 }
 

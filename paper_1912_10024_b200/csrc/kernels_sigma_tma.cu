@@ -5,7 +5,8 @@
 // K = (q, d) with a Hankel G_b operand), reorganized so that the FP64 tensor pipe never waits on
 // block-wide barriers or address arithmetic:
 //   warp 18          : producer. One elected lane issues, per stage, two cp.async.bulk.tensor loads:
-//                      the G_b rows E-Dmax+d0 .. +KC (TMA zero-fills rows outside [0,NE): reading R7,
+//                      the G_b rows E-Dmax+d0 .. +KC from the atom-major copy of G (one contiguous block;
+//                      TMA zero-fills rows outside [0,NE): reading R7,
 //                      and the padding columns Norb²..NPS) and the 72 x KCP coefficient tile.
 //   warps 0..17      : consumers. Warp w owns m-fragment w%9 and half of the n-fragments; it waits on the
 //                      stage's `full` mbarrier, runs DMMA.8x8x4, and releases the stage on `empty`.
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
         const int dd0 = dd_lo + c * C::KC;
         const int kp = (int)imod(kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
         double2* gs = smem + slot * C::STAGE;
-        tma_load_4d(gs, &tmG, 0, item.b_in, E - A.Dmax + dd0, kp, &full[slot]);
+        tma_load_4d(gs, &tmG, 0, E - A.Dmax + dd0, kp, item.b_in, &full[slot]);
         tma_load_4d(gs + C::G_STAGE, &tmC, 2 * dd0, q, 0, (int)(item.pair0 - A.cp0), &full[slot]);
         if (++c == nchunk) {
           c = 0;
@@ -297,10 +298,10 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
   CUtensorMap tmG, tmC;
   const uint64_t NN = (uint64_t)a.NN;
   {
-    const uint64_t dims[4] = {2 * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
-    const uint64_t strides[3] = {NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
-    const uint32_t box[4] = {2 * C::NPS, 1, C::KC, 1};
-    cudaError_t e = make_tmap_f64(&tmG, a.G, 4, dims, strides, box);
+    const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+    const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
+    const uint32_t box[4] = {2 * C::NPS, C::KC, 1, 1};
+    cudaError_t e = make_tmap_f64(&tmG, a.Gam, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
   {

@@ -36,6 +36,8 @@ struct qt_sse_plan_s {
   std::vector<int64_t> sig_chunks, pi_chunks;   // item boundaries
   double2* ws = nullptr;
   size_t ws_bytes = 0;
+  double2* ws_g = nullptr;      // atom-major copies of G^<, G^> [2][Nwin][Nkz][NE][NN]
+  size_t g_elems = 0;
   double flops[4] = {0, 0, 0, 0};
   // host-execute staging
   void* h_dev = nullptr;
@@ -212,6 +214,7 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_pi_pairs);
   cudaFree(p->d_pi_pair_item);
   cudaFree(p->ws);
+  cudaFree(p->ws_g);
   cudaFree(p->h_dev);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
@@ -368,6 +371,11 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     qt_sse_destroy(p);
     return s2;
   }
+  p->g_elems = (size_t)d.Nkz * d.NE * p->Nwin * p->NN;
+  if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess) {
+    qt_sse_destroy(p);
+    return QT_ERR_OUT_OF_MEMORY;
+  }
   if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) {
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
@@ -387,7 +395,7 @@ extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
   o->w_lo = p->w_lo;
   o->w_hi = p->w_hi;
   o->npairs = p->n_pi_pairs;
-  o->workspace_bytes = p->ws_bytes;
+  o->workspace_bytes = p->ws_bytes + 2 * p->g_elems * sizeof(double2);
   o->flops_sigma = p->flops[0] + p->flops[1];
   o->flops_pi = p->flops[2] + p->flops[3];
   o->halo_bytes = 0;
@@ -407,7 +415,8 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
   const size_t sig_bytes = (size_t)d.Nkz * d.NE * p->Nout * p->NN * sizeof(double2);
-  const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp;
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, d.Nkz, d.NE, p->Nwin, p->NN, cs));
   for (int X = 0; X < 2; ++X) {
     void* S = X == 0 ? SL : SG;
     QT_CUDA(cudaMemsetAsync(S, 0, sig_bytes, cs));
@@ -434,6 +443,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       QT_LAUNCH(QT_K_SIGMA_COEF, launch_sigma_coef(ca, cs));
       SigmaArgs sa;
       sa.G = (const double2*)(X == 0 ? GL : GG);
+      sa.Gam = p->ws_g + (X == 0 ? 0 : p->g_elems);
       sa.coef = p->ws;
       sa.cp0 = pp0;
       sa.npairs_chunk = pp1 - pp0;
@@ -471,8 +481,10 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
     if (q == PL || q == PG) return QT_ERR_INVALID_ARG;
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, d.Nkz, d.NE, p->Nwin, p->NN, cs));
   for (int X = 0; X < 2; ++X) {
-    const double2* GX = (const double2*)(X == 0 ? GL : GG);
+    const double2* GXam = p->ws_g + (X == 0 ? 0 : p->g_elems);
     const double2* GY = (const double2*)(X == 0 ? GG : GL);
     double2* P = (double2*)(X == 0 ? PL : PG);
     for (size_t c = 0; c + 1 < p->pi_chunks.size(); ++c) {
@@ -482,6 +494,7 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       const int64_t pp1 = p->pi_items[i1 - 1].pair0 + p->pi_items[i1 - 1].npair;
       PiWArgs wa;
       wa.GY = GY;
+      wa.GYam = p->ws_g + (X == 0 ? p->g_elems : 0);
       wa.dH = (const double2*)dH;
       wa.pairs = p->d_pi_pairs;
       wa.items = p->d_pi_items;
@@ -496,9 +509,9 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       wa.Norb = (int)d.Norb;
       wa.NN = (int)p->NN;
       wa.nEB = (int)((d.NE + kEB - 1) / kEB);
-      QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, pp1 - pp0, cs));
+      QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, i1 - i0, cs));
       PiCArgs ca;
-      ca.GX = GX;
+      ca.GX = GXam;
       ca.W = p->ws;
       ca.items = p->d_pi_items;
       ca.pairs = p->d_pi_pairs;
