@@ -107,8 +107,13 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
   if (tid < P) pairs_s[tid] = A.pairs[item.pair0 + tid];
   __syncthreads();
 
-  const int mi = warp % 9;
-  const bool upper = warp >= 9;
+  // Warp -> (m-fragment, n-half). Warp w runs on SM sub-partition w % 4; the 6-fragment halves go to
+  // the sub-partitions with 5 consumer warps and the 7-fragment halves to those with 4, so the DMMA
+  // counts per sub-partition are 30/31/28/28 (vs 33/32/26/26 for the naive w%9, w/9 split).
+  constexpr int kRole[18] = {9, 14, 1, 5, 10, 15, 2, 6, 11, 16, 3, 7, 12, 17, 4, 8, 13, 0};
+  const int role = warp < C::NCONS ? kRole[warp] : 0;
+  const int mi = role % 9;
+  const bool upper = role >= 9;
   const int f0 = upper ? C::NF0 : 0;
   CAcc acc[C::NF0];
 #pragma unroll
