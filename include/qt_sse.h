@@ -97,10 +97,16 @@ qt_status qt_sse_execute_host(qt_sse_plan_t plan, const void* dH, const void* G_
 
 qt_status qt_sse_query(qt_sse_plan_t plan, qt_sse_info* out);
 
-/* Halo exchange (nranks > 1): fills the halo atoms of the local input window from their
- * owners over NCCL. In-place on the caller's G≷, D≷ buffers (halo part only). */
+/* Halo exchange (nranks > 1, QT_SHARD_ATOM, plan created with an NCCL unique id — then qt_sse_plan is
+ * collective over the ranks): fills the halo atoms of the local input window (atoms owned by other ranks)
+ * from their owners with one grouped ncclSend/ncclRecv round on `cuda_stream`. In-place on the caller's
+ * window buffers; only halo atoms are written, owned atoms are only read. Returns QT_ERR_UNSUPPORTED
+ * when the plan has no communicator, QT_ERR_NCCL on NCCL failure. */
 qt_status qt_sse_halo_exchange(qt_sse_plan_t plan, void* G_less, void* G_gtr, void* D_less, void* D_gtr,
                                void* cuda_stream);
+
+/* Writes a fresh 128-byte ncclUniqueId into out128 (call on one rank, broadcast to the others). */
+qt_status qt_sse_nccl_unique_id(void* out128);
 
 void qt_sse_destroy(qt_sse_plan_t plan);   /* NULL-safe; frees workspace (+ NCCL comm) */
 const char* qt_sse_status_string(qt_status s);
@@ -110,6 +116,10 @@ const char* qt_sse_status_string(qt_status s);
  * (both X, 8 real flops per complex multiply-add, in-window valid-pair work only). */
 qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* neighbors_host, double out[4]);
 
+/* Host-only (no device needed): the qt_sse_info a plan for desc (incl. rank/nranks) would report:
+ * owned atoms, input window, valid pairs, flops, halo bytes received per exchange (workspace = 0). */
+qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* neighbors_host, qt_sse_info* out);
+
 /* Number of this library's kernel launches issued since load (for bench accounting). */
 uint64_t qt_sse_launch_count(void);
 
@@ -118,7 +128,7 @@ uint64_t qt_sse_launch_count(void);
  * returns, per kernel kind (QT_K_*), the summed milliseconds and launch counts since the
  * last reset, then clears them. */
 enum { QT_K_SIGMA_COEF = 0, QT_K_SIGMA = 1, QT_K_PI_W = 2, QT_K_PI_CONTRACT = 3, QT_K_PI_SELF = 4,
-       QT_K_RELAYOUT = 5, QT_K_NKINDS = 6 };
+       QT_K_RELAYOUT = 5, QT_K_HALO = 6, QT_K_NKINDS = 7 };
 qt_status qt_sse_timing_enable(qt_sse_plan_t plan, int enable);
 qt_status qt_sse_timing_read(qt_sse_plan_t plan, double ms[QT_K_NKINDS], int64_t launches[QT_K_NKINDS]);
 

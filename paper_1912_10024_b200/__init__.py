@@ -19,8 +19,9 @@ QT_OK, QT_ERR_INVALID_ARG, QT_ERR_UNSUPPORTED, QT_ERR_OUT_OF_MEMORY, QT_ERR_CUDA
 QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM = range(3)
 EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
-            "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read"]
-KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout"]
+            "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read", "qt_sse_nccl_unique_id",
+            "qt_sse_shard_info"]
+KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout", "k_halo_pack"]
 
 
 class Desc(ctypes.Structure):
@@ -60,10 +61,13 @@ def _load():
     lib.qt_sse_count_flops.argtypes = [ctypes.POINTER(Desc), P, ctypes.POINTER(ctypes.c_double)]
     lib.qt_sse_launch_count.argtypes = []
     lib.qt_sse_launch_count.restype = ctypes.c_uint64
+    lib.qt_sse_nccl_unique_id.argtypes = [P]
+    lib.qt_sse_shard_info.argtypes = [ctypes.POINTER(Desc), P, ctypes.POINTER(Info)]
     lib.qt_sse_timing_enable.argtypes = [P, I]
     lib.qt_sse_timing_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     for f in ("qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
-              "qt_sse_halo_exchange", "qt_sse_count_flops", "qt_sse_timing_enable", "qt_sse_timing_read"):
+              "qt_sse_halo_exchange", "qt_sse_count_flops", "qt_sse_timing_enable", "qt_sse_timing_read",
+              "qt_sse_nccl_unique_id", "qt_sse_shard_info"):
         getattr(lib, f).restype = I
     return lib
 
@@ -90,10 +94,17 @@ def _check(rc: int, what: str) -> None:
         raise QTError(f"{what}: {_get_lib().qt_sse_status_string(rc).decode()} (status {rc})")
 
 
-def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0) -> Desc:
+def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0, unique_id=None) -> Desc:
     """Desc from a qtgen.Problem-like object (Na, Nb, Norb, NE, Nw, Nkz, Nqz, shift0, shift_step)."""
     return Desc(p.Na, p.Nb, p.Norb, 3, p.NE, p.Nw, p.Nkz, p.Nqz, p.shift0, p.shift_step, 0, shard, rank, nranks,
-                None, workspace_limit)
+                unique_id, workspace_limit)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for a sharded plan (create on one rank, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_get_lib().qt_sse_nccl_unique_id(buf), "qt_sse_nccl_unique_id")
+    return buf.raw
 
 
 def count_flops(p) -> dict:
@@ -103,6 +114,15 @@ def count_flops(p) -> dict:
     _check(_get_lib().qt_sse_count_flops(ctypes.byref(d), nbr.ctypes.data, out), "qt_sse_count_flops")
     return dict(sigma_contraction=out[0], sigma_sandwich=out[1], pi_sandwich=out[2], pi_contraction=out[3],
                 total=sum(out))
+
+
+def shard_info(p, rank: int, nranks: int) -> dict:
+    """Host-only: owned atoms [a_lo,a_hi), input window [w_lo,w_hi), pairs, flops, halo bytes of a rank."""
+    d = make_desc(p, rank=rank, nranks=nranks, shard=QT_SHARD_ATOM if nranks > 1 else QT_SHARD_NONE)
+    i = Info()
+    nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
+    _check(_get_lib().qt_sse_shard_info(ctypes.byref(d), nbr.ctypes.data, ctypes.byref(i)), "qt_sse_shard_info")
+    return {k: getattr(i, k) for k, _ in Info._fields_}
 
 
 def launch_count() -> int:
@@ -122,8 +142,10 @@ def _stream(stream):
 class Plan:
     """Owns a qt_sse_plan_t (workspace, work lists) for one problem shape."""
 
-    def __init__(self, p, stream=None, workspace_limit=0, rank=0, nranks=1, shard=QT_SHARD_NONE):
-        self.desc = make_desc(p, rank=rank, nranks=nranks, shard=shard, workspace_limit=workspace_limit)
+    def __init__(self, p, stream=None, workspace_limit=0, rank=0, nranks=1, shard=QT_SHARD_NONE, unique_id=None):
+        self._uid = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
+        self.desc = make_desc(p, rank=rank, nranks=nranks, shard=shard, workspace_limit=workspace_limit,
+                              unique_id=None if self._uid is None else ctypes.addressof(self._uid))
         self._nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
         h = ctypes.c_void_p()
         _check(_get_lib().qt_sse_plan(ctypes.byref(self.desc), self._nbr.ctypes.data, _stream(stream), ctypes.byref(h)),
@@ -150,6 +172,11 @@ class Plan:
                                        sig_scale.real, sig_scale.imag, pi_scale.real, pi_scale.imag, _ptr(S_less),
                                        _ptr(S_gtr), _ptr(P_less), _ptr(P_gtr), _stream(stream)),
                "qt_sse_execute_host")
+
+    def halo_exchange(self, G_less, G_gtr, D_less, D_gtr, stream=None):
+        """Fill the halo atoms of this rank's input window from their owners (NCCL, in place)."""
+        _check(_get_lib().qt_sse_halo_exchange(self.h, _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
+                                               _stream(stream)), "qt_sse_halo_exchange")
 
     def timing(self, enable: bool = True):
         _check(_get_lib().qt_sse_timing_enable(self.h, int(enable)), "qt_sse_timing_enable")

@@ -19,6 +19,18 @@ PKG = ROOT / "paper_1912_10024_b200"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
+
+def _nccl_dir() -> Path:
+    """NCCL of the torch wheel (nvidia-nccl), so one libnccl.so.2 lives in the process with torch's."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.nccl (torch's NCCL wheel) not found")
+    return Path(list(spec.submodule_search_locations)[0])
+
+
+NCCL_DIR = _nccl_dir()
+
 TARGETS = {
     "libqtsse": dict(
         out=PKG / "libqtsse.so",
@@ -26,7 +38,8 @@ TARGETS = {
         deps=sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "qt_sse.h"],
         cmd=lambda srcs, out: [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
                                "-Xcompiler", "-fPIC,-O2", "-shared", f"-I{ROOT / 'include'}",
-                               *map(str, srcs), "-o", str(out), "-lcudart"],
+                               f"-I{NCCL_DIR / 'include'}", *map(str, srcs), "-o", str(out), "-lcudart",
+                               f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{NCCL_DIR / 'lib'}"],
     ),
     "qtgen_dev": dict(
         out=ROOT / "qtgen" / "libqtgen_dev.so",

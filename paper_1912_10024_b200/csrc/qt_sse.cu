@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "qt_sse.h"
+#include "halo.cuh"
 
 #include "kernels_decl.cuh"
 
@@ -42,6 +43,12 @@ struct qt_sse_plan_s {
   // host-execute staging
   void* h_dev = nullptr;
   size_t h_dev_bytes = 0;
+  // atom-halo exchange (nranks > 1)
+  void* comm = nullptr;
+  std::vector<HaloPeer> peers;
+  char* sendbuf = nullptr;
+  char* recvbuf = nullptr;
+  size_t send_total = 0, recv_total = 0;
   // per-kernel timing (qt_sse_timing_*)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -172,7 +179,29 @@ void owned_range(const qt_sse_desc* d, const int32_t* nbr, int64_t* lo, int64_t*
   *hi = d->rank == d->nranks - 1 ? d->Na : cut(d->rank + 1);
 }
 
+// input window of a rank: its owned atoms plus every neighbour of them (contiguous hull)
+void rank_window(const qt_sse_desc* d, const int32_t* nbr, int r, int64_t* a_lo, int64_t* a_hi, int64_t* w_lo,
+                 int64_t* w_hi) {
+  qt_sse_desc e = *d;
+  e.rank = r;
+  owned_range(&e, nbr, a_lo, a_hi);
+  *w_lo = *a_lo;
+  *w_hi = *a_hi;
+  for (int64_t a = *a_lo; a < *a_hi; ++a)
+    for (int64_t s = 0; s < d->Nb; ++s) {
+      const int32_t b = nbr[a * d->Nb + s];
+      if (b < 0) continue;
+      *w_lo = std::min<int64_t>(*w_lo, b);
+      *w_hi = std::max<int64_t>(*w_hi, b + 1);
+    }
+}
+
 }  // namespace
+
+extern "C" qt_status qt_sse_nccl_unique_id(void* out128) {
+  if (!out128) return QT_ERR_INVALID_ARG;
+  return nccl_unique_id(out128) == 0 ? QT_OK : QT_ERR_NCCL;
+}
 
 extern "C" const char* qt_sse_status_string(qt_status s) {
   switch (s) {
@@ -204,6 +233,35 @@ extern "C" qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* 
   return QT_OK;
 }
 
+extern "C" qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* nbr, qt_sse_info* o) {
+  qt_status st = validate_desc(desc);
+  if (st == QT_ERR_UNSUPPORTED) st = QT_OK;
+  if (st != QT_OK) return st;
+  if (!o) return QT_ERR_INVALID_ARG;
+  if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
+  rank_window(desc, nbr, desc->rank, &o->a_lo, &o->a_hi, &o->w_lo, &o->w_hi);
+  double np = 0;
+  for (int64_t a = o->a_lo; a < o->a_hi; ++a)
+    for (int64_t s = 0; s < desc->Nb; ++s) np += nbr[a * desc->Nb + s] >= 0;
+  double f[4];
+  count_flops(desc, np, f);
+  o->npairs = (int64_t)np;
+  o->workspace_bytes = 0;
+  o->flops_sigma = f[0] + f[1];
+  o->flops_pi = f[2] + f[3];
+  double recv = 0;
+  const double per_atom = 2.0 * desc->Nkz * desc->NE * desc->Norb * desc->Norb * 16 +
+                          2.0 * desc->Nqz * desc->Nw * (desc->Nb + 1) * 9 * 16;
+  for (int r = 0; r < desc->nranks; ++r) {
+    if (r == desc->rank) continue;
+    int64_t alo, ahi, wlo, whi;
+    rank_window(desc, nbr, r, &alo, &ahi, &wlo, &whi);
+    recv += std::max<int64_t>(0, std::min(o->w_hi, ahi) - std::max(o->w_lo, alo)) * per_atom;
+  }
+  o->halo_bytes = recv;
+  return QT_OK;
+}
+
 extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   if (!p) return;
   cudaFree(p->d_nbr_win);
@@ -215,6 +273,9 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_pi_pair_item);
   cudaFree(p->ws);
   cudaFree(p->ws_g);
+  cudaFree(p->sendbuf);
+  cudaFree(p->recvbuf);
+  nccl_comm_destroy(p->comm);
   cudaFree(p->h_dev);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
@@ -247,17 +308,31 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   p->DWp = (p->Dwin + 3) & ~3LL;
   p->NWP = (d.Nw + 7) & ~7LL;
   p->nbr.assign(nbr, nbr + d.Na * d.Nb);
-  owned_range(&d, nbr, &p->a_lo, &p->a_hi);
-  // input window: owned atoms + every neighbour (contiguous hull)
-  p->w_lo = p->a_lo;
-  p->w_hi = p->a_hi;
-  for (int64_t a = p->a_lo; a < p->a_hi; ++a)
-    for (int64_t s = 0; s < d.Nb; ++s) {
-      int32_t b = nbr[a * d.Nb + s];
-      if (b < 0) continue;
-      p->w_lo = std::min<int64_t>(p->w_lo, b);
-      p->w_hi = std::max<int64_t>(p->w_hi, b + 1);
+  rank_window(&d, nbr, d.rank, &p->a_lo, &p->a_hi, &p->w_lo, &p->w_hi);
+  // halo exchange plan: receive window atoms owned by peers, send owned atoms in the peers' windows
+  if (d.nranks > 1) {
+    const size_t per_atom = 2 * (size_t)d.Nkz * d.NE * d.Norb * d.Norb * 16 + 2 * (size_t)d.Nqz * d.Nw * (d.Nb + 1) * 9 * 16;
+    for (int r = 0; r < d.nranks; ++r) {
+      if (r == d.rank) continue;
+      int64_t alo, ahi, wlo, whi;
+      rank_window(&d, nbr, r, &alo, &ahi, &wlo, &whi);
+      HaloPeer h;
+      h.rank = r;
+      const int64_t rl = std::max(p->w_lo, alo), rh = std::min(p->w_hi, ahi);
+      const int64_t sl = std::max(p->a_lo, wlo), sh = std::min(p->a_hi, whi);
+      h.recv_lo = rl - p->w_lo;
+      h.recv_n = std::max<int64_t>(0, rh - rl);
+      h.send_lo = sl - p->w_lo;
+      h.send_n = std::max<int64_t>(0, sh - sl);
+      h.recv_bytes = h.recv_n * per_atom;
+      h.send_bytes = h.send_n * per_atom;
+      h.recv_off = p->recv_total;
+      h.send_off = p->send_total;
+      p->recv_total += h.recv_bytes;
+      p->send_total += h.send_bytes;
+      if (h.recv_n || h.send_n) p->peers.push_back(h);
     }
+  }
   p->Nwin = p->w_hi - p->w_lo;
   p->Nout = p->a_hi - p->a_lo;
   p->nbr_win.assign(p->Nwin * d.Nb, -1);
@@ -376,6 +451,17 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
   }
+  if (d.nranks > 1 && d.nccl_unique_id) {
+    if ((p->send_total && cudaMalloc(&p->sendbuf, p->send_total) != cudaSuccess) ||
+        (p->recv_total && cudaMalloc(&p->recvbuf, p->recv_total) != cudaSuccess)) {
+      qt_sse_destroy(p);
+      return QT_ERR_OUT_OF_MEMORY;
+    }
+    if (nccl_comm_init(&p->comm, d.nranks, d.nccl_unique_id, d.rank) != 0) {
+      qt_sse_destroy(p);
+      return QT_ERR_NCCL;
+    }
+  }
   if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) {
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
@@ -398,7 +484,7 @@ extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
   o->workspace_bytes = p->ws_bytes + 2 * p->g_elems * sizeof(double2);
   o->flops_sigma = p->flops[0] + p->flops[1];
   o->flops_pi = p->flops[2] + p->flops[3];
-  o->halo_bytes = 0;
+  o->halo_bytes = (double)p->recv_total;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? QT_OK : cuda_status(e);
 }
@@ -584,10 +670,33 @@ extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const 
   return QT_OK;
 }
 
-extern "C" qt_status qt_sse_halo_exchange(qt_sse_plan_t p, void*, void*, void*, void*, void*) {
+extern "C" qt_status qt_sse_halo_exchange(qt_sse_plan_t p, void* GL, void* GG, void* DL, void* DG, void* stream) {
   if (!p) return QT_ERR_INVALID_ARG;
   if (p->d.nranks == 1) return QT_OK;
-  return QT_ERR_UNSUPPORTED;
+  if (!p->comm) return QT_ERR_UNSUPPORTED;   // planned without an NCCL unique id
+  void* ts[4] = {GL, GG, DL, DG};
+  for (void* t : ts)
+    if (!aligned16(t)) return QT_ERR_INVALID_ARG;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const qt_sse_desc& d = p->d;
+  const int64_t outer[4] = {d.Nkz * d.NE, d.Nkz * d.NE, d.Nqz * d.Nw, d.Nqz * d.Nw};
+  const int64_t inner[4] = {p->NN * 16, p->NN * 16, (d.Nb + 1) * 9 * 16, (d.Nb + 1) * 9 * 16};
+  for (const HaloPeer& h : p->peers) {
+    size_t off = h.send_off;
+    for (int k = 0; k < 4; ++k) {
+      QT_LAUNCH(QT_K_HALO, launch_pack(ts[k], p->sendbuf + off, outer[k], p->Nwin, h.send_lo, h.send_n, inner[k], false, cs));
+      off += (size_t)outer[k] * h.send_n * inner[k];
+    }
+  }
+  if (nccl_exchange(p->comm, p->peers, p->sendbuf, p->recvbuf, cs) != 0) return QT_ERR_NCCL;
+  for (const HaloPeer& h : p->peers) {
+    size_t off = h.recv_off;
+    for (int k = 0; k < 4; ++k) {
+      QT_LAUNCH(QT_K_HALO, launch_pack(p->recvbuf + off, ts[k], outer[k], p->Nwin, h.recv_lo, h.recv_n, inner[k], true, cs));
+      off += (size_t)outer[k] * h.recv_n * inner[k];
+    }
+  }
+  return QT_OK;
 }
 
 extern "C" qt_status qt_sse_timing_enable(qt_sse_plan_t p, int enable) {
