@@ -295,7 +295,6 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   qt_status st = validate_desc(desc);
   if (st != QT_OK) return st;
   if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
-  if (desc->nranks > 1 && desc->nccl_unique_id != nullptr) return QT_ERR_UNSUPPORTED;  // NCCL halo: NEXT
   cudaStream_t cs = (cudaStream_t)stream;
   qt_sse_plan_s* p = new (std::nothrow) qt_sse_plan_s();
   if (!p) return QT_ERR_OUT_OF_MEMORY;
