@@ -26,6 +26,20 @@ __device__ __forceinline__ void cmma(CAcc& c, double ar, double ai, double nai, 
   dmma(c.i0, c.i1, ai, br);
 }
 
+// Gauss 3M complex product on three real accumulators: T1 += Ar·Br, T2 += Ai·Bi,
+// T3 += (Ar+Ai)(Br+Bi); value = (T1 - T2) + i (T3 - T1 - T2). as = ar + ai (computed once per A fragment).
+struct C3Acc {
+  double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
+  __device__ __forceinline__ double2 value(int k) const {
+    return make_double2(t1[k] - t2[k], (t3[k] - t1[k]) - t2[k]);
+  }
+};
+__device__ __forceinline__ void cmma3(C3Acc& c, double ar, double ai, double as, double br, double bi) {
+  dmma(c.t1[0], c.t1[1], ar, br);
+  dmma(c.t2[0], c.t2[1], ai, bi);
+  dmma(c.t3[0], c.t3[1], as, br + bi);
+}
+
 // 16-byte async global->shared copy; src_valid == false zero-fills the destination.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool src_valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);

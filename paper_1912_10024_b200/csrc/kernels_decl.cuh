@@ -23,8 +23,9 @@ struct SigmaArgs {
   const SigItem* items;
   const SigPair* pairs;
   double2* Sig;
+  double2* Gt;           // Gt scratch of the chunk [item][kz][E][72][NN] (TMA path)
   double2 scale;
-  int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk;
+  int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk, ntiles;
   int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin;
 };
 

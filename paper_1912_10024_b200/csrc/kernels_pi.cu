@@ -129,29 +129,21 @@ struct PiTma {
   static constexpr size_t SMEM = (size_t)PiCfg::STAGES * STAGE * 16 + 2 * PiCfg::STAGES * 8 + 128;
 };
 
-// DMMA work of one stage for one warp (NFW column fragments starting at f0).
-// Complex k-step over N column fragments (compile-time N): (re·re, re·im) for fragment f, then
-// (-im·im, im·re) for fragment f-1, so the two DMMAs on one accumulator are never adjacent.
+// Complex k-step over N column fragments with Gauss's 3-multiplication form: per fragment
+// T1 += Ar·Br, T2 += Ai·Bi, T3 += (Ar+Ai)(Br+Bi) (three real DMMAs instead of four); the complex
+// result is Re = T1 - T2, Im = T3 - T1 - T2 (formed once, in the epilogue).
 template <int N>
-__device__ __forceinline__ void pi_kstep(CAcc* acc, double2 a, const double2* gb) {
-  double2 bp = gb[0];
-  dmma(acc[0].r0, acc[0].r1, a.x, bp.x);
-  dmma(acc[0].i0, acc[0].i1, a.x, bp.y);
+__device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, const double2* gb) {
+  const double as = a.x + a.y;
 #pragma unroll
-  for (int f = 1; f < N; ++f) {
+  for (int f = 0; f < N; ++f) {
     const double2 b = gb[f * 8 * PiCfg::XC];
-    dmma(acc[f].r0, acc[f].r1, a.x, b.x);
-    dmma(acc[f].i0, acc[f].i1, a.x, b.y);
-    dmma(acc[f - 1].r0, acc[f - 1].r1, -a.y, bp.y);
-    dmma(acc[f - 1].i0, acc[f - 1].i1, a.y, bp.x);
-    bp = b;
+    cmma3(acc[f], a.x, a.y, as, b.x, b.y);
   }
-  dmma(acc[N - 1].r0, acc[N - 1].r1, -a.y, bp.y);
-  dmma(acc[N - 1].i0, acc[N - 1].i1, a.y, bp.x);
 }
 
 template <int N>
-__device__ __forceinline__ void pi_energy(CAcc* acc, const double2* ws, const double2* gs) {
+__device__ __forceinline__ void pi_energy(C3Acc* acc, const double2* ws, const double2* gs) {
 #pragma unroll
   for (int k4 = 0; k4 < PiCfg::XC; k4 += 4) pi_kstep<N>(acc, ws[k4], gs + k4);
 }
@@ -159,7 +151,7 @@ __device__ __forceinline__ void pi_energy(CAcc* acc, const double2* ws, const do
 // DMMA work of one stage for one warp. rem = NE - E0 - shift0: energy E0+el has in-window columns
 // m < rem - el; column fragments without any are skipped (fast path: all NFW fragments live).
 template <int NFW>
-__device__ __forceinline__ void pi_stage(CAcc* acc, const double2* ws, const double2* gs, int rem, int f0) {
+__device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double2* gs, int rem, int f0) {
   static_assert(NFW > 0, "empty fragment range");
   using C = PiCfg;
 #pragma unroll
@@ -173,14 +165,12 @@ __device__ __forceinline__ void pi_stage(CAcc* acc, const double2* ws, const dou
 #pragma unroll
       for (int k4 = 0; k4 < C::XC; k4 += 4) {
         const double2 a = w[k4];
+        const double as = a.x + a.y;
 #pragma unroll
         for (int f = 0; f < NFW; ++f) {
           if (f < nfe) {
             const double2 b = g[k4 + f * 8 * C::XC];
-            dmma(acc[f].r0, acc[f].r1, a.x, b.x);
-            dmma(acc[f].i0, acc[f].i1, a.x, b.y);
-            dmma(acc[f].r0, acc[f].r1, -a.y, b.y);
-            dmma(acc[f].i0, acc[f].i1, a.y, b.x);
+            cmma3(acc[f], a.x, a.y, as, b.x, b.y);
           }
         }
       }
@@ -222,9 +212,9 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   const int mi = warp % 9;
   const bool upper = warp >= 9;
   const int f0 = upper ? T::NF0 : 0;
-  CAcc acc[T::NF0];
+  C3Acc acc[T::NF0];
 #pragma unroll
-  for (int f = 0; f < T::NF0; ++f) acc[f] = CAcc{0.0, 0.0, 0.0, 0.0};
+  for (int f = 0; f < T::NF0; ++f) acc[f] = C3Acc{};
 
   if (warp == C::NCONS) {
     if (lane == 0) {
@@ -280,11 +270,9 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
           if (f < nfw) {
             const int m0 = (f0 + f) * 8 + 2 * (lane & 3);
             if (m0 < A.Nw)
-              A.Pi[((int64_t)qz * A.Nw + m0) * A.Nout * (A.Nb + 1) * 9 + base] =
-                  cmul(A.scale, make_double2(acc[f].r0, acc[f].i0));
+              A.Pi[((int64_t)qz * A.Nw + m0) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(0));
             if (m0 + 1 < A.Nw)
-              A.Pi[((int64_t)qz * A.Nw + m0 + 1) * A.Nout * (A.Nb + 1) * 9 + base] =
-                  cmul(A.scale, make_double2(acc[f].r1, acc[f].i1));
+              A.Pi[((int64_t)qz * A.Nw + m0 + 1) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(1));
           }
         }
       }

@@ -16,87 +16,87 @@
 
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 namespace qt {
 
 template <int NF>
 struct SigTmaCfg {
-  static constexpr int NP = 8 * NF;
-  static constexpr int NPS = NP + 2;        // ≡ 2 (mod 8): conflict-free B-fragment LDS.128
-  static constexpr int KC = 16;             // d values per stage (4 DMMA k-steps)
-  static constexpr int KCP = 20;            // ≡ 4 (mod 8): conflict-free A-fragment LDS.128
-  static constexpr int STAGES = 4;
-  static constexpr int G_STAGE = KC * NPS;  // complex elements
+  static constexpr int NFH0 = (NF + 1) / 2;  // n-fragments of column half 0
+  static constexpr int NFH1 = NF / 2;        // n-fragments of column half 1
+  static constexpr int NPS = NFH0 * 8 + 2;   // ≡ 2 (mod 8): conflict-free B-fragment LDS.128
+  static constexpr int KC = 16;              // d values per stage (4 DMMA k-steps)
+  static constexpr int KCP = 20;             // ≡ 4 (mod 8): conflict-free A-fragment LDS.128
+  static constexpr int STAGES = 5;
+  static constexpr int G_STAGE = KC * NPS;   // complex elements
   static constexpr int C_STAGE = kRows * KCP;
   static constexpr int STAGE = G_STAGE + C_STAGE;
   static constexpr uint32_t STAGE_BYTES = STAGE * 16;
   static constexpr int PIPE = STAGES * STAGE;
-  static constexpr int GT = kRows * NPS;
-  static constexpr int VS = kMaxPairs * 3 * NP;
-  static constexpr int HR = kMaxPairs * 3 * NP;
-  static constexpr int EPI = GT + VS + HR;
-  static constexpr int REGION = PIPE > EPI ? PIPE : EPI;
-  static constexpr int NCONS = 18;          // consumer warps
+  static constexpr int NCONS = 18;           // consumer warps: (m-fragment, half of the half-tile's n-frags)
   static constexpr int THREADS = (NCONS + 1) * 32;
-  static constexpr int NF0 = (NF + 1) / 2;  // n-fragments of warps 0..8
-  static constexpr int NF1 = NF / 2;        // n-fragments of warps 9..17
-  static constexpr size_t SMEM = (size_t)REGION * 16 + 2 * STAGES * 8 + kMaxPairs * sizeof(SigPair) + 128;
+  static constexpr int TMAXW = (NFH0 + 1) / 2;   // n-fragments per consumer warp (max)
+  static constexpr size_t SMEM = (size_t)PIPE * 16 + 2 * STAGES * 8 + 128;
   static_assert(2 * NPS <= 256, "TMA box width");
   static_assert((G_STAGE * 16) % 128 == 0 && (STAGE * 16) % 128 == 0, "TMA destination alignment");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-// One stage of DMMA work for a warp: NFW n-fragments, kc/4 k-steps. Complex product on split
-// accumulators, ordered so the two DMMAs that update the same accumulator are never adjacent and only
-// two B fragments are live: (re·re, re·im) for fragment f, then (-im·im, im·re) for fragment f-1.
+// One stage of DMMA work for a consumer warp with NFW n-fragments (Gauss 3M complex product: three
+// real DMMAs per complex 8x8x4 step, see C3Acc).
 template <int NFW, int NPS, int KC>
-__device__ __forceinline__ void sigma_stage(CAcc* acc, const double2* gs, const double2* cs, int kc) {
+__device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const double2* cs, int kc) {
   static_assert(NFW > 0, "empty fragment range");
 #pragma unroll
   for (int k4 = 0; k4 < KC; k4 += 4) {
     if (k4 < kc) {
       const double2 a = cs[k4];
+      const double as = a.x + a.y;
       const double2* gb = gs + k4 * NPS;
-      double2 bp = gb[0];
-      dmma(acc[0].r0, acc[0].r1, a.x, bp.x);
-      dmma(acc[0].i0, acc[0].i1, a.x, bp.y);
 #pragma unroll
-      for (int f = 1; f < NFW; ++f) {
+      for (int f = 0; f < NFW; ++f) {
         const double2 b = gb[f * 8];
-        dmma(acc[f].r0, acc[f].r1, a.x, b.x);
-        dmma(acc[f].i0, acc[f].i1, a.x, b.y);
-        dmma(acc[f - 1].r0, acc[f - 1].r1, -a.y, bp.y);
-        dmma(acc[f - 1].i0, acc[f - 1].i1, a.y, bp.x);
-        bp = b;
+        cmma3(acc[f], a.x, a.y, as, b.x, b.y);
       }
-      dmma(acc[NFW - 1].r0, acc[NFW - 1].r1, -a.y, bp.y);
-      dmma(acc[NFW - 1].i0, acc[NFW - 1].i1, a.y, bp.x);
     }
   }
 }
 
+struct SigTile {
+  SigItem item;
+  int E, kz, ch, il, dd_lo, dd_hi, nchunk, nst;
+};
+
+template <int KC>
+__device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
+  SigTile T;
+  T.ch = (int)(t & 1);
+  t >>= 1;
+  T.E = (int)(t % A.NE);
+  T.kz = (int)((t / A.NE) % A.Nkz);
+  T.il = (int)(t / ((int64_t)A.NE * A.Nkz));
+  T.item = A.items[T.il];
+  // K range: d with E+d in [0,NE) (R7), rounded to the k=4 step; chunks of KC per q.
+  T.dd_lo = max(0, A.Dmax - T.E) & ~3;
+  T.dd_hi = (min(A.Dwin, A.Dmax - T.E + A.NE) + 3) & ~3;
+  T.nchunk = (T.dd_hi - T.dd_lo + KC - 1) / KC;
+  T.nst = A.Nqz * T.nchunk;
+  return T;
+}
+
+// Persistent: CTA c processes tiles c, c + gridDim.x, ... with tile = (item, kz, E, column half).
+// The producer streams stages across tile boundaries; consumers store each finished tile of Gt
+// (complex, from the 3M accumulators) to the chunk's scratch [item][kz][E][72][Norb²].
 template <int NF>
 __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     k_sigma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmC, SigmaArgs A) {
   using C = SigTmaCfg<NF>;
   extern __shared__ uint8_t smem_raw[];
   double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::REGION);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE);
   uint64_t* empty = full + C::STAGES;
-  SigPair* pairs_s = reinterpret_cast<SigPair*>(empty + C::STAGES);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t blk = blockIdx.x;
-  const int E = (int)(blk % A.NE);
-  const int kz = (int)((blk / A.NE) % A.Nkz);
-  const SigItem item = A.items[blk / ((int64_t)A.NE * A.Nkz)];
-  const int P = item.npair;
-
-  // K range: d with E+d in [0,NE) (R7), rounded to the k=4 step; chunks of KC per q.
-  int dd_lo = max(0, A.Dmax - E), dd_hi = min(A.Dwin, A.Dmax - E + A.NE);
-  dd_lo &= ~3;
-  dd_hi = (dd_hi + 3) & ~3;
-  const int nchunk = (dd_hi - dd_lo + C::KC - 1) / C::KC;
-  const int nst = A.Nqz * nchunk;
-
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -104,96 +104,113 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (tid < P) pairs_s[tid] = A.pairs[item.pair0 + tid];
   __syncthreads();
-
-  // Warp -> (m-fragment, n-half). Warp w runs on SM sub-partition w % 4; the 6-fragment halves go to
-  // the sub-partitions with 5 consumer warps and the 7-fragment halves to those with 4, so the DMMA
-  // counts per sub-partition are 30/31/28/28 (vs 33/32/26/26 for the naive w%9, w/9 split).
-  constexpr int kRole[18] = {9, 14, 1, 5, 10, 15, 2, 6, 11, 16, 3, 7, 12, 17, 4, 8, 13, 0};
-  const int role = warp < C::NCONS ? kRole[warp] : 0;
-  const int mi = role % 9;
-  const bool upper = role >= 9;
-  const int f0 = upper ? C::NF0 : 0;
-  CAcc acc[C::NF0];
-#pragma unroll
-  for (int f = 0; f < C::NF0; ++f) acc[f] = CAcc{0.0, 0.0, 0.0, 0.0};
 
   if (warp == C::NCONS) {
     // ---------------- producer
     if (lane == 0) {
       prefetch_tmap(&tmG);
       prefetch_tmap(&tmC);
-      int q = 0, c = 0;
-      for (int st = 0; st < nst; ++st) {
-        const int slot = st & (C::STAGES - 1);
-        if (st >= C::STAGES) mbar_wait(&empty[slot], ((st / C::STAGES) - 1) & 1);
-        static_assert((C::STAGES & (C::STAGES - 1)) == 0, "power-of-two stage count");
-        mbar_arrive_expect_tx(&full[slot], C::STAGE_BYTES);
-        const int dd0 = dd_lo + c * C::KC;
-        const int kp = (int)imod(kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
-        double2* gs = smem + slot * C::STAGE;
-        tma_load_4d(gs, &tmG, 0, E - A.Dmax + dd0, kp, item.b_in, &full[slot]);
-        tma_load_4d(gs + C::G_STAGE, &tmC, 2 * dd0, q, 0, (int)(item.pair0 - A.cp0), &full[slot]);
-        if (++c == nchunk) {
-          c = 0;
-          ++q;
+      uint32_t g = 0;
+      for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
+        const SigTile T = sig_tile<C::KC>(A, t);
+        int q = 0, c = 0;
+        for (int st = 0; st < T.nst; ++st, ++g) {
+          const uint32_t slot = g % C::STAGES;
+          if (g >= C::STAGES) mbar_wait(&empty[slot], ((g / C::STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[slot], C::STAGE_BYTES);
+          const int dd0 = T.dd_lo + c * C::KC;
+          const int kp = (int)imod(T.kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
+          double2* gs = smem + slot * C::STAGE;
+          tma_load_4d(gs, &tmG, T.ch * C::NFH0 * 16, T.E - A.Dmax + dd0, kp, T.item.b_in, &full[slot]);
+          tma_load_4d(gs + C::G_STAGE, &tmC, 2 * dd0, q, 0, (int)(T.item.pair0 - A.cp0), &full[slot]);
+          if (++c == T.nchunk) {
+            c = 0;
+            ++q;
+          }
         }
       }
     }
-  } else {
-    // ---------------- consumers
-    const bool active = mi * 8 < 9 * P;
+    return;
+  }
+
+  // ---------------- consumers: warp -> (m-fragment, quarter q of the n-fragments of the half-tile).
+  // q = 1 warps (fewer fragments) sit on the sub-partitions with 5 consumer warps (warp w runs on w % 4).
+  constexpr int kRole[18] = {9, 14, 1, 5, 10, 15, 2, 6, 11, 16, 3, 7, 12, 17, 4, 8, 13, 0};
+  const int role = kRole[warp];
+  const int mi = role % 9, q = role / 9;
+  const int row = mi * 8 + (lane >> 2);
+  uint32_t g = 0;
+  for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
+    const SigTile T = sig_tile<C::KC>(A, t);
+    const int nfh = T.ch ? C::NFH1 : C::NFH0;
+    const int nfw = q ? nfh / 2 : (nfh + 1) / 2;
+    const int f0 = q ? (nfh + 1) / 2 : 0;
+    const bool active = mi * 8 < 9 * T.item.npair && nfw > 0;
+    C3Acc acc[C::TMAXW];
+#pragma unroll
+    for (int f = 0; f < C::TMAXW; ++f) acc[f] = C3Acc{};
     int c = 0;
-    for (int st = 0; st < nst; ++st) {
-      const int slot = st & (C::STAGES - 1);
-      mbar_wait(&full[slot], (st / C::STAGES) & 1);
+    for (int st = 0; st < T.nst; ++st, ++g) {
+      const uint32_t slot = g % C::STAGES;
+      mbar_wait(&full[slot], (g / C::STAGES) & 1);
       if (active) {
-        const int kc = min(C::KC, dd_hi - (dd_lo + c * C::KC));
+        const int kc = min(C::KC, T.dd_hi - (T.dd_lo + c * C::KC));
         const double2* gs = smem + slot * C::STAGE + (lane & 3) * C::NPS + (lane >> 2) + f0 * 8;
-        const double2* cs = smem + slot * C::STAGE + C::G_STAGE + (mi * 8 + (lane >> 2)) * C::KCP + (lane & 3);
-        if (upper) {
-          if constexpr (C::NF1 > 0) sigma_stage<C::NF1, C::NPS, C::KC>(acc, gs, cs, kc);
+        const double2* cs = smem + slot * C::STAGE + C::G_STAGE + row * C::KCP + (lane & 3);
+        if (nfw == C::TMAXW) {
+          sigma_stage<C::TMAXW, C::NPS, C::KC>(acc, gs, cs, kc);
         } else {
-          sigma_stage<C::NF0, C::NPS, C::KC>(acc, gs, cs, kc);
+          if constexpr (C::TMAXW > 1) sigma_stage<C::TMAXW - 1, C::NPS, C::KC>(acc, gs, cs, kc);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++c == nchunk) c = 0;
+      if (++c == T.nchunk) c = 0;
     }
-  }
-  __syncthreads();   // every stage consumed; the pipeline buffers are free
-
-  // ---- epilogue 1: Gt (72 x NP) -> shared memory; ∇_jH_{b r_t} -> shared memory
-  double2* Gt = smem;
-  double2* Vs = smem + C::GT;
-  double2* Hr = Vs + C::VS;
-  const int NN = A.NN, No = A.Norb;
-  if (warp < C::NCONS && mi * 8 < 9 * P) {
-    const int row = mi * 8 + (lane >> 2);
-    const int nfw = upper ? C::NF1 : C::NF0;
+    if (active && row < 9 * T.item.npair) {
+      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * kRows + row) * A.NN;
 #pragma unroll
-    for (int f = 0; f < C::NF0; ++f) {
-      if (f < nfw) {
-        const int col = (f0 + f) * 8 + 2 * (lane & 3);
-        Gt[row * C::NPS + col] = make_double2(acc[f].r0, acc[f].i0);
-        Gt[row * C::NPS + col + 1] = make_double2(acc[f].r1, acc[f].i1);
+      for (int f = 0; f < C::TMAXW; ++f) {
+        if (f < nfw) {
+          const int col = (T.ch * C::NFH0 + f0 + f) * 8 + 2 * (lane & 3);
+          if (col < A.NN) out[col] = acc[f].value(0);
+          if (col + 1 < A.NN) out[col + 1] = acc[f].value(1);
+        }
       }
     }
   }
-  for (int idx = tid; idx < P * 3 * NN; idx += C::THREADS) {
+}
+
+// ---------------------------------------------------------------- Σ sandwich + neighbour sum
+// Σ_a(kz,E) += scale · Σ_i ∇_iH_{a s} (Σ_j Gt^{ij} ∇_jH_{b r}) for every pair of the chunk's items (R8).
+// One CTA per (item, kz, E); Gt block and ∇H blocks staged in shared memory; register-blocked DFMA.
+__global__ void __launch_bounds__(256) k_sigma_sand(SigmaArgs A) {
+  extern __shared__ __align__(16) double2 sm[];
+  const int NN = A.NN, No = A.Norb;
+  const int64_t blk = blockIdx.x;
+  const int E = (int)(blk % A.NE);
+  const int kz = (int)((blk / A.NE) % A.Nkz);
+  const int il = (int)(blk / ((int64_t)A.NE * A.Nkz));
+  const SigItem item = A.items[il];
+  const int P = item.npair;
+  double2* Gt = sm;                       // [9P][NN]
+  double2* Hr = Gt + kRows * NN;          // [P][3][NN]
+  double2* Hl = Hr + kMaxPairs * 3 * NN;  // [P][3][NN]
+  double2* Vs = Hl + kMaxPairs * 3 * NN;  // [P][3][NN]
+  const double2* src = A.Gt + (((int64_t)il * A.Nkz + kz) * A.NE + E) * kRows * NN;
+  for (int idx = threadIdx.x; idx < 9 * P * NN; idx += blockDim.x) Gt[idx] = src[idx];
+  for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
     const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
-    Hr[t * 3 * C::NP + rem] = A.dH[((int64_t)item.b_in * A.Nb + pairs_s[t].r) * 3 * NN + rem];
+    const SigPair pr = A.pairs[item.pair0 + t];
+    Hr[idx] = A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem];
+    Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
   }
   __syncthreads();
-
-  // Register-blocked sandwich: each thread owns a 2 x YB output block (rows x, x+1; columns y0..y0+YB-1).
   constexpr int YB = 5;
   const int nxb = (No + 1) >> 1, nyb = (No + YB - 1) / YB;
-  // ---- epilogue 2: V^i_t = Σ_j Gt^{ij}_t · ∇_jH_{b r_t}
-  for (int idx = tid; idx < P * 3 * nxb * nyb; idx += C::THREADS) {
-    const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, ti = r1 / nxb;   // ti = t*3 + i
+  for (int idx = threadIdx.x; idx < P * 3 * nxb * nyb; idx += blockDim.x) {   // V^i = Σ_j Gt^{ij} ∇_jH_{br}
+    const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, ti = r1 / nxb;
     const int t = ti / 3, i = ti - 3 * t, x0 = 2 * xb, y0 = yb * YB;
     double2 s[2][YB];
 #pragma unroll
@@ -201,8 +218,8 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 #pragma unroll
       for (int w = 0; w < YB; ++w) s[u][w] = make_double2(0.0, 0.0);
     for (int j = 0; j < 3; ++j) {
-      const double2* g0 = Gt + (t * 9 + i * 3 + j) * C::NPS + x0 * No;
-      const double2* hr = Hr + t * 3 * C::NP + j * NN + y0;
+      const double2* g0 = Gt + (t * 9 + i * 3 + j) * NN + x0 * No;
+      const double2* hr = Hr + (t * 3 + j) * NN + y0;
       for (int v = 0; v < No; ++v) {
         const double2 ga = g0[v], gb = (x0 + 1 < No) ? g0[No + v] : make_double2(0.0, 0.0);
 #pragma unroll
@@ -217,20 +234,10 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int w = 0; w < YB; ++w)
-        if (x0 + u < No && y0 + w < No) Vs[ti * C::NP + (x0 + u) * No + y0 + w] = s[u][w];
+        if (x0 + u < No && y0 + w < No) Vs[ti * NN + (x0 + u) * No + y0 + w] = s[u][w];
   }
   __syncthreads();
-  // ∇_iH_{a_t s_t} -> shared memory (reuses the Gt region)
-  double2* Hl = smem;
-  for (int idx = tid; idx < P * 3 * NN; idx += C::THREADS) {
-    const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
-    const SigPair pr = pairs_s[t];
-    Hl[t * 3 * C::NP + rem] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
-  }
-  __syncthreads();
-
-  // ---- epilogue 3: S_t = Σ_i ∇_iH_{a_t s_t} · V^i_t; Σ_a += scale · S_t (R8)
-  for (int idx = tid; idx < P * nxb * nyb; idx += C::THREADS) {
+  for (int idx = threadIdx.x; idx < P * nxb * nyb; idx += blockDim.x) {       // S = Σ_i ∇_iH_{as} V^i
     const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, t = r1 / nxb;
     const int x0 = 2 * xb, y0 = yb * YB;
     double2 s[2][YB];
@@ -239,8 +246,8 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 #pragma unroll
       for (int w = 0; w < YB; ++w) s[u][w] = make_double2(0.0, 0.0);
     for (int i = 0; i < 3; ++i) {
-      const double2* hl = Hl + t * 3 * C::NP + i * NN + x0 * No;
-      const double2* v = Vs + (t * 3 + i) * C::NP + y0;
+      const double2* hl = Hl + (t * 3 + i) * NN + x0 * No;
+      const double2* v = Vs + (t * 3 + i) * NN + y0;
       for (int u = 0; u < No; ++u) {
         const double2 ha = hl[u], hb = (x0 + 1 < No) ? hl[No + u] : make_double2(0.0, 0.0);
 #pragma unroll
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
         }
       }
     }
-    const SigPair pr = pairs_s[t];
+    const SigPair pr = A.pairs[item.pair0 + t];
     double2* out = A.Sig + (((int64_t)kz * A.NE + E) * A.Nout + pr.a) * NN;
 #pragma unroll
     for (int u = 0; u < 2; ++u)
@@ -259,9 +266,8 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       for (int w = 0; w < YB; ++w)
         if (x0 + u < No && y0 + w < No) {
           const double2 r = cmul(A.scale, s[u][w]);
-          double* dst = reinterpret_cast<double*>(out + (x0 + u) * No + y0 + w);
-          atomicAdd(dst, r.x);
-          atomicAdd(dst + 1, r.y);
+          atomicAdd(reinterpret_cast<double*>(out + (x0 + u) * No + y0 + w), r.x);
+          atomicAdd(reinterpret_cast<double*>(out + (x0 + u) * No + y0 + w) + 1, r.y);
         }
   }
 }
@@ -317,10 +323,27 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     cudaError_t e = make_tmap_f64(&tmC, a.coef, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
-  const int64_t nblk = nitems * a.NE * a.Nkz;
-  if (nblk == 0) return cudaSuccess;
-  if (nblk > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  k_sigma<NF><<<(unsigned)nblk, C::THREADS, C::SMEM, st>>>(tmG, tmC, a);
+  SigmaArgs b = a;
+  b.ntiles = nitems * a.NE * a.Nkz * 2;
+  if (b.ntiles == 0) return cudaSuccess;
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t grid = std::min<int64_t>(b.ntiles, nsm);
+  k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmC, b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)(kRows + 3 * 3 * kMaxPairs) * a.NN * 16;
+  static bool cfg2 = false;
+  if (!cfg2) {
+    e = cudaFuncSetAttribute(k_sigma_sand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cfg2 = true;
+  }
+  k_sigma_sand<<<(unsigned)(nitems * a.NE * a.Nkz), 256, smem, st>>>(a);
   return cudaGetLastError();
 }
 

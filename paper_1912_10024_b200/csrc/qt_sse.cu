@@ -38,6 +38,7 @@ struct qt_sse_plan_s {
   double2* ws = nullptr;
   size_t ws_bytes = 0;
   double2* ws_g = nullptr;      // atom-major copies of G^<, G^> [2][Nwin][Nkz][NE][NN]
+  size_t gt_offset = 0;         // byte offset of the Σ Gt scratch inside ws
   size_t g_elems = 0;
   double flops[4] = {0, 0, 0, 0};
   // host-execute staging
@@ -413,9 +414,10 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
     budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
   }
-  const size_t need_min = std::max(coef_per_pair * kMaxPairs, w_per_item);
+  const size_t need_min = coef_per_pair * kMaxPairs + w_per_item + 256;
   if (budget < need_min) budget = need_min;
-  const size_t full = std::max(coef_per_pair * p->n_sig_pairs, w_per_item * p->pi_items.size());
+  const size_t full = std::max(coef_per_pair * p->n_sig_pairs + w_per_item * p->sig_items.size() + 256,
+                               w_per_item * p->pi_items.size());
   p->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
   // chunk item ranges so that each chunk's pairs fit the workspace
   // chunk item ranges so that each chunk's scratch fits the workspace (Σ: per pair; Π: per item)
@@ -434,8 +436,30 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
     bounds.push_back((int64_t)items.size());
   };
-  make_chunks(p->sig_items, coef_per_pair, true, p->sig_chunks);
   make_chunks(p->pi_items, w_per_item, false, p->pi_chunks);
+  // Σ chunks: coefficient tables of the chunk's pairs + (Norb <= 10) the Gt scratch of its items;
+  // the workspace is [coef region (max chunk pairs) | Gt region]
+  {
+    const bool gt = d.Norb <= 10;
+    const size_t gt_item = gt ? w_per_item : 0;
+    p->sig_chunks.clear();
+    p->sig_chunks.push_back(0);
+    int64_t np = 0, ni = 0, max_np = 0;
+    for (size_t i = 0; i < p->sig_items.size(); ++i) {
+      const int64_t u = p->sig_items[i].npair;
+      if (ni > 0 && (size_t)(np + u) * coef_per_pair + (size_t)(ni + 1) * gt_item > p->ws_bytes) {
+        p->sig_chunks.push_back((int64_t)i);
+        max_np = std::max(max_np, np);
+        np = 0;
+        ni = 0;
+      }
+      np += u;
+      ni += 1;
+    }
+    max_np = std::max(max_np, np);
+    p->sig_chunks.push_back((int64_t)p->sig_items.size());
+    p->gt_offset = ((size_t)max_np * coef_per_pair + 255) & ~size_t(255);
+  }
 
   qt_status s2;
   if ((s2 = upload(&p->d_nbr_win, p->nbr_win, cs)) != QT_OK || (s2 = upload(&p->d_sig_items, p->sig_items, cs)) != QT_OK ||
@@ -530,6 +554,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.G = (const double2*)(X == 0 ? GL : GG);
       sa.Gam = p->ws_g + (X == 0 ? 0 : p->g_elems);
       sa.coef = p->ws;
+      sa.Gt = reinterpret_cast<double2*>(reinterpret_cast<char*>(p->ws) + p->gt_offset);
       sa.cp0 = pp0;
       sa.npairs_chunk = pp1 - pp0;
       sa.dH = (const double2*)dH;
