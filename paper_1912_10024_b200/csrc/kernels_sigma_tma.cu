@@ -184,91 +184,89 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 
 // ---------------------------------------------------------------- Σ sandwich + neighbour sum
 // Σ_a(kz,E) += scale · Σ_i ∇_iH_{a s} (Σ_j Gt^{ij} ∇_jH_{b r}) for every pair of the chunk's items (R8).
-// One CTA per (item, kz, E); Gt block and ∇H blocks staged in shared memory; register-blocked DFMA.
+// One CTA per (item, kz, half of the item's pairs), looping over E: ∇H blocks stay in shared memory;
+// V-threads own (pair, E, i, x) and stream their Gt rows from the scratch straight into registers
+// (each value reused Norb times), S-threads own (pair, E, x); both keep Norb complex accumulators.
+constexpr int kSandPairs = 4;   // pairs per CTA
+constexpr int kSandE = 2;       // energies per iteration
+
 __global__ void __launch_bounds__(256) k_sigma_sand(SigmaArgs A) {
   extern __shared__ __align__(16) double2 sm[];
   const int NN = A.NN, No = A.Norb;
-  const int64_t blk = blockIdx.x;
-  const int E = (int)(blk % A.NE);
-  const int kz = (int)((blk / A.NE) % A.Nkz);
-  const int il = (int)(blk / ((int64_t)A.NE * A.Nkz));
+  const int half = blockIdx.x & 1;
+  const int64_t r = blockIdx.x >> 1;
+  const int kz = (int)(r % A.Nkz);
+  const int il = (int)(r / A.Nkz);
   const SigItem item = A.items[il];
-  const int P = item.npair;
-  double2* Gt = sm;                       // [9P][NN]
-  double2* Hr = Gt + kRows * NN;          // [P][3][NN]
-  double2* Hl = Hr + kMaxPairs * 3 * NN;  // [P][3][NN]
-  double2* Vs = Hl + kMaxPairs * 3 * NN;  // [P][3][NN]
-  const double2* src = A.Gt + (((int64_t)il * A.Nkz + kz) * A.NE + E) * kRows * NN;
-  for (int idx = threadIdx.x; idx < 9 * P * NN; idx += blockDim.x) Gt[idx] = src[idx];
+  const int t0 = half * kSandPairs;
+  const int P = min(kSandPairs, item.npair - t0);
+  if (P <= 0) return;
+  double2* Hr = sm;                          // [P][3][NN]
+  double2* Hl = Hr + kSandPairs * 3 * NN;    // [P][3][NN]
+  double2* Vs = Hl + kSandPairs * 3 * NN;    // [kSandE][P][3][NN]
   for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
     const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
-    const SigPair pr = A.pairs[item.pair0 + t];
+    const SigPair pr = A.pairs[item.pair0 + t0 + t];
     Hr[idx] = A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem];
     Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
   }
-  __syncthreads();
-  constexpr int YB = 5;
-  const int nxb = (No + 1) >> 1, nyb = (No + YB - 1) / YB;
-  for (int idx = threadIdx.x; idx < P * 3 * nxb * nyb; idx += blockDim.x) {   // V^i = Σ_j Gt^{ij} ∇_jH_{br}
-    const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, ti = r1 / nxb;
-    const int t = ti / 3, i = ti - 3 * t, x0 = 2 * xb, y0 = yb * YB;
-    double2 s[2][YB];
+  int a_out[kSandPairs];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+  for (int t = 0; t < kSandPairs; ++t) a_out[t] = t < P ? A.pairs[item.pair0 + t0 + t].a : 0;
+  const double2* gbase = A.Gt + ((int64_t)il * A.Nkz + kz) * A.NE * kRows * NN;
+  const int nv = kSandE * P * 3 * No;   // V units: (e, t, i, x)
+  const int ns = kSandE * P * No;       // S units: (e, t, x)
+  for (int e0 = 0; e0 < A.NE; e0 += kSandE) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < nv; u += blockDim.x) {
+      const int x = u % No, r1 = u / No, i = r1 % 3, r2 = r1 / 3, t = r2 % P, e = r2 / P;
+      if (e0 + e >= A.NE) continue;
+      double2 s[12];
 #pragma unroll
-      for (int w = 0; w < YB; ++w) s[u][w] = make_double2(0.0, 0.0);
-    for (int j = 0; j < 3; ++j) {
-      const double2* g0 = Gt + (t * 9 + i * 3 + j) * NN + x0 * No;
-      const double2* hr = Hr + (t * 3 + j) * NN + y0;
-      for (int v = 0; v < No; ++v) {
-        const double2 ga = g0[v], gb = (x0 + 1 < No) ? g0[No + v] : make_double2(0.0, 0.0);
+      for (int y = 0; y < 12; ++y) s[y] = make_double2(0.0, 0.0);
+      const double2* g = gbase + ((int64_t)(e0 + e) * kRows + (t0 + t) * 9 + i * 3) * NN + x * No;
 #pragma unroll
-        for (int w = 0; w < YB; ++w) {
-          const double2 h = (y0 + w < No) ? hr[v * No + w] : make_double2(0.0, 0.0);
-          cfma(s[0][w], ga, h);
-          cfma(s[1][w], gb, h);
+      for (int j = 0; j < 3; ++j) {
+        const double2* hr = Hr + (t * 3 + j) * NN;
+        for (int v = 0; v < No; ++v) {
+          const double2 gv = __ldg(g + j * NN + v);
+#pragma unroll
+          for (int y = 0; y < 12; ++y)
+            if (y < No) cfma(s[y], gv, hr[v * No + y]);
         }
       }
+      double2* vo = Vs + ((e * P + t) * 3 + i) * NN + x * No;
+#pragma unroll
+      for (int y = 0; y < 12; ++y)
+        if (y < No) vo[y] = s[y];
     }
+    __syncthreads();
+    for (int u = threadIdx.x; u < ns; u += blockDim.x) {
+      const int x = u % No, r1 = u / No, t = r1 % P, e = r1 / P;
+      if (e0 + e >= A.NE) continue;
+      double2 s[12];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+      for (int y = 0; y < 12; ++y) s[y] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int w = 0; w < YB; ++w)
-        if (x0 + u < No && y0 + w < No) Vs[ti * NN + (x0 + u) * No + y0 + w] = s[u][w];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < P * nxb * nyb; idx += blockDim.x) {       // S = Σ_i ∇_iH_{as} V^i
-    const int yb = idx % nyb, r1 = idx / nyb, xb = r1 % nxb, t = r1 / nxb;
-    const int x0 = 2 * xb, y0 = yb * YB;
-    double2 s[2][YB];
+      for (int i = 0; i < 3; ++i) {
+        const double2* hl = Hl + (t * 3 + i) * NN + x * No;
+        const double2* v = Vs + ((e * P + t) * 3 + i) * NN;
+        for (int k = 0; k < No; ++k) {
+          const double2 h = hl[k];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int w = 0; w < YB; ++w) s[u][w] = make_double2(0.0, 0.0);
-    for (int i = 0; i < 3; ++i) {
-      const double2* hl = Hl + (t * 3 + i) * NN + x0 * No;
-      const double2* v = Vs + (t * 3 + i) * NN + y0;
-      for (int u = 0; u < No; ++u) {
-        const double2 ha = hl[u], hb = (x0 + 1 < No) ? hl[No + u] : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int w = 0; w < YB; ++w) {
-          const double2 vv = (y0 + w < No) ? v[u * No + w] : make_double2(0.0, 0.0);
-          cfma(s[0][w], ha, vv);
-          cfma(s[1][w], hb, vv);
+          for (int y = 0; y < 12; ++y)
+            if (y < No) cfma(s[y], h, v[k * No + y]);
         }
       }
-    }
-    const SigPair pr = A.pairs[item.pair0 + t];
-    double2* out = A.Sig + (((int64_t)kz * A.NE + E) * A.Nout + pr.a) * NN;
+      double2* out = A.Sig + (((int64_t)kz * A.NE + e0 + e) * A.Nout + a_out[t]) * NN + x * No;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int w = 0; w < YB; ++w)
-        if (x0 + u < No && y0 + w < No) {
-          const double2 r = cmul(A.scale, s[u][w]);
-          atomicAdd(reinterpret_cast<double*>(out + (x0 + u) * No + y0 + w), r.x);
-          atomicAdd(reinterpret_cast<double*>(out + (x0 + u) * No + y0 + w) + 1, r.y);
+      for (int y = 0; y < 12; ++y)
+        if (y < No) {
+          const double2 rr = cmul(A.scale, s[y]);
+          atomicAdd(reinterpret_cast<double*>(out + y), rr.x);
+          atomicAdd(reinterpret_cast<double*>(out + y) + 1, rr.y);
         }
+    }
   }
 }
 
@@ -336,14 +334,14 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
   k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmC, b);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t)(kRows + 3 * 3 * kMaxPairs) * a.NN * 16;
+  const size_t smem = (size_t)(2 * kSandPairs * 3 + kSandE * kSandPairs * 3) * a.NN * 16;
   static bool cfg2 = false;
   if (!cfg2) {
     e = cudaFuncSetAttribute(k_sigma_sand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cfg2 = true;
   }
-  k_sigma_sand<<<(unsigned)(nitems * a.NE * a.Nkz), 256, smem, st>>>(a);
+  k_sigma_sand<<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);
   return cudaGetLastError();
 }
 
