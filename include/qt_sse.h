@@ -128,7 +128,7 @@ uint64_t qt_sse_launch_count(void);
  * returns, per kernel kind (QT_K_*), the summed milliseconds and launch counts since the
  * last reset, then clears them. */
 enum { QT_K_SIGMA_COEF = 0, QT_K_SIGMA = 1, QT_K_PI_W = 2, QT_K_PI_CONTRACT = 3, QT_K_PI_SELF = 4,
-       QT_K_RELAYOUT = 5, QT_K_HALO = 6, QT_K_NKINDS = 7 };
+       QT_K_RELAYOUT = 5, QT_K_HALO = 6, QT_K_SIGMA_SAND = 7, QT_K_NKINDS = 8 };
 qt_status qt_sse_timing_enable(qt_sse_plan_t plan, int enable);
 qt_status qt_sse_timing_read(qt_sse_plan_t plan, double ms[QT_K_NKINDS], int64_t launches[QT_K_NKINDS]);
 

@@ -21,7 +21,8 @@ EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
             "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read", "qt_sse_nccl_unique_id",
             "qt_sse_shard_info"]
-KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout", "k_halo_pack"]
+KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout", "k_halo_pack",
+                "k_sigma_sand"]
 
 
 class Desc(ctypes.Structure):

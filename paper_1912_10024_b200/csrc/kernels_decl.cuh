@@ -63,6 +63,7 @@ constexpr int kEB = 4;
 cudaError_t launch_sigma_coef(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
+cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st);
 cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st);

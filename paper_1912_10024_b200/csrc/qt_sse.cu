@@ -575,6 +575,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.Dmax = (int)p->Dmax;
       sa.Dwin = (int)p->Dwin;
       QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
+      QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
     }
   }
   return QT_OK;
