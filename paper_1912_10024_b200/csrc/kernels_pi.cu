@@ -14,93 +14,82 @@
 namespace qt {
 
 // W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] · T_i[q][x],  T_i = G^Y_b · ∇_iH_{br}   (the Π sandwich)
-// One CTA per (pair, kz); loops over energy chunks of kEB. ∇H blocks stay in shared memory; both
-// products are register-blocked 5x5 (2.5 complex MACs per shared-memory load); W is staged in shared
-// memory and written with contiguous 16-byte stores into the item's 72-row block.
-constexpr int kWB = 5;   // register block edge
+// One CTA per (work item, kz, half of the item's pairs), looping over energy pairs. Compile-time Norb;
+// T-threads own a row (t, e, i, q) of T_i = G^Y_b ∇_iH_{br}, W-threads own a column set (t, e, i, j, y):
+// W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x] for all x. The W block of (item, kz, E) is 72 contiguous
+// rows; each thread's stores fill part of it (L2 merges the partial lines).
+constexpr int kWPairs = 4;
+constexpr int kWE = 2;
 
-template <bool ROWS_X>
-__device__ __forceinline__ void block_mm(const double2* __restrict__ L, int ldl, const double2* __restrict__ R, int ldr,
-                                         int r0, int c0, int n, int No, double2 (&acc)[kWB][kWB]) {
-  // acc[u][w] += Σ_k L[(r0+u)*ldl + k] * R[k*ldr + c0 + w], rows/cols < No
-  for (int k = 0; k < n; ++k) {
-    double2 l[kWB], r[kWB];
-#pragma unroll
-    for (int u = 0; u < kWB; ++u) l[u] = (r0 + u < No) ? L[(r0 + u) * ldl + k] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int w = 0; w < kWB; ++w) r[w] = (c0 + w < No) ? R[k * ldr + c0 + w] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < kWB; ++u)
-#pragma unroll
-      for (int w = 0; w < kWB; ++w) cfma(acc[u][w], l[u], r[w]);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_pi_w(PiWArgs A) {
-  // One CTA per (work item = ≤8 pairs of one destination atom, kz); energy chunks of kWE (1 or 2).
-  const int kWE = A.nEB;
-  extern __shared__ __align__(16) double2 sm[];
-  const int NN = A.NN, No = A.Norb;
-  const int kz = (int)(blockIdx.x % A.Nkz);
-  const int64_t item = A.i0 + blockIdx.x / A.Nkz;
+template <int NO>
+__global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
+  constexpr int NN = NO * NO;
+  extern __shared__ __align__(16) double2 w_sm[];
+  double2* Hl = w_sm;                          // [kWPairs][3][NN]  ∇_jH_{as}
+  double2* Hr = Hl + kWPairs * 3 * NN;         // [kWPairs][3][NN]  ∇_iH_{br}
+  double2* Gb = Hr + kWPairs * 3 * NN;         // [kWPairs][kWE][NN]
+  double2* T = Gb + kWPairs * kWE * NN;        // [kWPairs][kWE][3][NN]
+  const int half = blockIdx.x & 1;
+  const int64_t r = blockIdx.x >> 1;
+  const int kz = (int)(r % A.Nkz);
+  const int64_t item = A.i0 + r / A.Nkz;
   const PiItem it = A.items[item];
-  const int P = it.npair;
-  double2* Hl = sm;                          // [P][3][NN]  ∇_jH_{as}
-  double2* Hr = Hl + kMaxPairs * 3 * NN;     // [P][3][NN]  ∇_iH_{br}
-  double2* Gb = Hr + kMaxPairs * 3 * NN;     // [P][kWE][NN]
-  double2* T = Gb + kMaxPairs * kWE * NN;    // [P][kWE][3][NN]
+  const int t0 = half * kWPairs;
+  const int P = min(kWPairs, it.npair - t0);
+  if (P <= 0) return;
   for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
     const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
-    const PiPair pr = A.pairs[it.pair0 + t];
+    const PiPair pr = A.pairs[it.pair0 + t0 + t];
     Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
     Hr[idx] = A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + rem];
   }
-  const int nb1 = (No + kWB - 1) / kWB, nb = nb1 * nb1;
   double2* Wdst = A.W + ((item - A.i0) * A.Nkz + kz) * (int64_t)A.NE * kRows * NN;
   for (int e0 = 0; e0 < A.NE; e0 += kWE) {
     const int ne = min(kWE, A.NE - e0);
     __syncthreads();
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
-      const int b_in = A.pairs[it.pair0 + t].b_in;
+      const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
       Gb[t * kWE * NN + rem] = A.GYam[(((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem];
     }
     __syncthreads();
-    // T_i(t, e) = G_b(e) · ∇_iH_{br}
-    for (int u = threadIdx.x; u < P * ne * 3 * nb; u += blockDim.x) {
-      const int bl = u % nb, r = u / nb, i = r % 3, te = r / 3, e = te % ne, t = te / ne;
-      const int r0 = (bl / nb1) * kWB, c0 = (bl % nb1) * kWB;
-      double2 acc[kWB][kWB];
+    // T_i(t, e)[q][x] = Σ_p G_b[q][p] ∇_iH_{br}[p][x]
+    for (int u = threadIdx.x; u < P * ne * 3 * NO; u += blockDim.x) {
+      const int q = u % NO, r1 = u / NO, i = r1 % 3, r2 = r1 / 3, e = r2 % ne, t = r2 / ne;
+      double2 g[NO], s[NO];
 #pragma unroll
-      for (int x = 0; x < kWB; ++x)
+      for (int k = 0; k < NO; ++k) {
+        g[k] = Gb[(t * kWE + e) * NN + q * NO + k];
+        s[k] = make_double2(0.0, 0.0);
+      }
+      const double2* h = Hr + (t * 3 + i) * NN;
 #pragma unroll
-        for (int y = 0; y < kWB; ++y) acc[x][y] = make_double2(0.0, 0.0);
-      block_mm<true>(Gb + (t * kWE + e) * NN, No, Hr + (t * 3 + i) * NN, No, r0, c0, No, No, acc);
-      double2* o = T + ((t * kWE + e) * 3 + i) * NN;
+      for (int k = 0; k < NO; ++k)
 #pragma unroll
-      for (int x = 0; x < kWB; ++x)
+        for (int x = 0; x < NO; ++x) cfma(s[x], g[k], h[k * NO + x]);
+      double2* o = T + ((t * kWE + e) * 3 + i) * NN + q * NO;
 #pragma unroll
-        for (int y = 0; y < kWB; ++y)
-          if (r0 + x < No && c0 + y < No) o[(r0 + x) * No + c0 + y] = acc[x][y];
+      for (int x = 0; x < NO; ++x) o[x] = s[x];
     }
     __syncthreads();
-    // W^{ij}(t, e)[x][y] = (∇_jH_{as} · T_i)[y][x] -> rows t*9 + ij of the item's block (L2 merges lines)
-    for (int u = threadIdx.x; u < P * ne * 9 * nb; u += blockDim.x) {
-      const int bl = u % nb, r = u / nb, ij = r % 9, te = r / 9, e = te % ne, t = te / ne;
+    // W^{ij}(t, e)[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x]
+    for (int u = threadIdx.x; u < P * ne * 9 * NO; u += blockDim.x) {
+      const int y = u % NO, r1 = u / NO, ij = r1 % 9, r2 = r1 / 9, e = r2 % ne, t = r2 / ne;
       const int i = ij / 3, j = ij - 3 * i;
-      const int y0 = (bl / nb1) * kWB, x0 = (bl % nb1) * kWB;
-      double2 acc[kWB][kWB];
+      double2 hrow[NO], s[NO];
 #pragma unroll
-      for (int x = 0; x < kWB; ++x)
+      for (int k = 0; k < NO; ++k) {
+        hrow[k] = Hl[(t * 3 + j) * NN + y * NO + k];
+        s[k] = make_double2(0.0, 0.0);
+      }
+      const double2* tt = T + ((t * kWE + e) * 3 + i) * NN;
 #pragma unroll
-        for (int y = 0; y < kWB; ++y) acc[x][y] = make_double2(0.0, 0.0);
-      block_mm<true>(Hl + (t * 3 + j) * NN, No, T + ((t * kWE + e) * 3 + i) * NN, No, y0, x0, No, No, acc);
-      double2* o = Wdst + ((int64_t)(e0 + e) * kRows + t * 9 + ij) * NN;
+      for (int q = 0; q < NO; ++q)
 #pragma unroll
-      for (int xx = 0; xx < kWB; ++xx)
+        for (int x = 0; x < NO; ++x) cfma(s[x], hrow[q], tt[q * NO + x]);
+      double2* o = Wdst + ((int64_t)(e0 + e) * kRows + (t0 + t) * 9 + ij) * NN + y;
 #pragma unroll
-        for (int yy = 0; yy < kWB; ++yy)
-          if (y0 + yy < No && x0 + xx < No) o[(x0 + xx) * No + y0 + yy] = acc[yy][xx];
+      for (int x = 0; x < NO; ++x) o[x * NO] = s[x];
     }
   }
 }
@@ -362,18 +351,32 @@ __global__ void k_pi_self(PiSelfArgs A) {
 }
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_pi_w(const PiWArgs& a, int64_t nitems_chunk, cudaStream_t st) {
-  int64_t nblk = nitems_chunk * a.Nkz;
-  if (nblk == 0) return cudaSuccess;
-  PiWArgs b = a;
-  b.nEB = (size_t)kMaxPairs * (6 + 2 + 6) * a.NN * sizeof(double2) <= 220 * 1024 ? 2 : 1;
-  size_t smem = (size_t)kMaxPairs * (6 + 4 * b.nEB) * a.NN * sizeof(double2);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_pi_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_pi_w<<<(unsigned)nblk, 256, smem, st>>>(b);
+template <int NO>
+static cudaError_t launch_pi_w_no(const PiWArgs& a, int64_t nitems, cudaStream_t st) {
+  const int smem = (6 + kWE + 3 * kWE) * kWPairs * NO * NO * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_pi_w<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_pi_w<NO><<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_pi_w(const PiWArgs& a, int64_t nitems_chunk, cudaStream_t st) {
+  if (nitems_chunk * a.Nkz == 0) return cudaSuccess;
+  switch (a.Norb) {
+    case 1: return launch_pi_w_no<1>(a, nitems_chunk, st);
+    case 2: return launch_pi_w_no<2>(a, nitems_chunk, st);
+    case 3: return launch_pi_w_no<3>(a, nitems_chunk, st);
+    case 4: return launch_pi_w_no<4>(a, nitems_chunk, st);
+    case 5: return launch_pi_w_no<5>(a, nitems_chunk, st);
+    case 6: return launch_pi_w_no<6>(a, nitems_chunk, st);
+    case 7: return launch_pi_w_no<7>(a, nitems_chunk, st);
+    case 8: return launch_pi_w_no<8>(a, nitems_chunk, st);
+    case 9: return launch_pi_w_no<9>(a, nitems_chunk, st);
+    case 10: return launch_pi_w_no<10>(a, nitems_chunk, st);
+    case 11: return launch_pi_w_no<11>(a, nitems_chunk, st);
+    case 12: return launch_pi_w_no<12>(a, nitems_chunk, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // one CTA per (atom, kz): copies the NE x NN block of that atom into its contiguous atom-major slot

@@ -184,15 +184,20 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 
 // ---------------------------------------------------------------- Σ sandwich + neighbour sum
 // Σ_a(kz,E) += scale · Σ_i ∇_iH_{a s} (Σ_j Gt^{ij} ∇_jH_{b r}) for every pair of the chunk's items (R8).
-// One CTA per (item, kz, half of the item's pairs), looping over E: ∇H blocks stay in shared memory;
-// V-threads own (pair, E, i, x) and stream their Gt rows from the scratch straight into registers
-// (each value reused Norb times), S-threads own (pair, E, x); both keep Norb complex accumulators.
+// One CTA per (item, kz, half of the item's pairs), looping over energy pairs. ∇H blocks stay in
+// shared memory. Compile-time Norb: a V-thread owns a row (e, t, i, x) of V^i = Σ_j Gt^{ij}∇_jH_{br}
+// (Gt row loaded into registers, ∇H broadcast from shared memory, Norb accumulators); an S-thread owns
+// a row (e, t, x) of S = Σ_i ∇_iH_{as} V^i and adds scale·S into Σ_a with RED.F64.
 constexpr int kSandPairs = 4;   // pairs per CTA
 constexpr int kSandE = 2;       // energies per iteration
 
-__global__ void __launch_bounds__(256) k_sigma_sand(SigmaArgs A) {
-  extern __shared__ __align__(16) double2 sm[];
-  const int NN = A.NN, No = A.Norb;
+template <int NO>
+__global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
+  constexpr int NN = NO * NO;
+  extern __shared__ __align__(16) double2 sand_sm[];
+  double2* Hr = sand_sm;                         // [kSandPairs][3][NN]
+  double2* Hl = Hr + kSandPairs * 3 * NN;        // [kSandPairs][3][NN]
+  double2* Vs = Hl + kSandPairs * 3 * NN;        // [kSandE][kSandPairs][3][NN]
   const int half = blockIdx.x & 1;
   const int64_t r = blockIdx.x >> 1;
   const int kz = (int)(r % A.Nkz);
@@ -201,71 +206,65 @@ __global__ void __launch_bounds__(256) k_sigma_sand(SigmaArgs A) {
   const int t0 = half * kSandPairs;
   const int P = min(kSandPairs, item.npair - t0);
   if (P <= 0) return;
-  double2* Hr = sm;                          // [P][3][NN]
-  double2* Hl = Hr + kSandPairs * 3 * NN;    // [P][3][NN]
-  double2* Vs = Hl + kSandPairs * 3 * NN;    // [kSandE][P][3][NN]
   for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
     const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
     const SigPair pr = A.pairs[item.pair0 + t0 + t];
     Hr[idx] = A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem];
     Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
   }
-  int a_out[kSandPairs];
-#pragma unroll
-  for (int t = 0; t < kSandPairs; ++t) a_out[t] = t < P ? A.pairs[item.pair0 + t0 + t].a : 0;
   const double2* gbase = A.Gt + ((int64_t)il * A.Nkz + kz) * A.NE * kRows * NN;
-  const int nv = kSandE * P * 3 * No;   // V units: (e, t, i, x)
-  const int ns = kSandE * P * No;       // S units: (e, t, x)
+  const int nv = kSandE * P * 3 * NO;   // V rows (e, t, i, x)
+  const int ns = kSandE * P * NO;       // S rows (e, t, x)
   for (int e0 = 0; e0 < A.NE; e0 += kSandE) {
     __syncthreads();
     for (int u = threadIdx.x; u < nv; u += blockDim.x) {
-      const int x = u % No, r1 = u / No, i = r1 % 3, r2 = r1 / 3, t = r2 % P, e = r2 / P;
+      const int x = u % NO, r1 = u / NO, i = r1 % 3, r2 = r1 / 3, t = r2 % P, e = r2 / P;
       if (e0 + e >= A.NE) continue;
-      double2 s[12];
+      double2 s[NO];
 #pragma unroll
-      for (int y = 0; y < 12; ++y) s[y] = make_double2(0.0, 0.0);
-      const double2* g = gbase + ((int64_t)(e0 + e) * kRows + (t0 + t) * 9 + i * 3) * NN + x * No;
+      for (int y = 0; y < NO; ++y) s[y] = make_double2(0.0, 0.0);
+      const double2* g = gbase + ((int64_t)(e0 + e) * kRows + (t0 + t) * 9 + i * 3) * NN + x * NO;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
+        double2 gv[NO];
+#pragma unroll
+        for (int v = 0; v < NO; ++v) gv[v] = __ldg(g + j * NN + v);
         const double2* hr = Hr + (t * 3 + j) * NN;
-        for (int v = 0; v < No; ++v) {
-          const double2 gv = __ldg(g + j * NN + v);
 #pragma unroll
-          for (int y = 0; y < 12; ++y)
-            if (y < No) cfma(s[y], gv, hr[v * No + y]);
-        }
+        for (int v = 0; v < NO; ++v)
+#pragma unroll
+          for (int y = 0; y < NO; ++y) cfma(s[y], gv[v], hr[v * NO + y]);
       }
-      double2* vo = Vs + ((e * P + t) * 3 + i) * NN + x * No;
+      double2* vo = Vs + ((e * kSandPairs + t) * 3 + i) * NN + x * NO;
 #pragma unroll
-      for (int y = 0; y < 12; ++y)
-        if (y < No) vo[y] = s[y];
+      for (int y = 0; y < NO; ++y) vo[y] = s[y];
     }
     __syncthreads();
     for (int u = threadIdx.x; u < ns; u += blockDim.x) {
-      const int x = u % No, r1 = u / No, t = r1 % P, e = r1 / P;
+      const int x = u % NO, r1 = u / NO, t = r1 % P, e = r1 / P;
       if (e0 + e >= A.NE) continue;
-      double2 s[12];
+      double2 s[NO];
 #pragma unroll
-      for (int y = 0; y < 12; ++y) s[y] = make_double2(0.0, 0.0);
+      for (int y = 0; y < NO; ++y) s[y] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const double2* hl = Hl + (t * 3 + i) * NN + x * No;
-        const double2* v = Vs + ((e * P + t) * 3 + i) * NN;
-        for (int k = 0; k < No; ++k) {
-          const double2 h = hl[k];
+        double2 h[NO];
 #pragma unroll
-          for (int y = 0; y < 12; ++y)
-            if (y < No) cfma(s[y], h, v[k * No + y]);
-        }
+        for (int k = 0; k < NO; ++k) h[k] = Hl[(t * 3 + i) * NN + x * NO + k];
+        const double2* v = Vs + ((e * kSandPairs + t) * 3 + i) * NN;
+#pragma unroll
+        for (int k = 0; k < NO; ++k)
+#pragma unroll
+          for (int y = 0; y < NO; ++y) cfma(s[y], h[k], v[k * NO + y]);
       }
-      double2* out = A.Sig + (((int64_t)kz * A.NE + e0 + e) * A.Nout + a_out[t]) * NN + x * No;
+      const int a_out = A.pairs[item.pair0 + t0 + t].a;
+      double* out = reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NE + e0 + e) * A.Nout + a_out) * NN + x * NO);
 #pragma unroll
-      for (int y = 0; y < 12; ++y)
-        if (y < No) {
-          const double2 rr = cmul(A.scale, s[y]);
-          atomicAdd(reinterpret_cast<double*>(out + y), rr.x);
-          atomicAdd(reinterpret_cast<double*>(out + y) + 1, rr.y);
-        }
+      for (int y = 0; y < NO; ++y) {
+        const double2 rr = cmul(A.scale, s[y]);
+        atomicAdd(out + 2 * y, rr.x);
+        atomicAdd(out + 2 * y + 1, rr.y);
+      }
     }
   }
 }
@@ -335,14 +334,30 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
-  if (a.NN > 100) return cudaSuccess;   // Norb 11, 12: the cp.async kernel applies the sandwich itself
-  const size_t smem = (size_t)(2 * kSandPairs * 3 + kSandE * kSandPairs * 3) * a.NN * 16;
-  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int NO>
+static cudaError_t launch_sand_no(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
+  const int smem = (2 + kSandE) * kSandPairs * 3 * NO * NO * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  if (nitems * a.Nkz == 0) return cudaSuccess;
-  k_sigma_sand<<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);
+  k_sigma_sand<NO><<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
+  if (nitems * a.Nkz == 0) return cudaSuccess;
+  switch (a.Norb) {
+    case 1: return launch_sand_no<1>(a, nitems, st);
+    case 2: return launch_sand_no<2>(a, nitems, st);
+    case 3: return launch_sand_no<3>(a, nitems, st);
+    case 4: return launch_sand_no<4>(a, nitems, st);
+    case 5: return launch_sand_no<5>(a, nitems, st);
+    case 6: return launch_sand_no<6>(a, nitems, st);
+    case 7: return launch_sand_no<7>(a, nitems, st);
+    case 8: return launch_sand_no<8>(a, nitems, st);
+    case 9: return launch_sand_no<9>(a, nitems, st);
+    case 10: return launch_sand_no<10>(a, nitems, st);
+    default: return cudaSuccess;   // Norb 11, 12: the cp.async kernel applies the sandwich itself
+  }
 }
 
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
