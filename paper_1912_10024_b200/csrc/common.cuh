@@ -40,6 +40,13 @@ __device__ __forceinline__ void cmma3(C3Acc& c, double ar, double ai, double as,
   dmma(c.t3[0], c.t3[1], as, br + bi);
 }
 
+// same with the B-side sum bs = br + bi precomputed
+__device__ __forceinline__ void cmma3s(C3Acc& c, double ar, double ai, double as, double br, double bi, double bs) {
+  dmma(c.t1[0], c.t1[1], ar, br);
+  dmma(c.t2[0], c.t2[1], ai, bi);
+  dmma(c.t3[0], c.t3[1], as, bs);
+}
+
 // 16-byte async global->shared copy; src_valid == false zero-fills the destination.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool src_valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);

@@ -13,11 +13,15 @@ struct CoefArgs {
   double2* coef;
   int64_t npairs, Nw, Nwin, Nb, Nqz, DWp;
   int Dmax, shift0;
+  // tiled layout (TMA path): [item - item0][q][dc][72 rows (t,ij)][20], d = 16*dc + k - Dmax
+  bool tiled;
+  int64_t item0, nitems, ndc, Dwin;
 };
 
 struct SigmaArgs {
   const double2* G;      // G^X, paper layout [Nkz][NE][Nwin][NN]
   const double2* Gam;    // G^X, atom-major copy [Nwin][Nkz][NE][NN] (TMA path)
+  const double* Gsum;    // Re + Im of Gam (same layout, doubles)
   const double2* coef;   // coefficient table of the current chunk: pair index p - cp0
   const double2* dH;
   const SigItem* items;
@@ -26,7 +30,7 @@ struct SigmaArgs {
   double2* Gt;           // Gt scratch of the chunk [item][kz][E][72][NN] (TMA path)
   double2 scale;
   int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk, ntiles;
-  int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin;
+  int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin, ndc;
 };
 
 struct PiWArgs {
@@ -61,6 +65,7 @@ struct PiSelfArgs {
 constexpr int kEB = 4;
 
 cudaError_t launch_sigma_coef(const CoefArgs& a, cudaStream_t st);
+cudaError_t launch_sigma_coef_tiled(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
@@ -68,7 +73,7 @@ cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st)
 cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st);
 // G [Nkz][NE][Nwin][NN] (paper layout) -> [Nwin][Nkz][NE][NN] (atom-major: every TMA box contiguous)
-cudaError_t launch_relayout(const double2* in, double2* out, int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN,
-                            cudaStream_t st);
+cudaError_t launch_relayout(const double2* in, double2* out, double* osum, int64_t Nkz, int64_t NE, int64_t Nwin,
+                            int64_t NN, cudaStream_t st);
 
 }  // namespace qt

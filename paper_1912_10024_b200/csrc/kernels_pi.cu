@@ -17,7 +17,7 @@ namespace qt {
 // One CTA per (work item, kz, half of the item's pairs), looping over energy pairs. Compile-time Norb;
 // T-threads own a row (t, e, i, q) of T_i = G^Y_b ∇_iH_{br}, W-threads own a column set (t, e, i, j, y):
 // W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x] for all x. The W block of (item, kz, E) is 72 contiguous
-// rows; each thread's stores fill part of it (L2 merges the partial lines).
+// rows per 20-wide xy chunk; each thread's stores fill part of it (L2 merges the partial lines).
 constexpr int kWPairs = 4;
 constexpr int kWE = 2;
 
@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
     Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
     Hr[idx] = A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + rem];
   }
-  double2* Wdst = A.W + ((item - A.i0) * A.Nkz + kz) * (int64_t)A.NE * kRows * NN;
+  constexpr int XC = 20;                       // = PiCfg::XC
+  constexpr int NXC = (NN + XC - 1) / XC;
+  double2* Wdst = A.W + ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NE * kRows * XC;
   for (int e0 = 0; e0 < A.NE; e0 += kWE) {
     const int ne = min(kWE, A.NE - e0);
     __syncthreads();
@@ -87,15 +89,18 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
       for (int q = 0; q < NO; ++q)
 #pragma unroll
         for (int x = 0; x < NO; ++x) cfma(s[x], hrow[q], tt[q * NO + x]);
-      double2* o = Wdst + ((int64_t)(e0 + e) * kRows + (t0 + t) * 9 + ij) * NN + y;
+      // W layout [xy chunk][E][72 rows][XC]: each Π stage reads one contiguous block
 #pragma unroll
-      for (int x = 0; x < NO; ++x) o[x * NO] = s[x];
+      for (int x = 0; x < NO; ++x) {
+        const int xy = x * NO + y, xc = xy / XC, c = xy - xc * XC;
+        Wdst[(((int64_t)xc * A.NE + e0 + e) * kRows + (t0 + t) * 9 + ij) * XC + c] = s[x];
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- Π correlation: TMA / mbarrier pipeline
-// Stage = (kz, E0..E0+EC-1, xy0..xy0+XC-1): the W tile [EC][72][XC] (5-D TMA box) and the G_a window
+// Stage = (kz, E0..E0+EC-1, xy0..xy0+XC-1): the W tile [EC][72][XC] (one contiguous 1-D bulk copy) and the G_a window
 // rows E0+s_0 .. E0+EC-1+s_{NWP-1} (4-D TMA box; rows >= NE zero-filled: reading R7). Warp 18 produces;
 // warps 0..17 consume (warp w: m-fragment w%9 of the rows (t,ij), half of the m-column fragments).
 struct PiCfg {
@@ -169,7 +174,7 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
 
 template <int NFM>
 __global__ void __launch_bounds__(PiCfg::THREADS, 1)
-    k_pi_contract(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmG, PiCArgs A) {
+    k_pi_contract(const __grid_constant__ CUtensorMap tmG, PiCArgs A) {
   using C = PiCfg;
   using T = PiTma<NFM>;
   extern __shared__ uint8_t smem_raw[];
@@ -207,7 +212,6 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
 
   if (warp == C::NCONS) {
     if (lane == 0) {
-      prefetch_tmap(&tmW);
       prefetch_tmap(&tmG);
       int kz = 0, xc = 0, ec = 0;
       for (int st = 0; st < nst; ++st) {
@@ -216,7 +220,8 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         mbar_arrive_expect_tx(&full[slot], T::STAGE_BYTES);
         double2* ws = smem + slot * T::STAGE;
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
-        tma_load_5d(ws, &tmW, 2 * xc * C::XC, 0, ec * C::EC, kz, il, &full[slot]);
+        bulk_load(ws, A.W + ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NE + ec * C::EC) * kRows * C::XC,
+                  C::W_STAGE * 16, &full[slot]);
         tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
         if (++ec == nec) {
           ec = 0;
@@ -282,15 +287,7 @@ static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
     configured = true;
   }
   const uint64_t NN = (uint64_t)a.NN;
-  CUtensorMap tmW, tmG;
-  {
-    const uint64_t dims[5] = {2 * NN, (uint64_t)kRows, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.nitems};
-    const uint64_t s1 = NN * 16, s2 = s1 * kRows, s3 = s2 * a.NE, s4 = s3 * a.Nkz;
-    const uint64_t strides[4] = {s1, s2, s3, s4};
-    const uint32_t box[5] = {2 * PiCfg::XC, (uint32_t)kRows, PiCfg::EC, 1, 1};
-    cudaError_t e = make_tmap_f64(&tmW, a.W, 5, dims, strides, box);
-    if (e != cudaSuccess) return e;
-  }
+  CUtensorMap tmG;
   {
     const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
     const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
@@ -300,7 +297,7 @@ static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
   }
   const int64_t nblk = a.nitems * a.Nqz;
   if (nblk == 0) return cudaSuccess;
-  k_pi_contract<NFM><<<(unsigned)nblk, PiCfg::THREADS, T::SMEM, st>>>(tmW, tmG, a);
+  k_pi_contract<NFM><<<(unsigned)nblk, PiCfg::THREADS, T::SMEM, st>>>(tmG, a);
   return cudaGetLastError();
 }
 
@@ -380,22 +377,28 @@ cudaError_t launch_pi_w(const PiWArgs& a, int64_t nitems_chunk, cudaStream_t st)
 }
 
 // one CTA per (atom, kz): copies the NE x NN block of that atom into its contiguous atom-major slot
+// also writes osum = Re + Im (the B-side sum of the Gauss 3M product, so consumers need no DADD)
 __global__ void __launch_bounds__(256) k_relayout(const double2* __restrict__ in, double2* __restrict__ out,
-                                                  int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN) {
+                                                  double* __restrict__ osum, int64_t Nkz, int64_t NE, int64_t Nwin,
+                                                  int64_t NN) {
   const int64_t a = blockIdx.x / Nkz, kz = blockIdx.x % Nkz;
   double2* o = out + (a * Nkz + kz) * NE * NN;
+  const int64_t NS = (NN + 1) & ~int64_t(1);   // sum-plane row stride: even, so TMA strides are 16-byte multiples
+  double* os = osum + (a * Nkz + kz) * NE * NS;
   const double2* src = in + (kz * NE * Nwin + a) * NN;
   const int64_t n = NE * NN;
   for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
     const int64_t e = idx / NN, uv = idx - e * NN;
-    o[idx] = __ldg(src + e * Nwin * NN + uv);
+    const double2 v = __ldg(src + e * Nwin * NN + uv);
+    o[idx] = v;
+    os[e * NS + uv] = v.x + v.y;
   }
 }
 
-cudaError_t launch_relayout(const double2* in, double2* out, int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN,
-                            cudaStream_t st) {
+cudaError_t launch_relayout(const double2* in, double2* out, double* osum, int64_t Nkz, int64_t NE, int64_t Nwin,
+                            int64_t NN, cudaStream_t st) {
   if (Nkz * Nwin == 0) return cudaSuccess;
-  k_relayout<<<(unsigned)(Nkz * Nwin), 256, 0, st>>>(in, out, Nkz, NE, Nwin, NN);
+  k_relayout<<<(unsigned)(Nkz * Nwin), 256, 0, st>>>(in, out, osum, Nkz, NE, Nwin, NN);
   return cudaGetLastError();
 }
 

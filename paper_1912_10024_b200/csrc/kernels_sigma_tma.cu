@@ -20,18 +20,70 @@
 
 namespace qt {
 
+// Coefficient tiles for the TMA path: coef[il][q][dc][row = t*9+ij][k], d = 16*dc + k - Dmax (k < 16;
+// k = 16..19 and rows t >= P are zero padding). Same values as k_sigma_coef (Eq. 3 four-term
+// combination; absorption Dc^X_{ij}, emission Dc^Y_{ji}: readings R2, R3).
+__global__ void k_sigma_coef_tiled(CoefArgs A) {
+  constexpr int KCP = 20;
+  const int64_t per_item = A.Nqz * A.ndc * kRows * KCP;
+  const int64_t total = A.nitems * per_item;
+  const int64_t pp0 = A.items[A.item0].pair0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx % KCP);
+    int64_t r = idx / KCP;
+    const int row = (int)(r % kRows);
+    r /= kRows;
+    const int64_t dc = r % A.ndc;
+    r /= A.ndc;
+    const int64_t q = r % A.Nqz;
+    const int64_t il = r / A.Nqz;
+    const SigItem item = A.items[A.item0 + il];
+    const int t = row / 9, ij = row - 9 * t;
+    const int64_t dd = 16 * dc + k;
+    double2 v = make_double2(0.0, 0.0);
+    if (k < 16 && t < item.npair && dd < A.Dwin) {
+      const int64_t d = dd - A.Dmax, ad = d < 0 ? -d : d;
+      if (ad >= A.shift0 && ad <= A.Dmax) {
+        const SigPair pr = A.pairs[item.pair0 - pp0 + t];
+        const int64_t b = item.b_in, m = ad - A.shift0, ns = A.Nb + 1;
+        const double2* D = d < 0 ? A.DX : A.DY;
+        const int e = d < 0 ? ij : (ij % 3) * 3 + ij / 3;
+        const int64_t base = (q * A.Nw + m) * A.Nwin;
+        const double2 dba = D[((base + b) * ns + pr.r + 1) * 9 + e];
+        const double2 dbb = D[((base + b) * ns + 0) * 9 + e];
+        const double2 daa = D[((base + pr.a_in) * ns + 0) * 9 + e];
+        const double2 dab = D[((base + pr.a_in) * ns + pr.s + 1) * 9 + e];
+        v.x = ((dba.x - dbb.x) - daa.x) + dab.x;
+        v.y = ((dba.y - dbb.y) - daa.y) + dab.y;
+      }
+    }
+    A.coef[idx] = v;
+  }
+}
+
+cudaError_t launch_sigma_coef_tiled(const CoefArgs& a, cudaStream_t st) {
+  const int64_t total = a.nitems * a.Nqz * a.ndc * kRows * 20;
+  if (total == 0) return cudaSuccess;
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_sigma_coef_tiled<<<(int)g, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int NF>
 struct SigTmaCfg {
   static constexpr int NFH0 = (NF + 1) / 2;  // n-fragments of column half 0
   static constexpr int NFH1 = NF / 2;        // n-fragments of column half 1
   static constexpr int NPS = NFH0 * 8 + 2;   // ≡ 2 (mod 8): conflict-free B-fragment LDS.128
   static constexpr int KC = 16;              // d values per stage (4 DMMA k-steps)
-  static constexpr int KCP = 20;             // ≡ 4 (mod 8): conflict-free A-fragment LDS.128
+  static constexpr int KCP = 20;             // ≡ 4 (mod 8): conflict-free A-fragment LDS.128 (tiled coef row)
   static constexpr int STAGES = 5;
   static constexpr int G_STAGE = KC * NPS;   // complex elements
+  static constexpr int S_STAGE = (KC * NPS / 2 + 7) & ~7;   // Re+Im plane of the G rows (doubles), complex units
   static constexpr int C_STAGE = kRows * KCP;
-  static constexpr int STAGE = G_STAGE + C_STAGE;
-  static constexpr uint32_t STAGE_BYTES = STAGE * 16;
+  static constexpr int STAGE = G_STAGE + S_STAGE + C_STAGE;
+  static constexpr uint32_t STAGE_BYTES = (G_STAGE + C_STAGE) * 16 + KC * NPS * 8;
   static constexpr int PIPE = STAGES * STAGE;
   static constexpr int NCONS = 18;           // consumer warps: (m-fragment, half of the half-tile's n-frags)
   static constexpr int THREADS = (NCONS + 1) * 32;
@@ -45,7 +97,7 @@ struct SigTmaCfg {
 // One stage of DMMA work for a consumer warp with NFW n-fragments (Gauss 3M complex product: three
 // real DMMAs per complex 8x8x4 step, see C3Acc).
 template <int NFW, int NPS, int KC>
-__device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const double2* cs, int kc) {
+__device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const double* ss, const double2* cs, int kc) {
   static_assert(NFW > 0, "empty fragment range");
 #pragma unroll
   for (int k4 = 0; k4 < KC; k4 += 4) {
@@ -53,18 +105,16 @@ __device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const
       const double2 a = cs[k4];
       const double as = a.x + a.y;
       const double2* gb = gs + k4 * NPS;
+      const double* sb = ss + k4 * NPS;
 #pragma unroll
-      for (int f = 0; f < NFW; ++f) {
-        const double2 b = gb[f * 8];
-        cmma3(acc[f], a.x, a.y, as, b.x, b.y);
-      }
+      for (int f = 0; f < NFW; ++f) cmma3s(acc[f], a.x, a.y, as, gb[f * 8].x, gb[f * 8].y, sb[f * 8]);
     }
   }
 }
 
 struct SigTile {
   SigItem item;
-  int E, kz, ch, il, dd_lo, dd_hi, nchunk, nst;
+  int E, kz, ch, il, dc_lo, nchunk, nst;
 };
 
 template <int KC>
@@ -76,10 +126,11 @@ __device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
   T.kz = (int)((t / A.NE) % A.Nkz);
   T.il = (int)(t / ((int64_t)A.NE * A.Nkz));
   T.item = A.items[T.il];
-  // K range: d with E+d in [0,NE) (R7), rounded to the k=4 step; chunks of KC per q.
-  T.dd_lo = max(0, A.Dmax - T.E) & ~3;
-  T.dd_hi = (min(A.Dwin, A.Dmax - T.E + A.NE) + 3) & ~3;
-  T.nchunk = (T.dd_hi - T.dd_lo + KC - 1) / KC;
+  // K range: shifts d = 16*dc + k - Dmax with E+d in [0,NE) (R7), in whole 16-shift chunks (rows outside
+  // the window are zero-filled by TMA; shifts beyond the table are zero coefficients).
+  T.dc_lo = max(0, A.Dmax - T.E) / KC;
+  const int dc_hi = (min(A.Dwin, A.Dmax - T.E + A.NE) + KC - 1) / KC;
+  T.nchunk = dc_hi - T.dc_lo;
   T.nst = A.Nqz * T.nchunk;
   return T;
 }
@@ -89,7 +140,7 @@ __device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
 // (complex, from the 3M accumulators) to the chunk's scratch [item][kz][E][72][Norb²].
 template <int NF>
 __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
-    k_sigma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmC, SigmaArgs A) {
+    k_sigma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmS, SigmaArgs A) {
   using C = SigTmaCfg<NF>;
   extern __shared__ uint8_t smem_raw[];
   double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -110,7 +161,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     // ---------------- producer
     if (lane == 0) {
       prefetch_tmap(&tmG);
-      prefetch_tmap(&tmC);
+      prefetch_tmap(&tmS);
       uint32_t g = 0;
       for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
         const SigTile T = sig_tile<C::KC>(A, t);
@@ -119,11 +170,13 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
           const uint32_t slot = g % C::STAGES;
           if (g >= C::STAGES) mbar_wait(&empty[slot], ((g / C::STAGES) - 1) & 1);
           mbar_arrive_expect_tx(&full[slot], C::STAGE_BYTES);
-          const int dd0 = T.dd_lo + c * C::KC;
+          const int dc = T.dc_lo + c;
           const int kp = (int)imod(T.kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
           double2* gs = smem + slot * C::STAGE;
-          tma_load_4d(gs, &tmG, T.ch * C::NFH0 * 16, T.E - A.Dmax + dd0, kp, T.item.b_in, &full[slot]);
-          tma_load_4d(gs + C::G_STAGE, &tmC, 2 * dd0, q, 0, (int)(T.item.pair0 - A.cp0), &full[slot]);
+          tma_load_4d(gs, &tmG, T.ch * C::NFH0 * 16, T.E - A.Dmax + dc * C::KC, kp, T.item.b_in, &full[slot]);
+          tma_load_4d(gs + C::G_STAGE, &tmS, T.ch * C::NFH0 * 8, T.E - A.Dmax + dc * C::KC, kp, T.item.b_in, &full[slot]);
+          bulk_load(gs + C::G_STAGE + C::S_STAGE, A.coef + (((int64_t)T.il * A.Nqz + q) * A.ndc + dc) * C::C_STAGE,
+                    C::C_STAGE * 16, &full[slot]);
           if (++c == T.nchunk) {
             c = 0;
             ++q;
@@ -155,13 +208,15 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       const uint32_t slot = g % C::STAGES;
       mbar_wait(&full[slot], (g / C::STAGES) & 1);
       if (active) {
-        const int kc = min(C::KC, T.dd_hi - (T.dd_lo + c * C::KC));
-        const double2* gs = smem + slot * C::STAGE + (lane & 3) * C::NPS + (lane >> 2) + f0 * 8;
-        const double2* cs = smem + slot * C::STAGE + C::G_STAGE + row * C::KCP + (lane & 3);
+        const int kc = C::KC;
+        const int boff = (lane & 3) * C::NPS + (lane >> 2) + f0 * 8;
+        const double2* gs = smem + slot * C::STAGE + boff;
+        const double* ss = reinterpret_cast<const double*>(smem + slot * C::STAGE + C::G_STAGE) + boff;
+        const double2* cs = smem + slot * C::STAGE + C::G_STAGE + C::S_STAGE + row * C::KCP + (lane & 3);
         if (nfw == C::TMAXW) {
-          sigma_stage<C::TMAXW, C::NPS, C::KC>(acc, gs, cs, kc);
+          sigma_stage<C::TMAXW, C::NPS, C::KC>(acc, gs, ss, cs, kc);
         } else {
-          if constexpr (C::TMAXW > 1) sigma_stage<C::TMAXW - 1, C::NPS, C::KC>(acc, gs, cs, kc);
+          if constexpr (C::TMAXW > 1) sigma_stage<C::TMAXW - 1, C::NPS, C::KC>(acc, gs, ss, cs, kc);
         }
       }
       __syncwarp();
@@ -303,7 +358,7 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  CUtensorMap tmG, tmC;
+  CUtensorMap tmG, tmS;
   const uint64_t NN = (uint64_t)a.NN;
   {
     const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
@@ -313,11 +368,11 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     if (e != cudaSuccess) return e;
   }
   {
-    const uint64_t D = (uint64_t)a.DWp;
-    const uint64_t dims[4] = {2 * D, (uint64_t)a.Nqz, 9, (uint64_t)a.npairs_chunk};
-    const uint64_t strides[3] = {D * 16, (uint64_t)a.Nqz * D * 16, 9ull * a.Nqz * D * 16};
-    const uint32_t box[4] = {2 * C::KCP, 1, 9, kMaxPairs};
-    cudaError_t e = make_tmap_f64(&tmC, a.coef, 4, dims, strides, box);
+    const uint64_t NS = (NN + 1) & ~1ull;   // even row stride of the Re+Im plane
+    const uint64_t dims[4] = {NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+    const uint64_t strides[3] = {NS * 8, (uint64_t)a.NE * NS * 8, (uint64_t)a.Nkz * a.NE * NS * 8};
+    const uint32_t box[4] = {C::NPS, C::KC, 1, 1};
+    cudaError_t e = make_tmap_f64(&tmS, a.Gsum, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
   SigmaArgs b = a;
@@ -330,7 +385,7 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t grid = std::min<int64_t>(b.ntiles, nsm);
-  k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmC, b);
+  k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmS, b);
   return cudaGetLastError();
 }
 

@@ -38,7 +38,11 @@ struct qt_sse_plan_s {
   double2* ws = nullptr;
   size_t ws_bytes = 0;
   double2* ws_g = nullptr;      // atom-major copies of G^<, G^> [2][Nwin][Nkz][NE][NN]
+  double* ws_gs = nullptr;      // their Re + Im planes [2][Nwin][Nkz][NE][NN rounded up to even]
+  size_t gs_elems() const { return (size_t)d.Nkz * d.NE * Nwin * ((NN + 1) & ~int64_t(1)); }
   size_t gt_offset = 0;         // byte offset of the Σ Gt scratch inside ws
+  bool sig_tma = true;          // Norb <= 10: TMA/3M k_sigma + separate sandwich
+  int64_t ndc = 0;              // 16-shift chunks of the Σ coefficient window
   size_t g_elems = 0;
   double flops[4] = {0, 0, 0, 0};
   // host-execute staging
@@ -274,6 +278,7 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_pi_pair_item);
   cudaFree(p->ws);
   cudaFree(p->ws_g);
+  cudaFree(p->ws_gs);
   cudaFree(p->sendbuf);
   cudaFree(p->recvbuf);
   nccl_comm_destroy(p->comm);
@@ -404,7 +409,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
 
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
-  const size_t w_per_item = (size_t)d.Nkz * d.NE * kRows * p->NN * sizeof(double2);
+  const size_t w_per_item = (size_t)d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
   size_t budget = d.workspace_limit;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
@@ -414,9 +419,10 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
     budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
   }
-  const size_t need_min = coef_per_pair * kMaxPairs + w_per_item + 256;
+  const size_t coef_item_t = (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * 20 * sizeof(double2);
+  const size_t need_min = std::max(coef_per_pair * kMaxPairs, coef_item_t) + w_per_item + 512;
   if (budget < need_min) budget = need_min;
-  const size_t full = std::max(coef_per_pair * p->n_sig_pairs + w_per_item * p->sig_items.size() + 256,
+  const size_t full = std::max((coef_per_pair * kMaxPairs + coef_item_t + w_per_item) * p->sig_items.size() + 512,
                                w_per_item * p->pi_items.size());
   p->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
   // chunk item ranges so that each chunk's pairs fit the workspace
@@ -437,28 +443,30 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     bounds.push_back((int64_t)items.size());
   };
   make_chunks(p->pi_items, w_per_item, false, p->pi_chunks);
-  // Σ chunks: coefficient tables of the chunk's pairs + (Norb <= 10) the Gt scratch of its items;
-  // the workspace is [coef region (max chunk pairs) | Gt region]
+  // Σ chunks. TMA path (Norb <= 10): per item a tiled coefficient block [q][16-shift chunk][72][20] +
+  // its Gt scratch; cp.async path (Norb 11, 12): per pair coefficient rows. Workspace = [coef | Gt].
   {
-    const bool gt = d.Norb <= 10;
-    const size_t gt_item = gt ? w_per_item : 0;
+    p->sig_tma = d.Norb <= 10;
+    p->ndc = (p->Dwin + 15) / 16;
+    const size_t coef_item = (size_t)d.Nqz * p->ndc * kRows * 20 * sizeof(double2);
+    const size_t gt_item = p->sig_tma ? w_per_item : 0;
     p->sig_chunks.clear();
     p->sig_chunks.push_back(0);
-    int64_t np = 0, ni = 0, max_np = 0;
+    size_t coef_acc = 0, gt_acc = 0, coef_max = 0;
     for (size_t i = 0; i < p->sig_items.size(); ++i) {
-      const int64_t u = p->sig_items[i].npair;
-      if (ni > 0 && (size_t)(np + u) * coef_per_pair + (size_t)(ni + 1) * gt_item > p->ws_bytes) {
+      const size_t cu = p->sig_tma ? coef_item : (size_t)p->sig_items[i].npair * coef_per_pair;
+      if (gt_acc > 0 && coef_acc + cu + gt_acc + gt_item + 256 > p->ws_bytes) {
         p->sig_chunks.push_back((int64_t)i);
-        max_np = std::max(max_np, np);
-        np = 0;
-        ni = 0;
+        coef_max = std::max(coef_max, coef_acc);
+        coef_acc = 0;
+        gt_acc = 0;
       }
-      np += u;
-      ni += 1;
+      coef_acc += cu;
+      gt_acc += gt_item == 0 ? 1 : gt_item;
     }
-    max_np = std::max(max_np, np);
+    coef_max = std::max(coef_max, coef_acc);
     p->sig_chunks.push_back((int64_t)p->sig_items.size());
-    p->gt_offset = ((size_t)max_np * coef_per_pair + 255) & ~size_t(255);
+    p->gt_offset = (coef_max + 255) & ~size_t(255);
   }
 
   qt_status s2;
@@ -470,7 +478,8 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     return s2;
   }
   p->g_elems = (size_t)d.Nkz * d.NE * p->Nwin * p->NN;
-  if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess) {
+  if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc(&p->ws_gs, 2 * p->gs_elems() * sizeof(double)) != cudaSuccess) {
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
   }
@@ -485,9 +494,15 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
       return QT_ERR_NCCL;
     }
   }
-  if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) {
+  // + slack: the last Π stage of a chunk may read one energy block past the chunk (its results are unused)
+  if (cudaMalloc(&p->ws, p->ws_bytes + (1 << 20)) != cudaSuccess) {
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
+  }
+  // zero once: padding columns of the Π W tiles are never written and must hold finite values
+  if (cudaMemsetAsync(p->ws, 0, p->ws_bytes + (1 << 20), cs) != cudaSuccess) {
+    qt_sse_destroy(p);
+    return QT_ERR_CUDA;
   }
   if (cudaStreamSynchronize(cs) != cudaSuccess) {
     qt_sse_destroy(p);
@@ -504,7 +519,7 @@ extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
   o->w_lo = p->w_lo;
   o->w_hi = p->w_hi;
   o->npairs = p->n_pi_pairs;
-  o->workspace_bytes = p->ws_bytes + 2 * p->g_elems * sizeof(double2);
+  o->workspace_bytes = p->ws_bytes + 2 * p->g_elems * sizeof(double2) + 2 * p->gs_elems() * sizeof(double);
   o->flops_sigma = p->flops[0] + p->flops[1];
   o->flops_pi = p->flops[2] + p->flops[3];
   o->halo_bytes = (double)p->recv_total;
@@ -524,8 +539,8 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
   const size_t sig_bytes = (size_t)d.Nkz * d.NE * p->Nout * p->NN * sizeof(double2);
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, d.Nkz, d.NE, p->Nwin, p->NN, cs));
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, d.NE, p->Nwin, p->NN, cs));
   for (int X = 0; X < 2; ++X) {
     void* S = X == 0 ? SL : SG;
     QT_CUDA(cudaMemsetAsync(S, 0, sig_bytes, cs));
@@ -549,10 +564,16 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       ca.DWp = p->DWp;
       ca.Dmax = (int)p->Dmax;
       ca.shift0 = d.shift0;
-      QT_LAUNCH(QT_K_SIGMA_COEF, launch_sigma_coef(ca, cs));
+      ca.tiled = p->sig_tma;
+      ca.item0 = i0;
+      ca.nitems = i1 - i0;
+      ca.ndc = p->ndc;
+      ca.Dwin = p->Dwin;
+      QT_LAUNCH(QT_K_SIGMA_COEF, p->sig_tma ? launch_sigma_coef_tiled(ca, cs) : launch_sigma_coef(ca, cs));
       SigmaArgs sa;
       sa.G = (const double2*)(X == 0 ? GL : GG);
       sa.Gam = p->ws_g + (X == 0 ? 0 : p->g_elems);
+      sa.Gsum = p->ws_gs + (X == 0 ? 0 : p->gs_elems());
       sa.coef = p->ws;
       sa.Gt = reinterpret_cast<double2*>(reinterpret_cast<char*>(p->ws) + p->gt_offset);
       sa.cp0 = pp0;
@@ -573,6 +594,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.Norb = (int)d.Norb;
       sa.NN = (int)p->NN;
       sa.Dmax = (int)p->Dmax;
+      sa.ndc = (int)p->ndc;
       sa.Dwin = (int)p->Dwin;
       QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
       QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
@@ -592,8 +614,8 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
     if (q == PL || q == PG) return QT_ERR_INVALID_ARG;
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, d.Nkz, d.NE, p->Nwin, p->NN, cs));
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, d.NE, p->Nwin, p->NN, cs));
   for (int X = 0; X < 2; ++X) {
     const double2* GXam = p->ws_g + (X == 0 ? 0 : p->g_elems);
     const double2* GY = (const double2*)(X == 0 ? GG : GL);
