@@ -40,14 +40,17 @@ struct PiWArgs {
   const PiPair* pairs;
   const PiItem* items;
   const int32_t* pair_item;   // pair -> item
-  double2* W;                 // [item - i0][Nkz][NE][72 rows (t,ij)][NN]
+  double2* W;                 // [item - i0][Nkz][xy chunk][NE][72 rows (t,ij)][20]
+  double* Wsum;               // Re + Im of W, same layout (doubles)
   int64_t p0, i0, Nwin, Nb;
   int NE, Nkz, Norb, NN, nEB;
 };
 
 struct PiCArgs {
   const double2* GX;     // G^X atom-major [Nwin][Nkz][NE][NN]
+  const double* GXsum;   // Re + Im of GX, row stride NN rounded up to even
   const double2* W;
+  const double* Wsum;
   const PiItem* items;
   const PiPair* pairs;
   double2* Pi;

@@ -45,7 +45,9 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
   }
   constexpr int XC = 20;                       // = PiCfg::XC
   constexpr int NXC = (NN + XC - 1) / XC;
-  double2* Wdst = A.W + ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NE * kRows * XC;
+  const int64_t wblk = ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NE * kRows * XC;
+  double2* Wdst = A.W + wblk;
+  double* Sdst = A.Wsum + wblk;
   for (int e0 = 0; e0 < A.NE; e0 += kWE) {
     const int ne = min(kWE, A.NE - e0);
     __syncthreads();
@@ -93,7 +95,9 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
 #pragma unroll
       for (int x = 0; x < NO; ++x) {
         const int xy = x * NO + y, xc = xy / XC, c = xy - xc * XC;
-        Wdst[(((int64_t)xc * A.NE + e0 + e) * kRows + (t0 + t) * 9 + ij) * XC + c] = s[x];
+        const int64_t o = (((int64_t)xc * A.NE + e0 + e) * kRows + (t0 + t) * 9 + ij) * XC + c;
+        Wdst[o] = s[x];
+        Sdst[o] = s[x].x + s[x].y;   // Gauss 3M A-side operand
       }
     }
   }
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
 // warps 0..17 consume (warp w: m-fragment w%9 of the rows (t,ij), half of the m-column fragments).
 struct PiCfg {
   static constexpr int XC = 20;      // xy per stage: 5 DMMA k-steps; row stride 80 words ≡ 16 (mod 32)
-  static constexpr int EC = 2;       // energies per stage
+  static constexpr int EC = 1;       // energies per stage
   static constexpr int STAGES = 3;
   static constexpr int W_STAGE = EC * kRows * XC;
   static constexpr int NCONS = 18;
@@ -116,55 +120,55 @@ template <int NFM>
 struct PiTma {
   static constexpr int NWP = NFM * 8;
   static constexpr int GROWS = PiCfg::EC + NWP - 1;
-  static constexpr int G_STAGE = ((GROWS * PiCfg::XC) + 7) & ~7;   // 128-byte multiple
-  static constexpr int STAGE = PiCfg::W_STAGE + G_STAGE;
-  static constexpr uint32_t STAGE_BYTES = (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 16;
+  static constexpr int WS_STAGE = PiCfg::W_STAGE / 2;                 // Re+Im of W (doubles), complex units
+  static constexpr int G_STAGE = ((GROWS * PiCfg::XC) + 7) & ~7;       // 128-byte multiple
+  static constexpr int GS_STAGE = ((GROWS * PiCfg::XC / 2) + 7) & ~7;  // Re+Im of the G window (doubles)
+  static constexpr int STAGE = PiCfg::W_STAGE + WS_STAGE + G_STAGE + GS_STAGE;
+  static constexpr uint32_t STAGE_BYTES = (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 16 + (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 8;
   static constexpr int NF0 = (NFM + 1) / 2, NF1 = NFM / 2;
   static constexpr size_t SMEM = (size_t)PiCfg::STAGES * STAGE * 16 + 2 * PiCfg::STAGES * 8 + 128;
 };
 
 // Complex k-step over N column fragments with Gauss's 3-multiplication form: per fragment
 // T1 += Ar·Br, T2 += Ai·Bi, T3 += (Ar+Ai)(Br+Bi) (three real DMMAs instead of four); the complex
-// result is Re = T1 - T2, Im = T3 - T1 - T2 (formed once, in the epilogue).
+// result is Re = T1 - T2, Im = T3 - T1 - T2 (formed once, in the epilogue). Both Re+Im operands come
+// precomputed from shared memory (no FP64 adds on the tensor pipe's issue port).
 template <int N>
-__device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, const double2* gb) {
-  const double as = a.x + a.y;
+__device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const double2* gb, const double* sb) {
 #pragma unroll
   for (int f = 0; f < N; ++f) {
     const double2 b = gb[f * 8 * PiCfg::XC];
-    cmma3(acc[f], a.x, a.y, as, b.x, b.y);
+    cmma3s(acc[f], a.x, a.y, as, b.x, b.y, sb[f * 8 * PiCfg::XC]);
   }
 }
 
-template <int N>
-__device__ __forceinline__ void pi_energy(C3Acc* acc, const double2* ws, const double2* gs) {
-#pragma unroll
-  for (int k4 = 0; k4 < PiCfg::XC; k4 += 4) pi_kstep<N>(acc, ws[k4], gs + k4);
-}
-
-// DMMA work of one stage for one warp. rem = NE - E0 - shift0: energy E0+el has in-window columns
-// m < rem - el; column fragments without any are skipped (fast path: all NFW fragments live).
+// DMMA work of one stage (EC energies) for one warp. rem = NE - E0 - shift0: energy E0+el has
+// in-window columns m < rem - el; column fragments without any are skipped.
 template <int NFW>
-__device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double2* gs, int rem, int f0) {
+__device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double* wss, const double2* gs,
+                                         const double* gss, int rem, int f0) {
   static_assert(NFW > 0, "empty fragment range");
   using C = PiCfg;
 #pragma unroll
   for (int el = 0; el < C::EC; ++el) {
     const int nfe = min(NFW, ((rem - el + 7) >> 3) - f0);
     const double2* w = ws + el * kRows * C::XC;
+    const double* wsm = wss + el * kRows * C::XC;
     const double2* g = gs + el * C::XC;
+    const double* gsm = gss + el * C::XC;
     if (nfe == NFW) {
-      pi_energy<NFW>(acc, w, g);
+#pragma unroll
+      for (int k4 = 0; k4 < C::XC; k4 += 4) pi_kstep<NFW>(acc, w[k4], wsm[k4], g + k4, gsm + k4);
     } else if (nfe > 0) {
 #pragma unroll
       for (int k4 = 0; k4 < C::XC; k4 += 4) {
         const double2 a = w[k4];
-        const double as = a.x + a.y;
+        const double as = wsm[k4];
 #pragma unroll
         for (int f = 0; f < NFW; ++f) {
           if (f < nfe) {
             const double2 b = g[k4 + f * 8 * C::XC];
-            cmma3(acc[f], a.x, a.y, as, b.x, b.y);
+            cmma3s(acc[f], a.x, a.y, as, b.x, b.y, gsm[k4 + f * 8 * C::XC]);
           }
         }
       }
@@ -174,7 +178,7 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
 
 template <int NFM>
 __global__ void __launch_bounds__(PiCfg::THREADS, 1)
-    k_pi_contract(const __grid_constant__ CUtensorMap tmG, PiCArgs A) {
+    k_pi_contract(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmGS, PiCArgs A) {
   using C = PiCfg;
   using T = PiTma<NFM>;
   extern __shared__ uint8_t smem_raw[];
@@ -213,6 +217,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   if (warp == C::NCONS) {
     if (lane == 0) {
       prefetch_tmap(&tmG);
+      prefetch_tmap(&tmGS);
       int kz = 0, xc = 0, ec = 0;
       for (int st = 0; st < nst; ++st) {
         const int slot = st % C::STAGES;
@@ -220,9 +225,12 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         mbar_arrive_expect_tx(&full[slot], T::STAGE_BYTES);
         double2* ws = smem + slot * T::STAGE;
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
-        bulk_load(ws, A.W + ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NE + ec * C::EC) * kRows * C::XC,
-                  C::W_STAGE * 16, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
+        const int64_t woff = ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NE + ec * C::EC) * kRows * C::XC;
+        bulk_load(ws, A.W + woff, C::W_STAGE * 16, &full[slot]);
+        bulk_load(ws + C::W_STAGE, A.Wsum + woff, C::W_STAGE * 8, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE + T::WS_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE + T::WS_STAGE + T::G_STAGE, &tmGS, xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in,
+                    &full[slot]);
         if (++ec == nec) {
           ec = 0;
           if (++xc == nxc) {
@@ -239,13 +247,18 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
       const int slot = st % C::STAGES;
       mbar_wait(&full[slot], (st / C::STAGES) & 1);
       if (active) {
-        const double2* ws = smem + slot * T::STAGE + (mi * 8 + (lane >> 2)) * C::XC + (lane & 3);
-        const double2* gs = smem + slot * T::STAGE + C::W_STAGE + (f0 * 8 + (lane >> 2)) * C::XC + (lane & 3);
+        const int aoff = (mi * 8 + (lane >> 2)) * C::XC + (lane & 3);
+        const int boff = (f0 * 8 + (lane >> 2)) * C::XC + (lane & 3);
+        const double2* st0 = smem + slot * T::STAGE;
+        const double2* ws = st0 + aoff;
+        const double* wss = reinterpret_cast<const double*>(st0 + C::W_STAGE) + aoff;
+        const double2* gs = st0 + C::W_STAGE + T::WS_STAGE + boff;
+        const double* gss = reinterpret_cast<const double*>(st0 + C::W_STAGE + T::WS_STAGE + T::G_STAGE) + boff;
         const int rem = A.NE - ec * C::EC - A.shift0;
         if (upper) {
-          if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, gs, rem, f0);
+          if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, wss, gs, gss, rem, f0);
         } else {
-          pi_stage<T::NF0>(acc, ws, gs, rem, f0);
+          pi_stage<T::NF0>(acc, ws, wss, gs, gss, rem, f0);
         }
       }
       __syncwarp();
@@ -287,7 +300,15 @@ static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
     configured = true;
   }
   const uint64_t NN = (uint64_t)a.NN;
-  CUtensorMap tmG;
+  CUtensorMap tmG, tmGS;
+  {
+    const uint64_t NS = (NN + 1) & ~1ull;
+    const uint64_t dims[4] = {NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+    const uint64_t strides[3] = {NS * 8, (uint64_t)a.NE * NS * 8, (uint64_t)a.Nkz * a.NE * NS * 8};
+    const uint32_t box[4] = {PiCfg::XC, (uint32_t)T::GROWS, 1, 1};
+    cudaError_t e = make_tmap_f64(&tmGS, a.GXsum, 4, dims, strides, box);
+    if (e != cudaSuccess) return e;
+  }
   {
     const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
     const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
@@ -297,7 +318,7 @@ static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
   }
   const int64_t nblk = a.nitems * a.Nqz;
   if (nblk == 0) return cudaSuccess;
-  k_pi_contract<NFM><<<(unsigned)nblk, PiCfg::THREADS, T::SMEM, st>>>(tmG, a);
+  k_pi_contract<NFM><<<(unsigned)nblk, PiCfg::THREADS, T::SMEM, st>>>(tmG, tmGS, a);
   return cudaGetLastError();
 }
 
