@@ -194,6 +194,13 @@ def test_cfg3_sampled_random():
 
 
 @pytest.mark.slow
+def test_cfg3_sampled_integer_bit_exact():
+    """Integer-exact inputs at full cfg3 size: sampled blocks must equal the oracle bit for bit (pin P2),
+    which checks every index map and the 3M recombination in the bench launch configuration."""
+    _sampled_parity(qtgen.problem("cfg3"), qtgen.INTEGER, 24, 48, exact=True)
+
+
+@pytest.mark.slow
 def test_cfg3_delta_full_coverage():
     """P3 at full size: D = δ reduces Σ to plain ∇H·G·∇H sandwiches, checked over EVERY block with cuBLAS."""
     p = qtgen.problem("cfg3")
