@@ -134,7 +134,17 @@ def calibrated_oracle(p, host, target_s, seed=7):
 
 
 # ---------------------------------------------------------------- main
+def _claim_stdout():
+    """Route everything else written to fd 1 (NCCL banners, library prints) to stderr; return a file
+    object on the real stdout for the single JSON line."""
+    sys.stdout.flush()
+    real = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(real, "w")
+
+
 def main():
+    out_stream = _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -154,7 +164,7 @@ def main():
     p = qtgen.problem(args.config)
 
     if args.impl == "reference":
-        return run_reference(args, p, rank, world)
+        return run_reference(args, p, rank, world, out_stream)
 
     import torch
     import torch.distributed as dist
@@ -323,13 +333,13 @@ def main():
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "halo_bytes_per_rank": info["halo_bytes"],
                "clocks": clk, "pct_fp64_peak": round(value / (FP64_PEAK_TFLOPS * world) * 100, 2)}
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=out_stream, flush=True)
     plan.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_reference(args, p, rank, world):
+def run_reference(args, p, rank, world, out_stream=sys.stdout):
     """--impl reference: the CPU oracle as it stands on the host cores, bounded sample per step."""
     if rank != 0:
         return
@@ -356,7 +366,7 @@ def run_reference(args, p, rank, world):
                             "sample": f"per step {ns} Σ blocks + ~{npi} Π blocks (random); "
                                       f"{nsig} + {npis} blocks in {tt:.1f} s total"},
            "e2e": {"value": round(v, 6), "unit": "Tflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out), file=out_stream, flush=True)
 
 
 if __name__ == "__main__":
