@@ -100,6 +100,7 @@ struct PiItem {
 };
 
 constexpr int kMaxPairs = 8;   // pairs per item -> 9*8 = 72 rows = 9 m-fragments
+constexpr int kMaxEpt = 4;     // energies per Σ tile for small items (1 pair: 2 m-fragments per energy)
 constexpr int kRows = 72;
 constexpr int kWarps = 9;
 constexpr int kThreads = kWarps * 32;

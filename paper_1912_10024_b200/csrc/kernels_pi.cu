@@ -207,8 +207,13 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   }
   __syncthreads();
 
-  const int mi = warp % 9;
-  const bool upper = warp >= 9;
+  // Warp w issues on sub-partition w % 4 (0, 1: five consumer warps; 2, 3: four). Roles (m-fragment mi,
+  // lower/upper column fragments) are placed so the 5-fragment (lower) warps fill sub-partitions 2, 3 and
+  // the 4-fragment ones 0, 1: DMMA work per sub-partition 21/20/20/20 for NFM = 9 (was 23/22/18/18).
+  constexpr int kPiRole[18] = {8, 10, 0, 1, 9, 12, 2, 3, 11, 14, 4, 5, 13, 16, 6, 7, 15, 17};
+  const int role = warp < C::NCONS ? kPiRole[warp] : 0;
+  const int mi = role % 9;
+  const bool upper = role >= 9;
   const int f0 = upper ? T::NF0 : 0;
   C3Acc acc[T::NF0];
 #pragma unroll

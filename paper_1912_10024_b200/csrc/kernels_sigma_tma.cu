@@ -100,6 +100,13 @@ struct SigTmaCfg {
   static constexpr int THREADS = (NCONS + 1) * 32;
   static constexpr int TMAXW = (NFH0 + 1) / 2;   // n-fragments per consumer warp (max)
   static constexpr size_t SMEM = (size_t)PIPE * 16 + 2 * STAGES * 8 + 128;
+  // Multi-energy stages (items of <= 3 pairs, see sig_ept): G rows for up to kMaxEpt energies (Hankel:
+  // energy E+e reads the same rows shifted by e) and a coefficient tile of <= 32 rows.
+  static constexpr int GROWS_M = KC + kMaxEpt - 1;
+  static constexpr int G_STAGE_M = (GROWS_M * NPS + 7) & ~7;
+  static constexpr int S_STAGE_M = ((GROWS_M * NPS + 1) / 2 + 7) & ~7;
+  __host__ __device__ static constexpr uint32_t stage_bytes_m(int F) { return GROWS_M * NPS * 24 + F * 8 * KCP * 16; }
+  static_assert(G_STAGE_M + S_STAGE_M + 32 * KCP <= STAGE, "multi-energy stage fits");
   static_assert(2 * NPS <= 256, "TMA box width");
   static_assert((G_STAGE * 16) % 128 == 0 && (STAGE * 16) % 128 == 0, "TMA destination alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -125,24 +132,32 @@ __device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const
 
 struct SigTile {
   SigItem item;
-  int E, kz, ch, il, dc_lo, nchunk, nst;
+  int E, kz, ch, il, dc_lo, nchunk, nst, F, ept;
+  bool skip;
 };
 
 template <int KC>
 __device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
   SigTile T;
-  T.ch = (int)(t & 1);
+  // Column half alternates between a CTA's consecutive tiles (the two halves differ in work; with an
+  // even grid, ch = t & 1 would give every CTA the same half for the whole launch).
+  T.ch = (int)((t ^ (t / gridDim.x)) & 1);
   t >>= 1;
   T.E = (int)(t % A.NE);
   T.kz = (int)((t / A.NE) % A.Nkz);
   T.il = (int)(t / ((int64_t)A.NE * A.Nkz));
   T.item = A.items[T.il];
-  // K range: shifts d = 16*dc + k - Dmax with E+d in [0,NE) (R7), in whole 16-shift chunks (rows outside
-  // the window are zero-filled by TMA; shifts beyond the table are zero coefficients).
-  T.dc_lo = max(0, A.Dmax - T.E) / KC;
+  // An item of n pairs fills F = ceil(9n/8) of the 9 m-fragments; small items process ept = 9/F
+  // consecutive energies per tile (tiles with E % ept != 0 are empty), one energy per group of F.
+  T.F = (9 * T.item.npair + 7) / 8;
+  T.ept = min(kMaxEpt, 9 / T.F);
+  T.skip = (T.E % T.ept) != 0;
+  // K range: shifts d = 16*dc + k - Dmax with E+e+d in [0,NE) for some e < ept (R7), in whole 16-shift
+  // chunks (rows outside the window are zero-filled by TMA; shifts beyond the table are zero coefficients).
+  T.dc_lo = max(0, A.Dmax - (T.E + T.ept - 1)) / KC;
   const int dc_hi = (min(A.Dwin, A.Dmax - T.E + A.NE) + KC - 1) / KC;
   T.nchunk = dc_hi - T.dc_lo;
-  T.nst = A.Nqz * T.nchunk;
+  T.nst = T.skip ? 0 : A.Nqz * T.nchunk;
   return T;
 }
 
@@ -151,7 +166,8 @@ __device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
 // (complex, from the 3M accumulators) to the chunk's scratch [item][kz][E][72][Norb²].
 template <int NF>
 __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
-    k_sigma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmS, SigmaArgs A) {
+    k_sigma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmS,
+            const __grid_constant__ CUtensorMap tmGm, const __grid_constant__ CUtensorMap tmSm, SigmaArgs A) {
   using C = SigTmaCfg<NF>;
   extern __shared__ uint8_t smem_raw[];
   double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -173,6 +189,8 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     if (lane == 0) {
       prefetch_tmap(&tmG);
       prefetch_tmap(&tmS);
+      prefetch_tmap(&tmGm);
+      prefetch_tmap(&tmSm);
       uint32_t g = 0;
       for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
         const SigTile T = sig_tile<C::KC>(A, t);
@@ -180,14 +198,18 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
         for (int st = 0; st < T.nst; ++st, ++g) {
           const uint32_t slot = g % C::STAGES;
           if (g >= C::STAGES) mbar_wait(&empty[slot], ((g / C::STAGES) - 1) & 1);
-          mbar_arrive_expect_tx(&full[slot], C::STAGE_BYTES);
+          const bool multi = T.ept > 1;
+          mbar_arrive_expect_tx(&full[slot], multi ? C::stage_bytes_m(T.F) : C::STAGE_BYTES);
           const int dc = T.dc_lo + c;
           const int kp = (int)imod(T.kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
           double2* gs = smem + slot * C::STAGE;
-          tma_load_4d(gs, &tmG, T.ch * C::NFH0 * 16, T.E - A.Dmax + dc * C::KC, kp, T.item.b_in, &full[slot]);
-          tma_load_4d(gs + C::G_STAGE, &tmS, T.ch * C::NFH0 * 8, T.E - A.Dmax + dc * C::KC, kp, T.item.b_in, &full[slot]);
-          bulk_load(gs + C::G_STAGE + C::S_STAGE, A.coef + (((int64_t)T.il * A.Nqz + q) * A.ndc + dc) * C::C_STAGE,
-                    C::C_STAGE * 16, &full[slot]);
+          const int soff = multi ? C::G_STAGE_M : C::G_STAGE;
+          const int coff = soff + (multi ? C::S_STAGE_M : C::S_STAGE);
+          const int r0 = T.E - A.Dmax + dc * C::KC;
+          tma_load_4d(gs, multi ? &tmGm : &tmG, T.ch * C::NFH0 * 16, r0, kp, T.item.b_in, &full[slot]);
+          tma_load_4d(gs + soff, multi ? &tmSm : &tmS, T.ch * C::NFH0 * 8, r0, kp, T.item.b_in, &full[slot]);
+          bulk_load(gs + coff, A.coef + (((int64_t)T.il * A.Nqz + q) * A.ndc + dc) * C::C_STAGE,
+                    (multi ? T.F * 8 : kRows) * C::KCP * 16, &full[slot]);
           if (++c == T.nchunk) {
             c = 0;
             ++q;
@@ -198,19 +220,33 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     return;
   }
 
-  // ---------------- consumers: warp -> (m-fragment, quarter q of the n-fragments of the half-tile).
-  // q = 1 warps (fewer fragments) sit on the sub-partitions with 5 consumer warps (warp w runs on w % 4).
-  constexpr int kRole[18] = {9, 14, 1, 5, 10, 15, 2, 6, 11, 16, 3, 7, 12, 17, 4, 8, 13, 0};
-  const int role = kRole[warp];
-  const int mi = role % 9, q = role / 9;
-  const int row = mi * 8 + (lane >> 2);
+  // ---------------- consumers: warp -> role (m-fragment mi, part q of the half-tile's n-fragments).
+  // Warp w issues on sub-partition w % 4; sub-partitions 0, 1 hold 5 consumer warps, 2, 3 hold 4. The
+  // role tables balance the DMMA work per sub-partition (the slowest one paces the CTA's pipeline):
+  //  kRoleA, split (ceil, floor): all 9 q=1 warps (fewer fragments) on the 5-warp sub-partitions,
+  //          e.g. Norb=10 half 0 (4+3 fragments) -> 15/16/16/16;
+  //  kRoleB, split (n/2+1, n/2-1) for an even fragment count n: 3+3+1+2 q=1 warps,
+  //          e.g. Norb=10 half 1 (4+2 fragments) -> 14/14/14/12 instead of 15/15/12/12.
+  constexpr int kRoleA[18] = {9, 14, 1, 5, 10, 15, 2, 6, 11, 16, 3, 7, 12, 17, 4, 8, 13, 0};
+  constexpr int kRoleB[18] = {9, 12, 15, 16, 10, 13, 4, 17, 11, 14, 5, 7, 0, 2, 6, 8, 1, 3};
+  const int roleA = kRoleA[warp], roleB = kRoleB[warp];
   uint32_t g = 0;
   for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
     const SigTile T = sig_tile<C::KC>(A, t);
+    if (T.skip) continue;
     const int nfh = T.ch ? C::NFH1 : C::NFH0;
-    const int nfw = q ? nfh / 2 : (nfh + 1) / 2;
-    const int f0 = q ? (nfh + 1) / 2 : 0;
-    const bool active = mi * 8 < 9 * T.item.npair && nfw > 0;
+    const bool split_b = (nfh % 2 == 0) && nfh / 2 + 1 == C::TMAXW;
+    const int role = split_b ? roleB : roleA;
+    const int mi = role % 9, q = role / 9;
+    const int n0 = split_b ? nfh / 2 + 1 : (nfh + 1) / 2;
+    const int nfw = q ? nfh - n0 : n0;
+    const int f0 = q ? n0 : 0;
+    const int e = mi / T.F, ml = mi - e * T.F;      // energy E+e, m-fragment ml of the item's rows
+    const int row = ml * 8 + (lane >> 2);
+    const bool active = e < T.ept && T.E + e < A.NE && nfw > 0;
+    const bool multi = T.ept > 1;
+    const int soff = multi ? C::G_STAGE_M : C::G_STAGE;
+    const int coff = soff + (multi ? C::S_STAGE_M : C::S_STAGE);
     C3Acc acc[C::TMAXW];
 #pragma unroll
     for (int f = 0; f < C::TMAXW; ++f) acc[f] = C3Acc{};
@@ -220,14 +256,16 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       mbar_wait(&full[slot], (g / C::STAGES) & 1);
       if (active) {
         const int kc = C::KC;
-        const int boff = (lane & 3) * C::NPS + (lane >> 2) + f0 * 8;
+        const int boff = ((lane & 3) + e) * C::NPS + (lane >> 2) + f0 * 8;
         const double2* gs = smem + slot * C::STAGE + boff;
-        const double* ss = reinterpret_cast<const double*>(smem + slot * C::STAGE + C::G_STAGE) + boff;
-        const double2* cs = smem + slot * C::STAGE + C::G_STAGE + C::S_STAGE + row * C::KCP + (lane & 3);
+        const double* ss = reinterpret_cast<const double*>(smem + slot * C::STAGE + soff) + boff;
+        const double2* cs = smem + slot * C::STAGE + coff + row * C::KCP + (lane & 3);
         if (nfw == C::TMAXW) {
           sigma_stage<C::TMAXW, C::NPS, C::KC>(acc, gs, ss, cs, kc);
-        } else {
+        } else if (nfw == C::TMAXW - 1) {
           if constexpr (C::TMAXW > 1) sigma_stage<C::TMAXW - 1, C::NPS, C::KC>(acc, gs, ss, cs, kc);
+        } else {
+          if constexpr (C::TMAXW > 2) sigma_stage<C::TMAXW - 2, C::NPS, C::KC>(acc, gs, ss, cs, kc);
         }
       }
       __syncwarp();
@@ -235,7 +273,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       if (++c == T.nchunk) c = 0;
     }
     if (active && row < 9 * T.item.npair) {
-      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * kRows + row) * A.NN;
+      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E + e) * kRows + row) * A.NN;
 #pragma unroll
       for (int f = 0; f < C::TMAXW; ++f) {
         if (f < nfw) {
@@ -369,22 +407,25 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  CUtensorMap tmG, tmS;
+  CUtensorMap tmG, tmS, tmGm, tmSm;
   const uint64_t NN = (uint64_t)a.NN;
-  {
-    const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
-    const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
-    const uint32_t box[4] = {2 * C::NPS, C::KC, 1, 1};
-    cudaError_t e = make_tmap_f64(&tmG, a.Gam, 4, dims, strides, box);
-    if (e != cudaSuccess) return e;
-  }
-  {
-    const uint64_t NS = (NN + 1) & ~1ull;   // even row stride of the Re+Im plane
-    const uint64_t dims[4] = {NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
-    const uint64_t strides[3] = {NS * 8, (uint64_t)a.NE * NS * 8, (uint64_t)a.Nkz * a.NE * NS * 8};
-    const uint32_t box[4] = {C::NPS, C::KC, 1, 1};
-    cudaError_t e = make_tmap_f64(&tmS, a.Gsum, 4, dims, strides, box);
-    if (e != cudaSuccess) return e;
+  for (int m = 0; m < 2; ++m) {
+    const uint32_t rows = m ? C::GROWS_M : C::KC;
+    {
+      const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+      const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
+      const uint32_t box[4] = {2 * C::NPS, rows, 1, 1};
+      cudaError_t e = make_tmap_f64(m ? &tmGm : &tmG, a.Gam, 4, dims, strides, box);
+      if (e != cudaSuccess) return e;
+    }
+    {
+      const uint64_t NS = (NN + 1) & ~1ull;   // even row stride of the Re+Im plane
+      const uint64_t dims[4] = {NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+      const uint64_t strides[3] = {NS * 8, (uint64_t)a.NE * NS * 8, (uint64_t)a.Nkz * a.NE * NS * 8};
+      const uint32_t box[4] = {C::NPS, rows, 1, 1};
+      cudaError_t e = make_tmap_f64(m ? &tmSm : &tmS, a.Gsum, 4, dims, strides, box);
+      if (e != cudaSuccess) return e;
+    }
   }
   SigmaArgs b = a;
   b.ntiles = nitems * a.NE * a.Nkz * 2;
@@ -395,8 +436,8 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t grid = std::min<int64_t>(b.ntiles, nsm);
-  k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmS, b);
+  const int64_t grid = std::min<int64_t>(b.ntiles, nsm) & ~int64_t(1);   // even: sig_tile pairs t = 2u, 2u+1 in one round
+  k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmS, tmGm, tmSm, b);
   return cudaGetLastError();
 }
 

@@ -484,6 +484,11 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
   }
+  // the odd-NN padding element of each sum-plane row is never written by k_relayout: keep it a finite zero
+  if (cudaMemsetAsync(p->ws_gs, 0, 2 * p->gs_elems() * sizeof(double), cs) != cudaSuccess) {
+    qt_sse_destroy(p);
+    return QT_ERR_CUDA;
+  }
   if (d.nranks > 1 && d.nccl_unique_id) {
     if ((p->send_total && cudaMalloc(&p->sendbuf, p->send_total) != cudaSuccess) ||
         (p->recv_total && cudaMalloc(&p->recvbuf, p->recv_total) != cudaSuccess)) {
