@@ -41,7 +41,6 @@ struct PiWArgs {
   const PiItem* items;
   const int32_t* pair_item;   // pair -> item
   double2* W;                 // [item - i0][Nkz][xy chunk][NE][72 rows (t,ij)][20]
-  double* Wsum;               // Re + Im of W, same layout (doubles)
   int64_t p0, i0, Nwin, Nb;
   int NE, Nkz, Norb, NN, nEB;
 };
@@ -50,7 +49,6 @@ struct PiCArgs {
   const double2* GX;     // G^X atom-major [Nwin][Nkz][NE][NN]
   const double* GXsum;   // Re + Im of GX, row stride NN rounded up to even
   const double2* W;
-  const double* Wsum;
   const PiItem* items;
   const PiPair* pairs;
   double2* Pi;

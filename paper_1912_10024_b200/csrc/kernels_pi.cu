@@ -47,7 +47,6 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
   constexpr int NXC = (NN + XC - 1) / XC;
   const int64_t wblk = ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NE * kRows * XC;
   double2* Wdst = A.W + wblk;
-  double* Sdst = A.Wsum + wblk;
   for (int e0 = 0; e0 < A.NE; e0 += kWE) {
     const int ne = min(kWE, A.NE - e0);
     __syncthreads();
@@ -97,7 +96,6 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
         const int xy = x * NO + y, xc = xy / XC, c = xy - xc * XC;
         const int64_t o = (((int64_t)xc * A.NE + e0 + e) * kRows + (t0 + t) * 9 + ij) * XC + c;
         Wdst[o] = s[x];
-        Sdst[o] = s[x].x + s[x].y;   // Gauss 3M A-side operand
       }
     }
   }
@@ -120,19 +118,19 @@ template <int NFM>
 struct PiTma {
   static constexpr int NWP = NFM * 8;
   static constexpr int GROWS = PiCfg::EC + NWP - 1;
-  static constexpr int WS_STAGE = PiCfg::W_STAGE / 2;                 // Re+Im of W (doubles), complex units
   static constexpr int G_STAGE = ((GROWS * PiCfg::XC) + 7) & ~7;       // 128-byte multiple
   static constexpr int GS_STAGE = ((GROWS * PiCfg::XC / 2) + 7) & ~7;  // Re+Im of the G window (doubles)
-  static constexpr int STAGE = PiCfg::W_STAGE + WS_STAGE + G_STAGE + GS_STAGE;
-  static constexpr uint32_t STAGE_BYTES = (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 16 + (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 8;
+  static constexpr int STAGE = PiCfg::W_STAGE + G_STAGE + GS_STAGE;
+  static constexpr uint32_t STAGE_BYTES = (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 16 + GROWS * PiCfg::XC * 8;
   static constexpr int NF0 = (NFM + 1) / 2, NF1 = NFM / 2;
   static constexpr size_t SMEM = (size_t)PiCfg::STAGES * STAGE * 16 + 2 * PiCfg::STAGES * 8 + 128;
 };
 
 // Complex k-step over N column fragments with Gauss's 3-multiplication form: per fragment
 // T1 += Ar·Br, T2 += Ai·Bi, T3 += (Ar+Ai)(Br+Bi) (three real DMMAs instead of four); the complex
-// result is Re = T1 - T2, Im = T3 - T1 - T2 (formed once, in the epilogue). Both Re+Im operands come
-// precomputed from shared memory (no FP64 adds on the tensor pipe's issue port).
+// result is Re = T1 - T2, Im = T3 - T1 - T2 (formed once, in the epilogue). The B-side Re+Im (one per
+// fragment) comes precomputed from shared memory; the A-side one (one per k-step, shared by all the
+// warp's fragments) is one DADD per 3·N DMMAs, cheaper than storing and streaming a W sum plane.
 template <int N>
 __device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const double2* gb, const double* sb) {
 #pragma unroll
@@ -145,7 +143,7 @@ __device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const
 // DMMA work of one stage (EC energies) for one warp. rem = NE - E0 - shift0: energy E0+el has
 // in-window columns m < rem - el; column fragments without any are skipped.
 template <int NFW>
-__device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double* wss, const double2* gs,
+__device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double2* gs,
                                          const double* gss, int rem, int f0) {
   static_assert(NFW > 0, "empty fragment range");
   using C = PiCfg;
@@ -153,17 +151,19 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
   for (int el = 0; el < C::EC; ++el) {
     const int nfe = min(NFW, ((rem - el + 7) >> 3) - f0);
     const double2* w = ws + el * kRows * C::XC;
-    const double* wsm = wss + el * kRows * C::XC;
     const double2* g = gs + el * C::XC;
     const double* gsm = gss + el * C::XC;
     if (nfe == NFW) {
 #pragma unroll
-      for (int k4 = 0; k4 < C::XC; k4 += 4) pi_kstep<NFW>(acc, w[k4], wsm[k4], g + k4, gsm + k4);
+      for (int k4 = 0; k4 < C::XC; k4 += 4) {
+        const double2 a = w[k4];
+        pi_kstep<NFW>(acc, a, a.x + a.y, g + k4, gsm + k4);
+      }
     } else if (nfe > 0) {
 #pragma unroll
       for (int k4 = 0; k4 < C::XC; k4 += 4) {
         const double2 a = w[k4];
-        const double as = wsm[k4];
+        const double as = a.x + a.y;
 #pragma unroll
         for (int f = 0; f < NFW; ++f) {
           if (f < nfe) {
@@ -232,9 +232,8 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
         const int64_t woff = ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NE + ec * C::EC) * kRows * C::XC;
         bulk_load(ws, A.W + woff, C::W_STAGE * 16, &full[slot]);
-        bulk_load(ws + C::W_STAGE, A.Wsum + woff, C::W_STAGE * 8, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE + T::WS_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE + T::WS_STAGE + T::G_STAGE, &tmGS, xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in,
+        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE + T::G_STAGE, &tmGS, xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in,
                     &full[slot]);
         if (++ec == nec) {
           ec = 0;
@@ -256,14 +255,13 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const int boff = (f0 * 8 + (lane >> 2)) * C::XC + (lane & 3);
         const double2* st0 = smem + slot * T::STAGE;
         const double2* ws = st0 + aoff;
-        const double* wss = reinterpret_cast<const double*>(st0 + C::W_STAGE) + aoff;
-        const double2* gs = st0 + C::W_STAGE + T::WS_STAGE + boff;
-        const double* gss = reinterpret_cast<const double*>(st0 + C::W_STAGE + T::WS_STAGE + T::G_STAGE) + boff;
+        const double2* gs = st0 + C::W_STAGE + boff;
+        const double* gss = reinterpret_cast<const double*>(st0 + C::W_STAGE + T::G_STAGE) + boff;
         const int rem = A.NE - ec * C::EC - A.shift0;
         if (upper) {
-          if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, wss, gs, gss, rem, f0);
+          if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, gs, gss, rem, f0);
         } else {
-          pi_stage<T::NF0>(acc, ws, wss, gs, gss, rem, f0);
+          pi_stage<T::NF0>(acc, ws, gs, gss, rem, f0);
         }
       }
       __syncwarp();

@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 // a row (e, t, x) of S = Σ_i ∇_iH_{as} V^i and adds scale·S into Σ_a with RED.F64.
 constexpr int kSandPairs = 4;   // pairs per CTA
 constexpr int kSandE = 2;       // energies per iteration
+constexpr int kSandY = 5;       // S columns per thread
 
 template <int NO>
 __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
@@ -344,30 +345,37 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
       for (int y = 0; y < NO; ++y) vo[y] = s[y];
     }
     __syncthreads();
-    for (int u = threadIdx.x; u < ns; u += blockDim.x) {
-      const int x = u % NO, r1 = u / NO, t = r1 % P, e = r1 / P;
+    // S-threads own (e, t, x, column group of kSandY): NYG = ceil(NO / kSandY) groups per row
+    constexpr int NYG = (NO + kSandY - 1) / kSandY;
+    for (int u = threadIdx.x; u < ns * NYG; u += blockDim.x) {
+      const int yg = u % NYG, r0 = u / NYG, x = r0 % NO, r1 = r0 / NO, t = r1 % P, e = r1 / P;
       if (e0 + e >= A.NE) continue;
-      double2 s[NO];
+      const int y0 = yg * kSandY;
+      double2 s[kSandY];
 #pragma unroll
-      for (int y = 0; y < NO; ++y) s[y] = make_double2(0.0, 0.0);
+      for (int y = 0; y < kSandY; ++y) s[y] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        double2 h[NO];
+        const double2* hl = Hl + (t * 3 + i) * NN + x * NO;
+        const double2* v = Vs + ((e * kSandPairs + t) * 3 + i) * NN + y0;
 #pragma unroll
-        for (int k = 0; k < NO; ++k) h[k] = Hl[(t * 3 + i) * NN + x * NO + k];
-        const double2* v = Vs + ((e * kSandPairs + t) * 3 + i) * NN;
+        for (int k = 0; k < NO; ++k) {
+          const double2 h = hl[k];
 #pragma unroll
-        for (int k = 0; k < NO; ++k)
-#pragma unroll
-          for (int y = 0; y < NO; ++y) cfma(s[y], h[k], v[k * NO + y]);
+          for (int y = 0; y < kSandY; ++y)
+            if (y0 + y < NO) cfma(s[y], h, v[k * NO + y]);
+        }
       }
       const int a_out = A.pairs[item.pair0 + t0 + t].a;
-      double* out = reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NE + e0 + e) * A.Nout + a_out) * NN + x * NO);
+      double* out =
+          reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NE + e0 + e) * A.Nout + a_out) * NN + x * NO + y0);
 #pragma unroll
-      for (int y = 0; y < NO; ++y) {
-        const double2 rr = cmul(A.scale, s[y]);
-        atomicAdd(out + 2 * y, rr.x);
-        atomicAdd(out + 2 * y + 1, rr.y);
+      for (int y = 0; y < kSandY; ++y) {
+        if (y0 + y < NO) {
+          const double2 rr = cmul(A.scale, s[y]);
+          atomicAdd(out + 2 * y, rr.x);
+          atomicAdd(out + 2 * y + 1, rr.y);
+        }
       }
     }
   }

@@ -410,7 +410,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
   // Π W scratch per item: complex tiles + Re+Im plane (24 bytes per element)
-  const size_t w_per_item = (size_t)d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20 * (sizeof(double2) + sizeof(double));
+  const size_t w_per_item = (size_t)d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
   size_t budget = d.workspace_limit;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
@@ -639,7 +639,6 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       wa.items = p->d_pi_items;
       wa.pair_item = p->d_pi_pair_item;
       wa.W = p->ws;
-      wa.Wsum = reinterpret_cast<double*>(p->ws + (size_t)(i1 - i0) * d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20);
       wa.p0 = pp0;
       wa.i0 = i0;
       wa.Nwin = p->Nwin;
@@ -653,7 +652,6 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       PiCArgs ca;
       ca.GX = GXam;
       ca.W = p->ws;
-      ca.Wsum = wa.Wsum;
       ca.GXsum = p->ws_gs + (X == 0 ? 0 : p->gs_elems());
       ca.items = p->d_pi_items;
       ca.pairs = p->d_pi_pairs;
