@@ -18,6 +18,13 @@ struct CoefArgs {
   int64_t item0, nitems, ndc, Dwin;
 };
 
+// Tiled Σ coefficient row (k_sigma_coef_tiled -> k_sigma): 16 coefficients, then (QT_SIG_CSUM) their
+// Re+Im sums in 8 complex slots, then padding to a row length ≡ 4 (mod 8) complex (conflict-free A loads).
+#ifndef QT_SIG_CSUM
+#define QT_SIG_CSUM 1
+#endif
+constexpr int kCoefKCP = QT_SIG_CSUM ? 28 : 20;
+
 struct SigmaArgs {
   const double2* G;      // G^X, paper layout [Nkz][NE][Nwin][NN]
   const double2* Gam;    // G^X, atom-major copy [Nwin][Nkz][NE][NN] (TMA path)

@@ -135,8 +135,8 @@ template <int N>
 __device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const double2* gb, const double* sb) {
 #pragma unroll
   for (int f = 0; f < N; ++f) {
-    const double2 b = gb[f * 8 * PiCfg::XC];
-    cmma3s(acc[f], a.x, a.y, as, b.x, b.y, sb[f * 8 * PiCfg::XC]);
+    const double2 b = gb[f * 16 * PiCfg::XC];
+    cmma3s(acc[f], a.x, a.y, as, b.x, b.y, sb[f * 16 * PiCfg::XC]);
   }
 }
 
@@ -149,7 +149,7 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
   using C = PiCfg;
 #pragma unroll
   for (int el = 0; el < C::EC; ++el) {
-    const int nfe = min(NFW, ((rem - el + 7) >> 3) - f0);
+    const int nfe = min(NFW, (((rem - el + 7) >> 3) - f0 + 1) >> 1);   // fragments f0 + 2f with columns < rem
     const double2* w = ws + el * kRows * C::XC;
     const double2* g = gs + el * C::XC;
     const double* gsm = gss + el * C::XC;
@@ -167,8 +167,8 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
 #pragma unroll
         for (int f = 0; f < NFW; ++f) {
           if (f < nfe) {
-            const double2 b = g[k4 + f * 8 * C::XC];
-            cmma3s(acc[f], a.x, a.y, as, b.x, b.y, gsm[k4 + f * 8 * C::XC]);
+            const double2 b = g[k4 + f * 16 * C::XC];
+            cmma3s(acc[f], a.x, a.y, as, b.x, b.y, gsm[k4 + f * 16 * C::XC]);
           }
         }
       }
@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   const int role = warp < C::NCONS ? kPiRole[warp] : 0;
   const int mi = role % 9;
   const bool upper = role >= 9;
-  const int f0 = upper ? T::NF0 : 0;
+  // column fragments are interleaved: lower warps own 0, 2, 4, .., upper warps 1, 3, 5, .. (so the
+  // out-of-window cut at large E (R7) removes work from both halves alike)
+  const int f0 = upper ? 1 : 0;
   C3Acc acc[T::NF0];
 #pragma unroll
   for (int f = 0; f < T::NF0; ++f) acc[f] = C3Acc{};
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
 #pragma unroll
         for (int f = 0; f < T::NF0; ++f) {
           if (f < nfw) {
-            const int m0 = (f0 + f) * 8 + 2 * (lane & 3);
+            const int m0 = (f0 + 2 * f) * 8 + 2 * (lane & 3);
             if (m0 < A.Nw)
               A.Pi[((int64_t)qz * A.Nw + m0) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(0));
             if (m0 + 1 < A.Nw)

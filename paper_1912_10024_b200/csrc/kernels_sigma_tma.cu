@@ -24,7 +24,7 @@ namespace qt {
 // k = 16..19 and rows t >= P are zero padding). Same values as k_sigma_coef (Eq. 3 four-term
 // combination; absorption Dc^X_{ij}, emission Dc^Y_{ji}: readings R2, R3).
 __global__ void k_sigma_coef_tiled(CoefArgs A) {
-  constexpr int KCP = 28;   // [16 coefficients | 16 Re+Im sums (8 complex slots) | 4 pad]
+  constexpr int KCP = kCoefKCP;
   const int64_t per_item = A.Nqz * A.ndc * kRows * KCP;
   const int64_t total = A.nitems * per_item;
   const int64_t pp0 = A.items[A.item0].pair0;
@@ -42,7 +42,7 @@ __global__ void k_sigma_coef_tiled(CoefArgs A) {
     const int t = row / 9, ij = row - 9 * t;
     // slot k < 16: coefficient dd = 16*dc + k; slots 16..23 hold the Re+Im sums of coefficients
     // 2(k-16) and 2(k-16)+1 (Gauss 3M A-side operand); slots 24..27 are padding
-    const bool is_sum = k >= 16 && k < 24;
+    const bool is_sum = QT_SIG_CSUM && k >= 16 && k < 24;
     double2 v = make_double2(0.0, 0.0);
     for (int h = 0; h < (is_sum ? 2 : 1); ++h) {
     const int64_t dd = 16 * dc + (is_sum ? 2 * (k - 16) + h : k);
@@ -74,7 +74,7 @@ __global__ void k_sigma_coef_tiled(CoefArgs A) {
 }
 
 cudaError_t launch_sigma_coef_tiled(const CoefArgs& a, cudaStream_t st) {
-  const int64_t total = a.nitems * a.Nqz * a.ndc * kRows * 28;
+  const int64_t total = a.nitems * a.Nqz * a.ndc * kRows * kCoefKCP;
   if (total == 0) return cudaSuccess;
   int64_t g = (total + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
@@ -88,8 +88,11 @@ struct SigTmaCfg {
   static constexpr int NFH1 = NF / 2;        // n-fragments of column half 1
   static constexpr int NPS = NFH0 * 8 + 2;   // ≡ 2 (mod 8): conflict-free B-fragment LDS.128
   static constexpr int KC = 16;              // d values per stage (4 DMMA k-steps)
-  static constexpr int KCP = 28;             // tiled coef row: 16 coef | 16 Re+Im sums | pad; ≡ 4 (mod 8)
-  static constexpr int STAGES = 4;
+  static constexpr int KCP = kCoefKCP;       // tiled coef row (see kernels_decl.cuh); ≡ 4 (mod 8)
+#ifndef QT_SIG_STAGES
+#define QT_SIG_STAGES 4
+#endif
+  static constexpr int STAGES = QT_SIG_STAGES;
   static constexpr int G_STAGE = KC * NPS;   // complex elements
   static constexpr int S_STAGE = (KC * NPS / 2 + 7) & ~7;   // Re+Im plane of the G rows (doubles), complex units
   static constexpr int C_STAGE = kRows * KCP;
@@ -121,7 +124,11 @@ __device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const
   for (int k4 = 0; k4 < KC; k4 += 4) {
     if (k4 < kc) {
       const double2 a = cs[k4];
+#if QT_SIG_CSUM
       const double as = reinterpret_cast<const double*>(cs - (threadIdx.x & 3))[32 + k4 + (threadIdx.x & 3)];
+#else
+      const double as = a.x + a.y;
+#endif
       const double2* gb = gs + k4 * NPS;
       const double* sb = ss + k4 * NPS;
 #pragma unroll

@@ -420,7 +420,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
     budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
   }
-  const size_t coef_item_t = (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * 28 * sizeof(double2);
+  const size_t coef_item_t = (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * kCoefKCP * sizeof(double2);
   const size_t need_min = std::max(coef_per_pair * kMaxPairs, coef_item_t) + w_per_item + 512;
   if (budget < need_min) budget = need_min;
   const size_t full = std::max((coef_per_pair * kMaxPairs + coef_item_t + w_per_item) * p->sig_items.size() + 512,
@@ -449,7 +449,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   {
     p->sig_tma = d.Norb <= 10;
     p->ndc = (p->Dwin + 15) / 16;
-    const size_t coef_item = (size_t)d.Nqz * p->ndc * kRows * 28 * sizeof(double2);
+    const size_t coef_item = (size_t)d.Nqz * p->ndc * kRows * kCoefKCP * sizeof(double2);
     const size_t gt_item = p->sig_tma ? w_per_item : 0;
     p->sig_chunks.clear();
     p->sig_chunks.push_back(0);
