@@ -154,6 +154,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-oracle sample time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp32 = QT_PREC_FP32_MIXED (reported separately: Σ contraction on tcgen05 tf32x3)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -185,7 +187,9 @@ def main():
         obj = [qt.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    plan = qt.Plan(p, stream=stream, unique_id=uid, **desc_kw)
+    fp32 = args.precision == "fp32"
+    plan = qt.Plan(p, stream=stream, unique_id=uid, precision=qt.QT_PREC_FP32_MIXED if fp32 else qt.QT_PREC_FP64,
+                   **desc_kw)
     info = plan.info()
     w_lo, w_hi, a_lo, a_hi = info["w_lo"], info["w_hi"], info["a_lo"], info["a_hi"]
     nwin, nout = w_hi - w_lo, a_hi - a_lo
@@ -266,17 +270,31 @@ def main():
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         prof_traffic = json.loads(tf.read_text()).get(args.config, {}).get("k_sigma")
-    roofline = {"bound": "tensor", "kernel": "k_sigma (Σ D-contraction, DMMA.8x8x4 FP64)",
-                "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": prof_traffic,
-                "flops_basis": "algorithmic: 8 real flops per complex MAC, in-window valid-pair work only",
-                "executed_dmma_tflops": round(achieved * 0.75, 3),
-                "executed_note": "Gauss 3M complex product: the tensor pipe executes 3 real 8x8x4 DMMAs (6 flops) "
-                                 "per complex MAC; executed = 0.75 x achieved",
-                "peak_source": "measured FP64 DMMA m8n8k4 sustained (profiles/r01_fp64_peak.jsonl); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
-                "launches_per_step": sig_n / args.steps, "share_of_step": round(sig_ms / ms_total, 4),
-                "kernels_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kern.items()}}
+    if not fp32:
+        roofline = {"bound": "tensor", "kernel": "k_sigma (Σ D-contraction, DMMA.8x8x4 FP64)",
+                    "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": prof_traffic,
+                    "flops_basis": "algorithmic: 8 real flops per complex MAC, in-window valid-pair work only",
+                    "executed_dmma_tflops": round(achieved * 0.75, 3),
+                    "executed_note": "Gauss 3M complex product: the tensor pipe executes 3 real 8x8x4 DMMAs (6 flops) "
+                                     "per complex MAC; executed = 0.75 x achieved",
+                    "peak_source": "measured FP64 DMMA m8n8k4 sustained (profiles/r01_fp64_peak.jsonl); "
+                                   "MEASURED_PEAKS.json has no FP64 entry"}
+    else:
+        # tcgen05 kind::tf32: 4 real products per complex MAC, each as 3 tf32 MMAs (hi·hi + hi·lo + lo·hi) =
+        # 24 tf32 flops per complex MAC = 3 x the algorithmic 8; peak = measured sustained bf16 x the guide's
+        # nominal tf32/bf16 ratio (1.1 / 2.25 PF dense).
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        tf32_peak = round(mp.get("bf16_tflops_sustained", 1385.4) * 1.1 / 2.25, 1)
+        roofline = {"bound": "tensor", "kernel": "k_sigma_tc (Σ D-contraction, tcgen05.mma kind::tf32, 3xTF32)",
+                    "achieved": round(3 * achieved, 3), "peak": tf32_peak, "unit": "TFLOP/s",
+                    "frac": round(3 * achieved / tf32_peak, 4), "traffic": None,
+                    "flops_basis": "useful tf32 flops: 3 x algorithmic (24 tf32 flops per complex MAC), padding "
+                                   "(Norb² of 128 UMMA rows, 72 of 80 columns) not counted",
+                    "algorithmic_tflops": round(achieved, 3),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (tf32/bf16 dense nominal)"}
+    roofline.update({"launches_per_step": sig_n / args.steps, "share_of_step": round(sig_ms / ms_total, 4),
+                     "kernels_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kern.items()}})
 
     # ---- e2e through the public C-ABI call on pinned HOST buffers (H2D + compute + D2H every step)
     e2e = None
@@ -323,16 +341,20 @@ def main():
                "seconds": round(dt, 2)}
 
     if rank == 0:
-        out = {"metric": METRIC, "value": round(value, 3), "unit": "Tflop/s", "n_gpus": world, "steps": args.steps,
+        out = {"metric": METRIC if not fp32 else METRIC.replace("FP64 Tflop/s", "Tflop/s (FP32 mixed mode)"),
+               "value": round(value, 3), "unit": "Tflop/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64" if not fp32 else "f32-mixed (Σ contraction tf32x3 on tcgen05, FP32 accumulate; "
+                                               "sandwiches and Π FP64)",
+               "data": "synthetic",
                "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
                                       f"NE={p.NE}, Nω={p.Nw}, Nkz=Nqz={p.Nkz}",
                           "flops_per_step": flops_step, "parallelism": f"atom-shard x{world}",
                           "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (in_bytes / 1e9)},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "halo_bytes_per_rank": info["halo_bytes"],
-               "clocks": clk, "pct_fp64_peak": round(value / (FP64_PEAK_TFLOPS * world) * 100, 2)}
+               "clocks": clk, "pct_fp64_peak": None if fp32 else round(value / (FP64_PEAK_TFLOPS * world) * 100, 2)}
         print(json.dumps(out), file=out_stream, flush=True)
     plan.close()
     if world > 1:

@@ -42,7 +42,7 @@ extern "C" {
 typedef enum {
   QT_OK = 0,
   QT_ERR_INVALID_ARG = 1,   /* bad dims, neighbour table, null/misaligned/aliased pointer */
-  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12, shift_step != 1, FP32 mode, ...                */
+  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12 (> 10 in FP32 mode), shift_step != 1, Nω > 128 */
   QT_ERR_OUT_OF_MEMORY = 3,
   QT_ERR_CUDA = 4,
   QT_ERR_NCCL = 5,
@@ -55,7 +55,12 @@ typedef enum { QT_SHARD_NONE = 0, QT_SHARD_ENERGY = 1, QT_SHARD_ATOM = 2 } qt_sh
 typedef struct {
   int64_t Na, Nb, Norb, N3D, NE, Nw, Nkz, Nqz; /* paper symbols; N3D must be 3; Nkz == Nqz          */
   int32_t shift0, shift_step;                  /* ħω_m/ΔE = shift0 + m·shift_step; shift0 ≥ 1        */
-  qt_precision precision;                      /* QT_PREC_FP64 only (FP32 mode: not yet)            */
+  qt_precision precision;                      /* QT_PREC_FP64, or QT_PREC_FP32_MIXED (Norb <= 10): */
+                                               /* the Σ D-contraction on tcgen05 (kind::tf32, each */
+                                               /* operand split hi+lo, FP32 accumulation in TMEM,  */
+                                               /* ≤1e-5 per block for conditioned blocks); the ∇H  */
+                                               /* sandwiches and Π stay FP64 (SURVEY §8(f) NEXT(1),*/
+                                               /* PAPER.md §4.4)                         */
   qt_shard shard;                              /* QT_SHARD_NONE, or QT_SHARD_ATOM with nranks > 1   */
   int32_t rank, nranks;
   const void* nccl_unique_id;                  /* host ptr to a 128-byte ncclUniqueId (nranks > 1)  */

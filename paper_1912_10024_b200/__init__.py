@@ -17,6 +17,7 @@ _LIB_PATH = _HERE / "libqtsse.so"
 
 QT_OK, QT_ERR_INVALID_ARG, QT_ERR_UNSUPPORTED, QT_ERR_OUT_OF_MEMORY, QT_ERR_CUDA, QT_ERR_NCCL, QT_ERR_INTERNAL = range(7)
 QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM = range(3)
+QT_PREC_FP64, QT_PREC_FP32_MIXED = 0, 1
 EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
             "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read", "qt_sse_nccl_unique_id",
@@ -95,10 +96,11 @@ def _check(rc: int, what: str) -> None:
         raise QTError(f"{what}: {_get_lib().qt_sse_status_string(rc).decode()} (status {rc})")
 
 
-def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0, unique_id=None) -> Desc:
+def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0, unique_id=None,
+              precision=QT_PREC_FP64) -> Desc:
     """Desc from a qtgen.Problem-like object (Na, Nb, Norb, NE, Nw, Nkz, Nqz, shift0, shift_step)."""
-    return Desc(p.Na, p.Nb, p.Norb, 3, p.NE, p.Nw, p.Nkz, p.Nqz, p.shift0, p.shift_step, 0, shard, rank, nranks,
-                unique_id, workspace_limit)
+    return Desc(p.Na, p.Nb, p.Norb, 3, p.NE, p.Nw, p.Nkz, p.Nqz, p.shift0, p.shift_step, precision, shard, rank,
+                nranks, unique_id, workspace_limit)
 
 
 def nccl_unique_id() -> bytes:
@@ -143,10 +145,12 @@ def _stream(stream):
 class Plan:
     """Owns a qt_sse_plan_t (workspace, work lists) for one problem shape."""
 
-    def __init__(self, p, stream=None, workspace_limit=0, rank=0, nranks=1, shard=QT_SHARD_NONE, unique_id=None):
+    def __init__(self, p, stream=None, workspace_limit=0, rank=0, nranks=1, shard=QT_SHARD_NONE, unique_id=None,
+                 precision=QT_PREC_FP64):
         self._uid = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
         self.desc = make_desc(p, rank=rank, nranks=nranks, shard=shard, workspace_limit=workspace_limit,
-                              unique_id=None if self._uid is None else ctypes.addressof(self._uid))
+                              unique_id=None if self._uid is None else ctypes.addressof(self._uid),
+                              precision=precision)
         self._nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
         h = ctypes.c_void_p()
         _check(_get_lib().qt_sse_plan(ctypes.byref(self.desc), self._nbr.ctypes.data, _stream(stream), ctypes.byref(h)),
@@ -201,11 +205,11 @@ class Plan:
             pass
 
 
-def run(p, t: dict, sig_scale=1j, pi_scale=-1j, plan: Plan | None = None):
+def run(p, t: dict, sig_scale=1j, pi_scale=-1j, plan: Plan | None = None, precision=QT_PREC_FP64):
     """Σ≷, Π≷ for device inputs t (dict of complex128 CUDA tensors as made by qtgen.dev_inputs)."""
     import torch
     own = plan is None
-    plan = Plan(p) if own else plan
+    plan = Plan(p, precision=precision) if own else plan
     sh = p.shapes()
     out = dict(S_less=torch.empty(sh["G"], dtype=torch.complex128, device="cuda"),
                S_gtr=torch.empty(sh["G"], dtype=torch.complex128, device="cuda"),

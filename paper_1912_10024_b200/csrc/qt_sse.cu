@@ -1,5 +1,7 @@
 // qt_sse.cu — C ABI of libqtsse.so (include/qt_sse.h): plan validation, work lists,
 // workspace, and the stream-ordered kernel sequence for Σ≷ (Eq. 3) and Π≷ (Eq. 4).
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -39,6 +41,10 @@ struct qt_sse_plan_s {
   size_t ws_bytes = 0;
   double2* ws_g = nullptr;      // atom-major copies of G^<, G^> [2][Nwin][Nkz][NE][NN]
   double* ws_gs = nullptr;      // their Re + Im planes [2][Nwin][Nkz][NE][NN rounded up to even]
+  bool fp32 = false;            // QT_PREC_FP32_MIXED: Σ contraction on tcgen05 (kind::tf32, 3xTF32 split)
+  float* ws_gtp = nullptr;      // FP32 mode: split G planes [2][Nwin][Nkz][4][NN][NEp]
+  int64_t NEp = 0, Kp = 0;      // FP32 mode: energy row length (multiple of 4), coefficient row length
+  size_t gtp_elems() const { return (size_t)Nwin * d.Nkz * 4 * kTcRowsA * NEp; }
   size_t gs_elems() const { return (size_t)d.Nkz * d.NE * Nwin * ((NN + 1) & ~int64_t(1)); }
   size_t gt_offset = 0;         // byte offset of the Σ Gt scratch inside ws
   bool sig_tma = true;          // Norb <= 10: TMA/3M k_sigma + separate sandwich
@@ -69,6 +75,12 @@ qt_status cuda_status(cudaError_t e) {
   if (e == cudaErrorMemoryAllocation) return QT_ERR_OUT_OF_MEMORY;
   return QT_ERR_CUDA;
 }
+// a failed kernel launch: the status, plus (with QT_DEBUG set in the environment) the CUDA error on stderr
+qt_status launch_fail(int kind, cudaError_t e, int line) {
+  static const bool dbg = getenv("QT_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "qt_sse: launch of kernel kind %d failed (qt_sse.cu:%d): %s\n", kind, line, cudaGetErrorString(e));
+  return cuda_status(e);
+}
 #define QT_CUDA(call)                           \
   do {                                          \
     cudaError_t e_ = (call);                    \
@@ -92,7 +104,7 @@ cudaEvent_t take_event(qt_sse_plan_s* p) {
       if (ea_ && eb_) cudaEventRecord(ea_, cs);                          \
     }                                                                    \
     cudaError_t e_ = (call);                                             \
-    if (e_ != cudaSuccess) return cuda_status(e_);                       \
+    if (e_ != cudaSuccess) return launch_fail(kind, e_, __LINE__);      \
     if (ea_ && eb_) {                                                    \
       cudaEventRecord(eb_, cs);                                          \
       p->recs.push_back({kind, ea_, eb_});                               \
@@ -108,7 +120,8 @@ qt_status validate_desc(const qt_sse_desc* d) {
   if (d->N3D != 3 || d->Nkz != d->Nqz) return QT_ERR_INVALID_ARG;
   if (d->shift0 < 1 || d->shift_step < 1) return QT_ERR_INVALID_ARG;     // S:287 grid alignment
   if (d->Na > (1LL << 30) || d->Nb > 4096) return QT_ERR_INVALID_ARG;
-  if (d->precision != QT_PREC_FP64) return QT_ERR_UNSUPPORTED;
+  if (d->precision != QT_PREC_FP64 && d->precision != QT_PREC_FP32_MIXED) return QT_ERR_UNSUPPORTED;
+  if (d->precision == QT_PREC_FP32_MIXED && d->Norb > 10) return QT_ERR_UNSUPPORTED;   // M = Norb² <= 128, FP64 sandwich
   if (d->Norb > 12 || d->shift_step != 1 || d->Nw > 128) return QT_ERR_UNSUPPORTED;
   if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return QT_ERR_INVALID_ARG;
   if (d->nranks > 1 && d->shard != QT_SHARD_ATOM) return QT_ERR_UNSUPPORTED;
@@ -279,6 +292,7 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->ws);
   cudaFree(p->ws_g);
   cudaFree(p->ws_gs);
+  cudaFree(p->ws_gtp);
   cudaFree(p->sendbuf);
   cudaFree(p->recvbuf);
   nccl_comm_destroy(p->comm);
@@ -420,7 +434,11 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
     budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
   }
-  const size_t coef_item_t = (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * kCoefKCP * sizeof(double2);
+  p->fp32 = d.precision == QT_PREC_FP32_MIXED;
+  p->NEp = std::max<int64_t>(32, (d.NE + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
+  p->Kp = (p->Dwin + 3 + 31) & ~int64_t(31);   // delayed coefficient rows (d + s, s <= 3), whole 32-chunks
+  const size_t coef_item_t = p->fp32 ? (size_t)d.Nqz * 16 * kTcRows * p->Kp * sizeof(float)
+                                     : (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * kCoefKCP * sizeof(double2);
   const size_t need_min = std::max(coef_per_pair * kMaxPairs, coef_item_t) + w_per_item + 512;
   if (budget < need_min) budget = need_min;
   const size_t full = std::max((coef_per_pair * kMaxPairs + coef_item_t + w_per_item) * p->sig_items.size() + 512,
@@ -449,7 +467,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   {
     p->sig_tma = d.Norb <= 10;
     p->ndc = (p->Dwin + 15) / 16;
-    const size_t coef_item = (size_t)d.Nqz * p->ndc * kRows * kCoefKCP * sizeof(double2);
+    const size_t coef_item = coef_item_t;
     const size_t gt_item = p->sig_tma ? w_per_item : 0;
     p->sig_chunks.clear();
     p->sig_chunks.push_back(0);
@@ -480,7 +498,8 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   }
   p->g_elems = (size_t)d.Nkz * d.NE * p->Nwin * p->NN;
   if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess ||
-      cudaMalloc(&p->ws_gs, 2 * p->gs_elems() * sizeof(double)) != cudaSuccess) {
+      cudaMalloc(&p->ws_gs, 2 * p->gs_elems() * sizeof(double)) != cudaSuccess ||
+      (p->fp32 && cudaMalloc(&p->ws_gtp, 2 * p->gtp_elems() * sizeof(float)) != cudaSuccess)) {
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
   }
@@ -545,8 +564,14 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
   const size_t sig_bytes = (size_t)d.Nkz * d.NE * p->Nout * p->NN * sizeof(double2);
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, d.NE, p->Nwin, p->NN, cs));
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  if (p->fp32) {
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GL, p->ws_gtp, d.Nkz, d.NE, p->NEp, p->Nwin, (int)p->NN, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GG, p->ws_gtp + p->gtp_elems(), d.Nkz, d.NE, p->NEp, p->Nwin,
+                                                (int)p->NN, cs));
+  } else {
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, d.NE, p->Nwin, p->NN, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  }
   for (int X = 0; X < 2; ++X) {
     void* S = X == 0 ? SL : SG;
     QT_CUDA(cudaMemsetAsync(S, 0, sig_bytes, cs));
@@ -575,7 +600,9 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       ca.nitems = i1 - i0;
       ca.ndc = p->ndc;
       ca.Dwin = p->Dwin;
-      QT_LAUNCH(QT_K_SIGMA_COEF, p->sig_tma ? launch_sigma_coef_tiled(ca, cs) : launch_sigma_coef(ca, cs));
+      QT_LAUNCH(QT_K_SIGMA_COEF, p->fp32      ? launch_sigma_coef_tc(ca, (int)p->Kp, cs)
+                                 : p->sig_tma ? launch_sigma_coef_tiled(ca, cs)
+                                              : launch_sigma_coef(ca, cs));
       SigmaArgs sa;
       sa.G = (const double2*)(X == 0 ? GL : GG);
       sa.Gam = p->ws_g + (X == 0 ? 0 : p->g_elems);
@@ -602,7 +629,12 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.Dmax = (int)p->Dmax;
       sa.ndc = (int)p->ndc;
       sa.Dwin = (int)p->Dwin;
-      QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
+      if (p->fp32) {
+        QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : p->gtp_elems()), p->NEp,
+                                              reinterpret_cast<const float*>(p->ws), (int)p->Kp, i1 - i0, cs));
+      } else {
+        QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
+      }
       QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
     }
   }

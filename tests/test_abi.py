@@ -99,13 +99,16 @@ def test_invalid_arguments_rejected_before_device_use():
             n[a, free[0]] = n[a, s]
         assert qt.lib.qt_sse_count_flops(ctypes.byref(d), np.ascontiguousarray(n).ctypes.data, out) == \
             qt.QT_ERR_INVALID_ARG, bad
-    # unsupported: Norb > 12, FP32 mode
+    # unsupported: Norb > 12; FP32 mixed mode with Norb > 10; an unknown precision
     d = qt.make_desc(p)
     d.Norb = 13
     h = ctypes.c_void_p()
     assert qt.lib.qt_sse_plan(ctypes.byref(d), nbr.ctypes.data, None, ctypes.byref(h)) == qt.QT_ERR_UNSUPPORTED
+    d = qt.make_desc(p, precision=qt.QT_PREC_FP32_MIXED)
+    d.Norb = 11
+    assert qt.lib.qt_sse_plan(ctypes.byref(d), nbr.ctypes.data, None, ctypes.byref(h)) == qt.QT_ERR_UNSUPPORTED
     d = qt.make_desc(p)
-    d.precision = 1
+    d.precision = 7
     assert qt.lib.qt_sse_plan(ctypes.byref(d), nbr.ctypes.data, None, ctypes.byref(h)) == qt.QT_ERR_UNSUPPORTED
     assert qt.lib.qt_sse_status_string(qt.QT_ERR_UNSUPPORTED) == b"unsupported configuration"
     qt.lib.qt_sse_destroy(None)   # NULL-safe

