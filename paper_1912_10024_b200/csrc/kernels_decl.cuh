@@ -80,10 +80,17 @@ cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t s
 // FP32 mixed-precision Σ contraction (tcgen05 kind::tf32; kernels_sigma_tc.cu). Coefficient planes
 // [item][q][4 planes][kTcRows][Kp] fp32; G planes [Nwin][Nkz][4][kTcRowsA][NEp] fp32.
 constexpr int kTcRows = 80;
+constexpr int kTcPiPairs = 14;   // FP32-mode Π items: <= 14 pairs of one destination atom (126 of 128 UMMA rows)
+constexpr int kTcPiRows = 128;
 constexpr int kTcRowsA = 128;   // G plane rows (Norb² padded to the UMMA M)
 cudaError_t launch_relayout_tc(const double2* G, float* out, int64_t Nkz, int64_t NE, int64_t NEp, int64_t Nwin, int NN,
                                cudaStream_t st);
 cudaError_t launch_sigma_coef_tc(const CoefArgs& a, int Kp, cudaStream_t st);
+cudaError_t launch_relayout_pi_tc(const double2* G, float* out, int64_t Nkz, int64_t NE, int64_t Epad, int64_t Nwin, int NN,
+                                  int NNp, cudaStream_t st);
+cudaError_t launch_pi_w_tc(const PiWArgs& a, float* Wp, int NNp, int64_t nitems, cudaStream_t st);
+cudaError_t launch_pi_contract_tc(const PiCArgs& a, const float* Wp, const float* Gp, int64_t Epad, int NNp, int64_t nitems,
+                                  cudaStream_t st);
 cudaError_t launch_sigma_tc(const SigmaArgs& a, const float* Gtp, int64_t NEp, const float* coef, int Kp, int64_t nitems,
                             cudaStream_t st);
 cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st);

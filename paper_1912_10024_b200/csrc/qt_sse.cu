@@ -43,6 +43,9 @@ struct qt_sse_plan_s {
   double* ws_gs = nullptr;      // their Re + Im planes [2][Nwin][Nkz][NE][NN rounded up to even]
   bool fp32 = false;            // QT_PREC_FP32_MIXED: Σ contraction on tcgen05 (kind::tf32, 3xTF32 split)
   float* ws_gtp = nullptr;      // FP32 mode: split G planes [2][Nwin][Nkz][4][NN][NEp]
+  float* ws_gpi = nullptr;      // FP32 mode: split G^X planes for Π [Nwin][Nkz][4][Epad][NNp] (one X at a time)
+  int64_t Epad = 0, NNp = 0;
+  size_t gpi_elems() const { return (size_t)Nwin * d.Nkz * 4 * Epad * NNp; }
   int64_t NEp = 0, Kp = 0;      // FP32 mode: energy row length (multiple of 4), coefficient row length
   size_t gtp_elems() const { return (size_t)Nwin * d.Nkz * 4 * kTcRowsA * NEp; }
   size_t gs_elems() const { return (size_t)d.Nkz * d.NE * Nwin * ((NN + 1) & ~int64_t(1)); }
@@ -121,7 +124,8 @@ qt_status validate_desc(const qt_sse_desc* d) {
   if (d->shift0 < 1 || d->shift_step < 1) return QT_ERR_INVALID_ARG;     // S:287 grid alignment
   if (d->Na > (1LL << 30) || d->Nb > 4096) return QT_ERR_INVALID_ARG;
   if (d->precision != QT_PREC_FP64 && d->precision != QT_PREC_FP32_MIXED) return QT_ERR_UNSUPPORTED;
-  if (d->precision == QT_PREC_FP32_MIXED && d->Norb > 10) return QT_ERR_UNSUPPORTED;   // M = Norb² <= 128, FP64 sandwich
+  if (d->precision == QT_PREC_FP32_MIXED && (d->Norb > 10 || d->Nw > 80))   // UMMA M = Norb² <= 128, N = Nω <= 80
+    return QT_ERR_UNSUPPORTED;
   if (d->Norb > 12 || d->shift_step != 1 || d->Nw > 128) return QT_ERR_UNSUPPORTED;
   if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return QT_ERR_INVALID_ARG;
   if (d->nranks > 1 && d->shard != QT_SHARD_ATOM) return QT_ERR_UNSUPPORTED;
@@ -293,6 +297,7 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->ws_g);
   cudaFree(p->ws_gs);
   cudaFree(p->ws_gtp);
+  cudaFree(p->ws_gpi);
   cudaFree(p->sendbuf);
   cudaFree(p->recvbuf);
   nccl_comm_destroy(p->comm);
@@ -405,11 +410,12 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
       q.a_in = (int32_t)(a - p->w_lo);
       mine.push_back(q);
     }
-    for (size_t k = 0; k < mine.size(); k += kMaxPairs) {
+    const size_t cap = d.precision == QT_PREC_FP32_MIXED ? kTcPiPairs : kMaxPairs;   // 126 / 72 GEMM rows
+    for (size_t k = 0; k < mine.size(); k += cap) {
       PiItem it;
       it.a_out = (int32_t)(a - p->a_lo);
       it.a_in = (int32_t)(a - p->w_lo);
-      it.npair = (int32_t)std::min<size_t>(kMaxPairs, mine.size() - k);
+      it.npair = (int32_t)std::min<size_t>(cap, mine.size() - k);
       it.pair0 = (int32_t)pp.size();
       for (int t = 0; t < it.npair; ++t) {
         pp.push_back(mine[k + t]);
@@ -424,7 +430,12 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
   // Π W scratch per item: complex tiles + Re+Im plane (24 bytes per element)
-  const size_t w_per_item = (size_t)d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
+  const size_t gt_per_item = (size_t)d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
+  p->NNp = (p->NN + 3) & ~int64_t(3);
+  p->Epad = d.NE + d.shift0 + 80 + 1;
+  const size_t w_per_item = d.precision == QT_PREC_FP32_MIXED
+                                ? (size_t)4 * kTcPiRows * d.Nkz * d.NE * p->NNp * sizeof(float)
+                                : gt_per_item;
   size_t budget = d.workspace_limit;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
@@ -468,7 +479,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     p->sig_tma = d.Norb <= 10;
     p->ndc = (p->Dwin + 15) / 16;
     const size_t coef_item = coef_item_t;
-    const size_t gt_item = p->sig_tma ? w_per_item : 0;
+    const size_t gt_item = p->sig_tma ? gt_per_item : 0;
     p->sig_chunks.clear();
     p->sig_chunks.push_back(0);
     size_t coef_acc = 0, gt_acc = 0, coef_max = 0;
@@ -499,7 +510,8 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   p->g_elems = (size_t)d.Nkz * d.NE * p->Nwin * p->NN;
   if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess ||
       cudaMalloc(&p->ws_gs, 2 * p->gs_elems() * sizeof(double)) != cudaSuccess ||
-      (p->fp32 && cudaMalloc(&p->ws_gtp, 2 * p->gtp_elems() * sizeof(float)) != cudaSuccess)) {
+      (p->fp32 && cudaMalloc(&p->ws_gtp, 2 * p->gtp_elems() * sizeof(float)) != cudaSuccess) ||
+      (p->fp32 && cudaMalloc(&p->ws_gpi, p->gpi_elems() * sizeof(float)) != cudaSuccess)) {
     qt_sse_destroy(p);
     return QT_ERR_OUT_OF_MEMORY;
   }
@@ -658,6 +670,9 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
     const double2* GXam = p->ws_g + (X == 0 ? 0 : p->g_elems);
     const double2* GY = (const double2*)(X == 0 ? GG : GL);
     double2* P = (double2*)(X == 0 ? PL : PG);
+    if (p->fp32)
+      QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_pi_tc((const double2*)(X == 0 ? GL : GG), p->ws_gpi, d.Nkz, d.NE, p->Epad,
+                                                     p->Nwin, (int)p->NN, (int)p->NNp, cs));
     for (size_t c = 0; c + 1 < p->pi_chunks.size(); ++c) {
       const int64_t i0 = p->pi_chunks[c], i1 = p->pi_chunks[c + 1];
       if (i1 <= i0) continue;
@@ -680,7 +695,11 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       wa.Norb = (int)d.Norb;
       wa.NN = (int)p->NN;
       wa.nEB = (int)((d.NE + kEB - 1) / kEB);
-      QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, i1 - i0, cs));
+      if (p->fp32) {
+        QT_LAUNCH(QT_K_PI_W, launch_pi_w_tc(wa, reinterpret_cast<float*>(p->ws), (int)p->NNp, i1 - i0, cs));
+      } else {
+        QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, i1 - i0, cs));
+      }
       PiCArgs ca;
       ca.GX = GXam;
       ca.W = p->ws;
@@ -702,7 +721,12 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       ca.Nw = (int)d.Nw;
       ca.NWP = (int)p->NWP;
       ca.shift0 = d.shift0;
-      QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
+      if (p->fp32) {
+        QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract_tc(ca, reinterpret_cast<const float*>(p->ws), p->ws_gpi, p->Epad,
+                                                          (int)p->NNp, i1 - i0, cs));
+      } else {
+        QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
+      }
     }
     PiSelfArgs sa;
     sa.Pi = P;
