@@ -120,7 +120,7 @@ def test_fp32_small_config_sampled():
 
 @pytest.mark.slow
 def test_fp32_cfg3_sampled():
-    """The bench workload (cfg3) in FP32 mode: sampled Σ blocks vs the oracle at 1e-5."""
+    """The bench workload (cfg3) in FP32 mode: sampled Σ and Π blocks vs the oracle at 1e-5."""
     p = qtgen.problem("cfg3")
     inp = qtgen.host_inputs(p, qtgen.RANDOM)
     t = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
@@ -134,4 +134,14 @@ def test_fp32_cfg3_sampled():
     ref = oracle.sigma_blocks(p, inp, sb, 1j)
     S = (out["S_less"], out["S_gtr"])
     got = np.stack([S[x][k, e, a].cpu().numpy() for x, k, e, a in sb])
-    assert rel_fro(got, ref, AX) <= TOL_FP32
+    err_s = rel_fro(got, ref, AX)
+    a_s = rng.integers(0, p.Na, n)
+    pb = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nqz, n),
+                   np.concatenate([[0, p.Nw - 1], rng.integers(0, p.Nw, n - 2)]), a_s,
+                   [rng.choice(np.concatenate([[0], 1 + np.nonzero(p.nbr[x] >= 0)[0]])) for x in a_s]], 1)
+    ref_p = oracle.pi_blocks(p, inp, pb, -1j)
+    P = (out["P_less"], out["P_gtr"])
+    got_p = np.stack([P[x][q, m, a, s].cpu().numpy() for x, q, m, a, s in pb])
+    err_p = rel_fro(got_p, ref_p, AX)
+    print(f"cfg3 FP32 mode: max per-block rel. Frobenius error Σ {err_s:.2e}, Π {err_p:.2e}")
+    assert err_s <= TOL_FP32 and err_p <= TOL_FP32, (err_s, err_p)
