@@ -38,6 +38,7 @@ struct SigmaArgs {
   double2 scale;
   int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk, ntiles;
   int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin, ndc;
+  int rows;              // Gt rows per (item, kz, E) block: 72 (items of <= 8 pairs) or 128 (FP32 mode, <= 14)
 };
 
 struct PiWArgs {
@@ -79,7 +80,7 @@ cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st)
 cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 // FP32 mixed-precision Σ contraction (tcgen05 kind::tf32; kernels_sigma_tc.cu). Coefficient planes
 // [item][q][4 planes][kTcRows][Kp] fp32; G planes [Nwin][Nkz][4][kTcRowsA][NEp] fp32.
-constexpr int kTcRows = 80;
+constexpr int kTcRows = 128;    // FP32-mode Σ items: <= 14 pairs (126 coefficient rows) = UMMA N
 constexpr int kTcPiPairs = 14;   // FP32-mode Π items: <= 14 pairs of one destination atom (126 of 128 UMMA rows)
 constexpr int kTcPiRows = 128;
 constexpr int kTcRowsA = 128;   // G plane rows (Norb² padded to the UMMA M)

@@ -29,14 +29,14 @@
 namespace qt {
 
 constexpr int kTcM = kTcRowsA;                   // UMMA M: Norb² entries of a G block (Norb <= 11)
-constexpr int kTcN = kTcRows;                    // UMMA N: the item's 72 coefficient rows, padded to 16
-constexpr int kTcKC = 32;                        // shifts per stage: one 128-byte swizzle row of fp32
-constexpr int kTcStages = 2;
-constexpr int kTcAPlane = kTcM * kTcKC;          // floats per A plane tile (16 KB)
-constexpr int kTcBPlane = kTcN * kTcKC;          // floats per B plane tile (10 KB)
+constexpr int kTcN = kTcRows;                    // UMMA N: the item's <= 126 coefficient rows (14 pairs)
+constexpr int kTcKC = 16;                        // shifts per stage: one 64-byte swizzle row of fp32
+constexpr int kTcStages = 3;
+constexpr int kTcAPlane = kTcM * kTcKC;          // floats per A plane tile (8 KB)
+constexpr int kTcBPlane = kTcN * kTcKC;          // floats per B plane tile (8 KB)
 constexpr int kTcStage = 4 * (kTcAPlane + kTcBPlane);
 constexpr uint32_t kTcStageBytes = kTcStage * 4;
-constexpr int kTcBufCols = 256;                  // TMEM columns per accumulator buffer (Re: 0..79, Im: 80..159)
+constexpr int kTcBufCols = 256;                  // TMEM columns per accumulator buffer (Re: 0..127, Im: 128..255)
 constexpr size_t kTcSmem = (size_t)kTcStages * kTcStageBytes + 1024 + 256;
 static_assert(kTcSmem <= 227 * 1024, "shared memory");
 
@@ -265,14 +265,14 @@ __global__ void __launch_bounds__(192, 1)
             const int kc = (T.c0 + c) * kTcKC;
             const int k_lo = max(0, T.dlo + T.sh - kc) / 8, k_hi = min(kTcKC, T.dhi + T.sh - kc + 7) / 8;
             for (int kk = k_lo; kk < k_hi; ++kk) {
-              const uint64_t arh = umma_desc_k128(sa + 0 * kTcAPlane + kk * 8);
-              const uint64_t arl = umma_desc_k128(sa + 1 * kTcAPlane + kk * 8);
-              const uint64_t aih = umma_desc_k128(sa + 2 * kTcAPlane + kk * 8);
-              const uint64_t ail = umma_desc_k128(sa + 3 * kTcAPlane + kk * 8);
-              const uint64_t brh = umma_desc_k128(sb + 0 * kTcBPlane + kk * 8);
-              const uint64_t brl = umma_desc_k128(sb + 1 * kTcBPlane + kk * 8);
-              const uint64_t bih = umma_desc_k128(sb + 2 * kTcBPlane + kk * 8);
-              const uint64_t bil = umma_desc_k128(sb + 3 * kTcBPlane + kk * 8);
+              const uint64_t arh = umma_desc_k64(sa + 0 * kTcAPlane + kk * 8);
+              const uint64_t arl = umma_desc_k64(sa + 1 * kTcAPlane + kk * 8);
+              const uint64_t aih = umma_desc_k64(sa + 2 * kTcAPlane + kk * 8);
+              const uint64_t ail = umma_desc_k64(sa + 3 * kTcAPlane + kk * 8);
+              const uint64_t brh = umma_desc_k64(sb + 0 * kTcBPlane + kk * 8);
+              const uint64_t brl = umma_desc_k64(sb + 1 * kTcBPlane + kk * 8);
+              const uint64_t bih = umma_desc_k64(sb + 2 * kTcBPlane + kk * 8);
+              const uint64_t bil = umma_desc_k64(sb + 3 * kTcBPlane + kk * 8);
               // Re += Ar·Br − Ai·Bi
               umma_tf32(dre, arh, brh, id_pos, acc);
               umma_tf32(dre, arh, brl, id_pos, true);
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const uint32_t taddr = tm + ((uint32_t)(quarter * 32) << 16) + buf * kTcBufCols;
       const int rows = 9 * T.item.npair;
-      double2* out = A.Gt + (((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * kRows * A.NN + rc;
+      double2* out = A.Gt + (((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * A.rows * A.NN + rc;
       for (int n0 = 0; n0 < rows; n0 += 16) {
         float re[16], im[16];
         tmem_ld16(taddr + n0, re);
@@ -341,8 +341,10 @@ cudaError_t make_tmap_f32_sw128(CUtensorMap* m, const void* base, int rank, cons
     return cudaErrorNotSupported;
   auto fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   const uint32_t estr[5] = {1, 1, 1, 1, 1};
+  // swizzle span = the box's inner row (16 fp32 = 64 B for Σ, 32 fp32 = 128 B for Π)
+  const CUtensorMapSwizzle sw = box[0] * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS && getenv("QT_DEBUG"))
     fprintf(stderr, "qt_sse: cuTensorMapEncodeTiled (fp32, rank %d, dims %llu x %llu, box %u x %u) failed: %d\n", rank,

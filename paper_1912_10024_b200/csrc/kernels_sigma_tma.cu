@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       if (++c == T.nchunk) c = 0;
     }
     if (active && row < 9 * T.item.npair) {
-      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E + e) * kRows + row) * A.NN;
+      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E + e) * A.rows + row) * A.NN;
 #pragma unroll
       for (int f = 0; f < C::TMAXW; ++f) {
         if (f < nfw) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 
 // ---------------------------------------------------------------- Σ sandwich + neighbour sum
 // Σ_a(kz,E) += scale · Σ_i ∇_iH_{a s} (Σ_j Gt^{ij} ∇_jH_{b r}) for every pair of the chunk's items (R8).
-// One CTA per (item, kz, half of the item's pairs), looping over energy pairs. ∇H blocks stay in
+// One CTA per (item, kz, group of 4 of the item's pairs), looping over energy pairs. ∇H blocks stay in
 // shared memory. Compile-time Norb: a V-thread owns a row (e, t, i, x) of V^i = Σ_j Gt^{ij}∇_jH_{br}
 // (Gt row loaded into registers, ∇H broadcast from shared memory, Norb accumulators); an S-thread owns
 // a row (e, t, x) of S = Σ_i ∇_iH_{as} V^i and adds scale·S into Σ_a with RED.F64.
@@ -310,8 +310,9 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
   double2* Hr = sand_sm;                         // [kSandPairs][3][NN]
   double2* Hl = Hr + kSandPairs * 3 * NN;        // [kSandPairs][3][NN]
   double2* Vs = Hl + kSandPairs * 3 * NN;        // [kSandE][kSandPairs][3][NN]
-  const int half = blockIdx.x & 1;
-  const int64_t r = blockIdx.x >> 1;
+  const int ngrp = (A.rows / 9 + kSandPairs - 1) / kSandPairs;   // pair groups per item (2 or 4)
+  const int half = blockIdx.x % ngrp;
+  const int64_t r = blockIdx.x / ngrp;
   const int kz = (int)(r % A.Nkz);
   const int il = (int)(r / A.Nkz);
   const SigItem item = A.items[il];
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
     Hr[idx] = A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem];
     Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
   }
-  const double2* gbase = A.Gt + ((int64_t)il * A.Nkz + kz) * A.NE * kRows * NN;
+  const double2* gbase = A.Gt + ((int64_t)il * A.Nkz + kz) * A.NE * A.rows * NN;
   const int nv = kSandE * P * 3 * NO;   // V rows (e, t, i, x)
   const int ns = kSandE * P * NO;       // S rows (e, t, x)
   for (int e0 = 0; e0 < A.NE; e0 += kSandE) {
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
       double2 s[NO];
 #pragma unroll
       for (int y = 0; y < NO; ++y) s[y] = make_double2(0.0, 0.0);
-      const double2* g = gbase + ((int64_t)(e0 + e) * kRows + (t0 + t) * 9 + i * 3) * NN + x * NO;
+      const double2* g = gbase + ((int64_t)(e0 + e) * A.rows + (t0 + t) * 9 + i * 3) * NN + x * NO;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         double2 gv[NO];
@@ -461,7 +462,8 @@ static cudaError_t launch_sand_no(const SigmaArgs& a, int64_t nitems, cudaStream
   const int smem = (2 + kSandE) * kSandPairs * 3 * NO * NO * 16;
   cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sigma_sand<NO><<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);
+  const int ngrp = (a.rows / 9 + kSandPairs - 1) / kSandPairs;
+  k_sigma_sand<NO><<<(unsigned)(nitems * a.Nkz * ngrp), 256, smem, st>>>(a);
   return cudaGetLastError();
 }
 

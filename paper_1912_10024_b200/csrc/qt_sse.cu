@@ -45,6 +45,7 @@ struct qt_sse_plan_s {
   float* ws_gtp = nullptr;      // FP32 mode: split G planes [2][Nwin][Nkz][4][NN][NEp]
   float* ws_gpi = nullptr;      // FP32 mode: split G^X planes for Π [Nwin][Nkz][4][Epad][NNp] (one X at a time)
   int64_t Epad = 0, NNp = 0;
+  int64_t sig_rows = kRows;     // Gt rows per (item, kz, E): 72, or 128 in FP32 mode (items of <= 14 pairs)
   size_t gpi_elems() const { return (size_t)Nwin * d.Nkz * 4 * Epad * NNp; }
   int64_t NEp = 0, Kp = 0;      // FP32 mode: energy row length (multiple of 4), coefficient row length
   size_t gtp_elems() const { return (size_t)Nwin * d.Nkz * 4 * kTcRowsA * NEp; }
@@ -381,11 +382,12 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
       q.r = (int32_t)r;
       mine.push_back(q);
     }
-    for (size_t k = 0; k < mine.size(); k += kMaxPairs) {
+    const size_t scap = d.precision == QT_PREC_FP32_MIXED ? kTcPiPairs : kMaxPairs;   // 126 / 72 GEMM rows
+    for (size_t k = 0; k < mine.size(); k += scap) {
       SigItem it;
       it.b_in = (int32_t)(b - p->w_lo);
       it.b = (int32_t)b;
-      it.npair = (int32_t)std::min<size_t>(kMaxPairs, mine.size() - k);
+      it.npair = (int32_t)std::min<size_t>(scap, mine.size() - k);
       it.pair0 = (int32_t)sp.size();
       for (int t = 0; t < it.npair; ++t) {
         sp.push_back(mine[k + t]);
@@ -430,7 +432,8 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
   // Π W scratch per item: complex tiles + Re+Im plane (24 bytes per element)
-  const size_t gt_per_item = (size_t)d.Nkz * d.NE * kRows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
+  p->sig_rows = d.precision == QT_PREC_FP32_MIXED ? kTcRows : kRows;   // Gt rows per (item, kz, E)
+  const size_t gt_per_item = (size_t)d.Nkz * d.NE * p->sig_rows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
   p->NNp = (p->NN + 3) & ~int64_t(3);
   p->Epad = d.NE + d.shift0 + 80 + 1;
   const size_t w_per_item = d.precision == QT_PREC_FP32_MIXED
@@ -641,6 +644,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.Dmax = (int)p->Dmax;
       sa.ndc = (int)p->ndc;
       sa.Dwin = (int)p->Dwin;
+      sa.rows = (int)p->sig_rows;
       if (p->fp32) {
         QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : p->gtp_elems()), p->NEp,
                                               reinterpret_cast<const float*>(p->ws), (int)p->Kp, i1 - i0, cs));

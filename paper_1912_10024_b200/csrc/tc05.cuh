@@ -38,6 +38,19 @@ __device__ __forceinline__ uint64_t umma_desc_k128(const void* smem_tile) {
   return d;
 }
 
+// same for a tile [rows][16 x 4-byte] written with CU_TENSOR_MAP_SWIZZLE_64B (8-row x 64-byte atoms, SBO 512 B,
+// base 512-byte aligned); K advances by 8 tf32 = +32 bytes within the 64-byte row
+__device__ __forceinline__ uint64_t umma_desc_k64(const void* smem_tile) {
+  const uint32_t a = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;                      // layout: SWIZZLE_64B
+  return d;
+}
+
 // ---- instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, M x N, optional negation
 __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N, bool neg_a = false, bool neg_b = false) {
   return (1u << 4)                          // c_format = F32

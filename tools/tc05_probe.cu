@@ -8,6 +8,24 @@
 #include <cmath>
 #include <vector>
 #include "../paper_1912_10024_b200/csrc/tc05.cuh"
+#ifdef SW64
+constexpr int KC = 16;
+__device__ __forceinline__ uint64_t desc_sw(const void* p) {
+  const uint32_t a = qt::smem_u32(p);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+#define SWZ CU_TENSOR_MAP_SWIZZLE_64B
+#else
+constexpr int KC = 32;
+#define desc_sw umma_desc_k128
+#define SWZ CU_TENSOR_MAP_SWIZZLE_128B
+#endif
 using namespace qt;
 #ifndef PN
 #define PN 64
@@ -25,8 +43,8 @@ constexpr int M = 128, N = PN, K = 64;   // K = 2 swizzle chunks of 32
 __global__ void probe(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, float* C, int neg) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
-  float* sA = (float*)base;                    // [K/32][128][32]
-  float* sB = (float*)(base + (K / 32) * M * 128);   // [K/32][N][32]
+  float* sA = (float*)base;
+  float* sB = (float*)(base + (K / KC) * M * KC * 4);
   __shared__ uint64_t bar_load, bar_mma;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -36,17 +54,17 @@ __global__ void probe(const __grid_constant__ CUtensorMap tA, const __grid_const
   const uint32_t tm = tbase;
   if (threadIdx.x == 32) {
     mbar_arrive_expect_tx(&bar_load, (M + N) * K * 4);
-    for (int c = 0; c < K / 32; ++c) {
-      TLOAD(sA + c * M * 32, &tA, c * 32);
-      TLOAD(sB + c * N * 32, &tB, c * 32);
+    for (int c = 0; c < K / KC; ++c) {
+      TLOAD(sA + c * M * KC, &tA, c * KC);
+      TLOAD(sB + c * N * KC, &tB, c * KC);
     }
     mbar_wait(&bar_load, 0);
     tc_fence_after();
     const uint32_t idesc = umma_idesc_tf32(M, N, neg != 0, false);
     for (int k = 0; k < K / 8; ++k) {
-      const int c = k / 4, kk = k % 4;
-      const uint64_t ad = umma_desc_k128((uint8_t*)(sA + c * M * 32) + kk * 32);
-      const uint64_t bd = umma_desc_k128((uint8_t*)(sB + c * N * 32) + kk * 32);
+      const int c = k / (KC / 8), kk = k % (KC / 8);
+      const uint64_t ad = desc_sw((uint8_t*)(sA + c * M * KC) + kk * 32);
+      const uint64_t bd = desc_sw((uint8_t*)(sB + c * N * KC) + kk * 32);
       umma_tf32(tm, ad, bd, idesc, k > 0);
     }
     umma_commit(&bar_mma);
@@ -85,10 +103,10 @@ int main() {
 #else
   const int RANK = 4;
 #endif
-  { cuuint64_t dims[5] = {K, M, 1, 1, 1}; cuuint64_t str[4] = {K * 4, M * K * 4, M * K * 4, M * K * 4}; cuuint32_t box[5] = {32, M, 1, 1, 1};
-    CUresult r = enc(&tA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RANK, dA, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); printf("encA %d\n", r); }
-  { cuuint64_t dims[5] = {K, N, 1, 1, 1}; cuuint64_t str[4] = {K * 4, N * K * 4, N * K * 4, N * K * 4}; cuuint32_t box[5] = {32, N, 1, 1, 1};
-    CUresult r = enc(&tB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RANK, dB, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); printf("encB %d\n", r); }
+  { cuuint64_t dims[5] = {K, M, 1, 1, 1}; cuuint64_t str[4] = {K * 4, M * K * 4, M * K * 4, M * K * 4}; cuuint32_t box[5] = {KC, M, 1, 1, 1};
+    CUresult r = enc(&tA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RANK, dA, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, SWZ, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); printf("encA %d\n", r); }
+  { cuuint64_t dims[5] = {K, N, 1, 1, 1}; cuuint64_t str[4] = {K * 4, N * K * 4, N * K * 4, N * K * 4}; cuuint32_t box[5] = {KC, N, 1, 1, 1};
+    CUresult r = enc(&tB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RANK, dB, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, SWZ, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); printf("encB %d\n", r); }
   const int smem = 1024 + (M + N) * K * 4;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int neg = 0; neg < 2; ++neg) {
