@@ -69,6 +69,27 @@ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
+__device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+// complex type of a real type (double2 / float2), conversions from / to double2
+template <class R> struct Cx;
+template <> struct Cx<double> {
+  using T = double2;
+  __device__ static T zero() { return make_double2(0.0, 0.0); }
+  __device__ static T from(double2 v) { return v; }
+  __device__ static double2 wide(T v) { return v; }
+};
+template <> struct Cx<float> {
+  using T = float2;
+  __device__ static T zero() { return make_float2(0.f, 0.f); }
+  __device__ static T from(double2 v) { return make_float2((float)v.x, (float)v.y); }
+  __device__ static double2 wide(T v) { return make_double2((double)v.x, (double)v.y); }
+};
+
 __host__ __device__ inline int64_t imod(int64_t x, int64_t n) {
   int64_t r = x % n;
   return r < 0 ? r + n : r;

@@ -39,6 +39,7 @@ struct SigmaArgs {
   int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk, ntiles;
   int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin, ndc;
   int rows;              // Gt rows per (item, kz, E) block: 72 (items of <= 8 pairs) or 128 (FP32 mode, <= 14)
+  int gt_f32;            // Gt scratch holds float2 (FP32 mixed mode: k_sigma_tc -> FP32 sandwich)
 };
 
 struct PiWArgs {

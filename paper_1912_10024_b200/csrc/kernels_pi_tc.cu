@@ -25,16 +25,20 @@
 
 namespace qt {
 
+#define UMMA_DESC(p) (kPKC == 16 ? umma_desc_k64(p) : umma_desc_k128(p))
 constexpr int kPM = 128;                 // UMMA M: rows (t, ij), 9·14 = 126 used
 constexpr int kPN = 80;                  // UMMA N: frequencies m (Nω <= 80 in this mode)
-constexpr int kPKC = 32;                 // K per stage (one 128-byte swizzle row of fp32)
-constexpr int kPStages = 2;
+#ifndef QT_PI_KC
+#define QT_PI_KC 32
+#endif
+constexpr int kPKC = QT_PI_KC;           // K per stage: one 64-byte (16) or 128-byte (32) swizzle row of fp32
+constexpr int kPStages = kPKC == 16 ? 4 : 2;
 constexpr int kPAPlane = kPM * kPKC;
 constexpr int kPBPlane = kPN * kPKC;
 constexpr int kPStage = 4 * (kPAPlane + kPBPlane);
 constexpr uint32_t kPStageBytes = kPStage * 4;
 constexpr int kPBufCols = 256;
-constexpr int kSegChunks = 4;            // chunks per FP32 accumulation segment (128 products per accumulator)
+constexpr int kSegChunks = 128 / kPKC;   // chunks per FP32 accumulation segment (128 products per accumulator)
 constexpr int kPEpiWarps = 20;           // epilogue warps: 4 TMEM lane quarters x 5 groups of 16 frequencies
 constexpr int kPCols = 16;               // frequencies per epilogue thread (FP64 accumulators)
 constexpr int kPThreads = (2 + kPEpiWarps) * 32;
@@ -81,7 +85,8 @@ cudaError_t launch_relayout_pi_tc(const double2* G, float* out, int64_t Nkz, int
   return cudaGetLastError();
 }
 
-// W_p^{ij}(kz,E)[x][y] = (∇_jH_{as} G^Y_b(kz,E) ∇_iH_{br})[y][x] (FP64, as k_pi_w) written as split planes
+// W_p^{ij}(kz,E)[x][y] = (∇_jH_{as} G^Y_b(kz,E) ∇_iH_{br})[y][x] (FP32 arithmetic on FP32-rounded inputs; the
+// same order as k_pi_w) written as split planes
 // Wp[il][plane][row = t·9+ij][k = (kz·NE + E)·NNp + x·Norb + y]; xy padding columns are zero. One CTA per
 // (item, kz, group of 4 pairs), looping over energy pairs.
 constexpr int kTWPairs = 4;
@@ -90,11 +95,11 @@ constexpr int kTWE = 2;
 template <int NO>
 __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict__ Wp, int NNp) {
   constexpr int NN = NO * NO;
-  extern __shared__ __align__(16) double2 w_sm[];
-  double2* Hl = w_sm;                          // [kTWPairs][3][NN]  ∇_jH_{as}
-  double2* Hr = Hl + kTWPairs * 3 * NN;        // [kTWPairs][3][NN]  ∇_iH_{br}
-  double2* Gb = Hr + kTWPairs * 3 * NN;        // [kTWPairs][kTWE][NN]
-  double2* T = Gb + kTWPairs * kTWE * NN;      // [kTWPairs][kTWE][3][NN]
+  extern __shared__ __align__(16) float2 w_sm[];
+  float2* Hl = w_sm;                           // [kTWPairs][3][NN]  ∇_jH_{as}
+  float2* Hr = Hl + kTWPairs * 3 * NN;         // [kTWPairs][3][NN]  ∇_iH_{br}
+  float2* Gb = Hr + kTWPairs * 3 * NN;         // [kTWPairs][kTWE][NN]
+  float2* T = Gb + kTWPairs * kTWE * NN;       // [kTWPairs][kTWE][3][NN]
   constexpr int NG = (kTcPiPairs + kTWPairs - 1) / kTWPairs;
   const int grp = blockIdx.x % NG;
   const int64_t r = blockIdx.x / NG;
@@ -107,8 +112,8 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
   for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
     const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
     const PiPair pr = A.pairs[it.pair0 + t0 + t];
-    Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
-    Hr[idx] = A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + rem];
+    Hl[idx] = Cx<float>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem]);
+    Hr[idx] = Cx<float>::from(A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + rem]);
   }
   const int64_t K = (int64_t)A.Nkz * A.NE * NNp;                    // row length
   const int64_t plane = (int64_t)kTcPiRows * K;
@@ -119,23 +124,23 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      Gb[t * kTWE * NN + rem] = A.GYam[(((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem];
+      Gb[t * kTWE * NN + rem] = Cx<float>::from(A.GYam[(((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem]);
     }
     __syncthreads();
     for (int u = threadIdx.x; u < P * ne * 3 * NO; u += blockDim.x) {   // T_i = G_b ∇_iH_{br}
       const int q = u % NO, r1 = u / NO, i = r1 % 3, r2 = r1 / 3, e = r2 % ne, t = r2 / ne;
-      double2 g[NO], s[NO];
+      float2 g[NO], s[NO];
 #pragma unroll
       for (int k = 0; k < NO; ++k) {
         g[k] = Gb[(t * kTWE + e) * NN + q * NO + k];
-        s[k] = make_double2(0.0, 0.0);
+        s[k] = make_float2(0.f, 0.f);
       }
-      const double2* h = Hr + (t * 3 + i) * NN;
+      const float2* h = Hr + (t * 3 + i) * NN;
 #pragma unroll
       for (int k = 0; k < NO; ++k)
 #pragma unroll
         for (int x = 0; x < NO; ++x) cfma(s[x], g[k], h[k * NO + x]);
-      double2* o = T + ((t * kTWE + e) * 3 + i) * NN + q * NO;
+      float2* o = T + ((t * kTWE + e) * 3 + i) * NN + q * NO;
 #pragma unroll
       for (int x = 0; x < NO; ++x) o[x] = s[x];
     }
@@ -143,13 +148,13 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
     for (int u = threadIdx.x; u < P * ne * 9 * NO; u += blockDim.x) {   // W^{ij}[x][y] = Σ_q ∇_jH[y][q] T_i[q][x]
       const int y = u % NO, r1 = u / NO, ij = r1 % 9, r2 = r1 / 9, e = r2 % ne, t = r2 / ne;
       const int i = ij / 3, j = ij - 3 * i;
-      double2 hrow[NO], s[NO];
+      float2 hrow[NO], s[NO];
 #pragma unroll
       for (int k = 0; k < NO; ++k) {
         hrow[k] = Hl[(t * 3 + j) * NN + y * NO + k];
-        s[k] = make_double2(0.0, 0.0);
+        s[k] = make_float2(0.f, 0.f);
       }
-      const double2* tt = T + ((t * kTWE + e) * 3 + i) * NN;
+      const float2* tt = T + ((t * kTWE + e) * 3 + i) * NN;
 #pragma unroll
       for (int q = 0; q < NO; ++q)
 #pragma unroll
@@ -157,13 +162,11 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
       float* o = Wi + (int64_t)((t0 + t) * 9 + ij) * K + ((int64_t)kz * A.NE + e0 + e) * NNp + y;
 #pragma unroll
       for (int x = 0; x < NO; ++x) {
-        float h, l;
-        split3_p(s[x].x, h, l);
-        o[x * NO] = h;
-        o[plane + x * NO] = l;
-        split3_p(s[x].y, h, l);
-        o[2 * plane + x * NO] = h;
-        o[3 * plane + x * NO] = l;
+        const float hr = tf32_rna_p(s[x].x), hi_ = tf32_rna_p(s[x].y);
+        o[x * NO] = hr;
+        o[plane + x * NO] = s[x].x - hr;
+        o[2 * plane + x * NO] = hi_;
+        o[3 * plane + x * NO] = s[x].y - hi_;
       }
     }
     if constexpr (true) {   // zero the xy padding columns of these energies
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
 
 template <int NO>
 static cudaError_t launch_pi_w_tc_no(const PiWArgs& a, float* Wp, int NNp, int64_t nitems, cudaStream_t st) {
-  const int smem = (6 + kTWE + 3 * kTWE) * kTWPairs * NO * NO * 16;
+  const int smem = (6 + kTWE + 3 * kTWE) * kTWPairs * NO * NO * 8;
   cudaError_t e = cudaFuncSetAttribute(k_pi_w_tc<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   constexpr int NG = (kTcPiPairs + kTWPairs - 1) / kTWPairs;
@@ -291,14 +294,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const float* sb = sa + 4 * kPAPlane;
 #pragma unroll 1
             for (int kk = 0; kk < kPKC / 8; ++kk) {
-              const uint64_t arh = umma_desc_k128(sa + 0 * kPAPlane + kk * 8);
-              const uint64_t arl = umma_desc_k128(sa + 1 * kPAPlane + kk * 8);
-              const uint64_t aih = umma_desc_k128(sa + 2 * kPAPlane + kk * 8);
-              const uint64_t ail = umma_desc_k128(sa + 3 * kPAPlane + kk * 8);
-              const uint64_t brh = umma_desc_k128(sb + 0 * kPBPlane + kk * 8);
-              const uint64_t brl = umma_desc_k128(sb + 1 * kPBPlane + kk * 8);
-              const uint64_t bih = umma_desc_k128(sb + 2 * kPBPlane + kk * 8);
-              const uint64_t bil = umma_desc_k128(sb + 3 * kPBPlane + kk * 8);
+              const uint64_t arh = UMMA_DESC(sa + 0 * kPAPlane + kk * 8);
+              const uint64_t arl = UMMA_DESC(sa + 1 * kPAPlane + kk * 8);
+              const uint64_t aih = UMMA_DESC(sa + 2 * kPAPlane + kk * 8);
+              const uint64_t ail = UMMA_DESC(sa + 3 * kPAPlane + kk * 8);
+              const uint64_t brh = UMMA_DESC(sb + 0 * kPBPlane + kk * 8);
+              const uint64_t brl = UMMA_DESC(sb + 1 * kPBPlane + kk * 8);
+              const uint64_t bih = UMMA_DESC(sb + 2 * kPBPlane + kk * 8);
+              const uint64_t bil = UMMA_DESC(sb + 3 * kPBPlane + kk * 8);
               umma_tf32(dre, arh, brh, id_pos, acc);
               umma_tf32(dre, arh, brl, id_pos, true);
               umma_tf32(dre, arl, brh, id_pos, true);

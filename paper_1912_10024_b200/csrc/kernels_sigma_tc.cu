@@ -10,8 +10,8 @@
 // Precision: every operand is split x ≈ hi + lo with hi = tf32(x), lo = tf32(x − hi) ("3xTF32"), and a real
 // product is hi·hi + hi·lo + lo·hi (relative error ~2^-21); complex products use four real products
 // (Re = ArBr − AiBi via the UMMA negate-A bit, Im = ArBi + AiBr): 12 UMMAs per 8-wide k-step. FP32
-// accumulation over K = Nqz·(2Nω+1) terms in TMEM; the epilogue widens to FP64 (Gt scratch), and the
-// ∇H sandwich (k_sigma_sand) stays FP64.
+// accumulation over K = Nqz·(2Nω+1) terms in TMEM; the epilogue stores the FP32 Gt scratch and the ∇H
+// sandwich (k_sigma_sand<_, float>) runs in FP32, adding into the FP64 Σ.
 //
 // Warp roles (persistent CTA per SM, 192 threads): warp 0 = TMA producer, warp 1 = UMMA issuer (+ TMEM
 // allocation), warps 2..5 = epilogue (TMEM lane quarter warp%4: rc rows 32·(warp%4) ..). Two TMEM
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const uint32_t taddr = tm + ((uint32_t)(quarter * 32) << 16) + buf * kTcBufCols;
       const int rows = 9 * T.item.npair;
-      double2* out = A.Gt + (((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * A.rows * A.NN + rc;
+      float2* out = reinterpret_cast<float2*>(A.Gt) + (((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * A.rows * A.NN + rc;
       for (int n0 = 0; n0 < rows; n0 += 16) {
         float re[16], im[16];
         tmem_ld16(taddr + n0, re);
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(192, 1)
         if (rc < A.NN) {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (n0 + i < rows) out[(int64_t)(n0 + i) * A.NN] = make_double2((double)re[i], (double)im[i]);
+            if (n0 + i < rows) out[(int64_t)(n0 + i) * A.NN] = make_float2(re[i], im[i]);
         }
       }
       tc_fence_before();

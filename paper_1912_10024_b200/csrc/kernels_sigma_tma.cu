@@ -303,13 +303,15 @@ constexpr int kSandPairs = 4;   // pairs per CTA
 constexpr int kSandE = 2;       // energies per iteration
 constexpr int kSandY = 5;       // S columns per thread
 
-template <int NO>
+template <int NO, class R>
 __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
+  using C2 = typename Cx<R>::T;
   constexpr int NN = NO * NO;
-  extern __shared__ __align__(16) double2 sand_sm[];
-  double2* Hr = sand_sm;                         // [kSandPairs][3][NN]
-  double2* Hl = Hr + kSandPairs * 3 * NN;        // [kSandPairs][3][NN]
-  double2* Vs = Hl + kSandPairs * 3 * NN;        // [kSandE][kSandPairs][3][NN]
+  extern __shared__ __align__(16) double2 sand_raw[];
+  C2* sand_sm = reinterpret_cast<C2*>(sand_raw);
+  C2* Hr = sand_sm;                         // [kSandPairs][3][NN]
+  C2* Hl = Hr + kSandPairs * 3 * NN;             // [kSandPairs][3][NN]
+  C2* Vs = Hl + kSandPairs * 3 * NN;             // [kSandE][kSandPairs][3][NN]
   const int ngrp = (A.rows / 9 + kSandPairs - 1) / kSandPairs;   // pair groups per item (2 or 4)
   const int half = blockIdx.x % ngrp;
   const int64_t r = blockIdx.x / ngrp;
@@ -322,10 +324,10 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
   for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
     const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
     const SigPair pr = A.pairs[item.pair0 + t0 + t];
-    Hr[idx] = A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem];
-    Hl[idx] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem];
+    Hr[idx] = Cx<R>::from(A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem]);
+    Hl[idx] = Cx<R>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem]);
   }
-  const double2* gbase = A.Gt + ((int64_t)il * A.Nkz + kz) * A.NE * A.rows * NN;
+  const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)il * A.Nkz + kz) * A.NE * A.rows * NN;
   const int nv = kSandE * P * 3 * NO;   // V rows (e, t, i, x)
   const int ns = kSandE * P * NO;       // S rows (e, t, x)
   for (int e0 = 0; e0 < A.NE; e0 += kSandE) {
@@ -333,22 +335,22 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
     for (int u = threadIdx.x; u < nv; u += blockDim.x) {
       const int x = u % NO, r1 = u / NO, i = r1 % 3, r2 = r1 / 3, t = r2 % P, e = r2 / P;
       if (e0 + e >= A.NE) continue;
-      double2 s[NO];
+      C2 s[NO];
 #pragma unroll
-      for (int y = 0; y < NO; ++y) s[y] = make_double2(0.0, 0.0);
-      const double2* g = gbase + ((int64_t)(e0 + e) * A.rows + (t0 + t) * 9 + i * 3) * NN + x * NO;
+      for (int y = 0; y < NO; ++y) s[y] = Cx<R>::zero();
+      const C2* g = gbase + ((int64_t)(e0 + e) * A.rows + (t0 + t) * 9 + i * 3) * NN + x * NO;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        double2 gv[NO];
+        C2 gv[NO];
 #pragma unroll
         for (int v = 0; v < NO; ++v) gv[v] = __ldg(g + j * NN + v);
-        const double2* hr = Hr + (t * 3 + j) * NN;
+        const C2* hr = Hr + (t * 3 + j) * NN;
 #pragma unroll
         for (int v = 0; v < NO; ++v)
 #pragma unroll
           for (int y = 0; y < NO; ++y) cfma(s[y], gv[v], hr[v * NO + y]);
       }
-      double2* vo = Vs + ((e * kSandPairs + t) * 3 + i) * NN + x * NO;
+      C2* vo = Vs + ((e * kSandPairs + t) * 3 + i) * NN + x * NO;
 #pragma unroll
       for (int y = 0; y < NO; ++y) vo[y] = s[y];
     }
@@ -359,16 +361,16 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
       const int yg = u % NYG, r0 = u / NYG, x = r0 % NO, r1 = r0 / NO, t = r1 % P, e = r1 / P;
       if (e0 + e >= A.NE) continue;
       const int y0 = yg * kSandY;
-      double2 s[kSandY];
+      C2 s[kSandY];
 #pragma unroll
-      for (int y = 0; y < kSandY; ++y) s[y] = make_double2(0.0, 0.0);
+      for (int y = 0; y < kSandY; ++y) s[y] = Cx<R>::zero();
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const double2* hl = Hl + (t * 3 + i) * NN + x * NO;
-        const double2* v = Vs + ((e * kSandPairs + t) * 3 + i) * NN + y0;
+        const C2* hl = Hl + (t * 3 + i) * NN + x * NO;
+        const C2* v = Vs + ((e * kSandPairs + t) * 3 + i) * NN + y0;
 #pragma unroll
         for (int k = 0; k < NO; ++k) {
-          const double2 h = hl[k];
+          const C2 h = hl[k];
 #pragma unroll
           for (int y = 0; y < kSandY; ++y)
             if (y0 + y < NO) cfma(s[y], h, v[k * NO + y]);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
 #pragma unroll
       for (int y = 0; y < kSandY; ++y) {
         if (y0 + y < NO) {
-          const double2 rr = cmul(A.scale, s[y]);
+          const double2 rr = cmul(A.scale, Cx<R>::wide(s[y]));
           atomicAdd(out + 2 * y, rr.x);
           atomicAdd(out + 2 * y + 1, rr.y);
         }
@@ -457,14 +459,19 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
   return cudaGetLastError();
 }
 
-template <int NO>
-static cudaError_t launch_sand_no(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
-  const int smem = (2 + kSandE) * kSandPairs * 3 * NO * NO * 16;
-  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+template <int NO, class R>
+static cudaError_t launch_sand_nr(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
+  const int smem = (2 + kSandE) * kSandPairs * 3 * NO * NO * (int)sizeof(typename Cx<R>::T);
+  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int ngrp = (a.rows / 9 + kSandPairs - 1) / kSandPairs;
-  k_sigma_sand<NO><<<(unsigned)(nitems * a.Nkz * ngrp), 256, smem, st>>>(a);
+  k_sigma_sand<NO, R><<<(unsigned)(nitems * a.Nkz * ngrp), 256, smem, st>>>(a);
   return cudaGetLastError();
+}
+// FP64 Gt scratch (72-row items) or, in the FP32 mixed mode (128-row items), FP32 Gt and an FP32 sandwich
+template <int NO>
+static cudaError_t launch_sand_no(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
+  return a.gt_f32 ? launch_sand_nr<NO, float>(a, nitems, st) : launch_sand_nr<NO, double>(a, nitems, st);
 }
 
 cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {

@@ -433,7 +433,8 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
   // Π W scratch per item: complex tiles + Re+Im plane (24 bytes per element)
   p->sig_rows = d.precision == QT_PREC_FP32_MIXED ? kTcRows : kRows;   // Gt rows per (item, kz, E)
-  const size_t gt_per_item = (size_t)d.Nkz * d.NE * p->sig_rows * ((p->NN + 19) / 20) * 20 * sizeof(double2);
+  const size_t gt_per_item = (size_t)d.Nkz * d.NE * p->sig_rows * ((p->NN + 19) / 20) * 20 *
+                             (d.precision == QT_PREC_FP32_MIXED ? sizeof(float2) : sizeof(double2));
   p->NNp = (p->NN + 3) & ~int64_t(3);
   p->Epad = d.NE + d.shift0 + 80 + 1;
   const size_t w_per_item = d.precision == QT_PREC_FP32_MIXED
@@ -645,6 +646,7 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.ndc = (int)p->ndc;
       sa.Dwin = (int)p->Dwin;
       sa.rows = (int)p->sig_rows;
+      sa.gt_f32 = p->fp32 ? 1 : 0;
       if (p->fp32) {
         QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : p->gtp_elems()), p->NEp,
                                               reinterpret_cast<const float*>(p->ws), (int)p->Kp, i1 - i0, cs));
