@@ -345,8 +345,8 @@ def main():
                "value": round(value, 3), "unit": "Tflop/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None,
-               "dtype": "f64" if not fp32 else "f32-mixed (Σ contraction tf32x3 on tcgen05, FP32 accumulate; "
-                                               "sandwiches and Π FP64)",
+               "dtype": "f64" if not fp32 else "f32-mixed (Σ and Π contractions tf32x3 on tcgen05, FP32 sandwiches; "
+                                               "FP64 inputs/outputs, Π re-accumulated in FP64)",
                "data": "synthetic",
                "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
                                       f"NE={p.NE}, Nω={p.Nw}, Nkz=Nqz={p.Nkz}",

@@ -1,5 +1,6 @@
 """torchrun worker for tests/test_multigpu.py: atom-sharded Σ/Π with the NCCL halo exchange vs the
-unsharded single-GPU result (bit-exact in integer mode, <= 1e-12 relative Frobenius otherwise)."""
+unsharded single-GPU result in the same precision mode (bit-exact in integer mode, <= 1e-12 relative
+Frobenius otherwise: only the order of the FP64 atomic neighbour sums differs)."""
 import os
 import sys
 
@@ -19,12 +20,13 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name = sys.argv[1] if len(sys.argv) > 1 else "small"
     mode = qtgen.INTEGER if (len(sys.argv) > 2 and sys.argv[2] == "integer") else qtgen.RANDOM
+    prec = qt.QT_PREC_FP32_MIXED if (len(sys.argv) > 3 and sys.argv[3] == "fp32") else qt.QT_PREC_FP64
     p = qtgen.problem(name)
     full = qtgen.dev_inputs(p, mode)
-    ref = qt.run(p, full, 1.0, 1j)                          # unsharded reference on this GPU
+    ref = qt.run(p, full, 1.0, 1j, precision=prec)          # unsharded reference on this GPU (same precision)
     obj = [qt.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    plan = qt.Plan(p, rank=rank, nranks=world, shard=qt.QT_SHARD_ATOM, unique_id=obj[0])
+    plan = qt.Plan(p, rank=rank, nranks=world, shard=qt.QT_SHARD_ATOM, unique_id=obj[0], precision=prec)
     info = plan.info()
     a_lo, a_hi, w_lo, w_hi = info["a_lo"], info["a_hi"], info["w_lo"], info["w_hi"]
     win = {}
@@ -58,7 +60,8 @@ def main():
     assert worst <= 1e-12, worst
     dist.barrier()
     if rank == 0:
-        print(f"mgpu ok: {name} {world} ranks, halo {info['halo_bytes']/1e6:.1f} MB/rank, max rel {worst:.2e}")
+        print(f"mgpu ok: {name} {world} ranks, precision {prec}, halo {info['halo_bytes']/1e6:.1f} MB/rank, "
+              f"max rel {worst:.2e}")
     plan.close()
     dist.destroy_process_group()
 
