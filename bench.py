@@ -154,6 +154,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-oracle sample time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workspace-gb", type=float, default=0.0, help="plan scratch cap (0 = min(48 GB, 30%% of HBM))")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 = QT_PREC_FP32_MIXED (reported separately: Σ contraction on tcgen05 tf32x3)")
     args = ap.parse_args()
@@ -181,7 +182,8 @@ def main():
     # ---- plan (atom shard of this rank) and resident inputs for its window
     total_mem = torch.cuda.get_device_properties(local).total_memory
     desc_kw = dict(rank=rank, nranks=world, shard=qt.QT_SHARD_ATOM if world > 1 else qt.QT_SHARD_NONE,
-                   workspace_limit=int(min(48 << 30, 0.3 * total_mem)))
+                   workspace_limit=int(args.workspace_gb * (1 << 30)) if args.workspace_gb > 0
+                   else int(min(48 << 30, 0.3 * total_mem)))
     uid = None
     if world > 1:
         obj = [qt.nccl_unique_id() if rank == 0 else None]
