@@ -27,8 +27,8 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
   extern __shared__ __align__(16) double2 w_sm[];
   double2* Hl = w_sm;                          // [kWPairs][3][NN]  ∇_jH_{as}
   double2* Hr = Hl + kWPairs * 3 * NN;         // [kWPairs][3][NN]  ∇_iH_{br}
-  double2* Gb = Hr + kWPairs * 3 * NN;         // [kWPairs][kWE][NN]
-  double2* T = Gb + kWPairs * kWE * NN;        // [kWPairs][kWE][3][NN]
+  double2* Gb = Hr + kWPairs * 3 * NN;         // [2 buffers][kWPairs][kWE][NN]
+  double2* T = Gb + 2 * kWPairs * kWE * NN;    // [kWPairs][kWE][3][NN]
   const int half = blockIdx.x & 1;
   const int64_t r = blockIdx.x >> 1;
   const int kz = (int)(r % A.Nkz);
@@ -47,13 +47,25 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
   constexpr int NXC = (NN + XC - 1) / XC;
   const int64_t wblk = ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NE * kRows * XC;
   double2* Wdst = A.W + wblk;
-  for (int e0 = 0; e0 < A.NE; e0 += kWE) {
+  // G_b(kz, e0 .. e0+kWE-1) of the group's pairs: cp.async into one of two buffers, one step ahead
+  auto prefetch = [&](int e0, double2* dst) {
     const int ne = min(kWE, A.NE - e0);
-    __syncthreads();
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      Gb[t * kWE * NN + rem] = A.GYam[(((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem];
+      cp_async16(dst + t * kWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem, true);
+    }
+    cp_async_commit();
+  };
+  prefetch(0, Gb);
+  for (int e0 = 0, itr = 0; e0 < A.NE; e0 += kWE, ++itr) {
+    const int ne = min(kWE, A.NE - e0);
+    const double2* Gc = Gb + (itr & 1) * kWPairs * kWE * NN;
+    if (e0 + kWE < A.NE) {
+      prefetch(e0 + kWE, Gb + ((itr + 1) & 1) * kWPairs * kWE * NN);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
     // T_i(t, e)[q][x] = Σ_p G_b[q][p] ∇_iH_{br}[p][x]
@@ -62,7 +74,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
       double2 g[NO], s[NO];
 #pragma unroll
       for (int k = 0; k < NO; ++k) {
-        g[k] = Gb[(t * kWE + e) * NN + q * NO + k];
+        g[k] = Gc[(t * kWE + e) * NN + q * NO + k];
         s[k] = make_double2(0.0, 0.0);
       }
       const double2* h = Hr + (t * 3 + i) * NN;
@@ -376,7 +388,7 @@ __global__ void k_pi_self(PiSelfArgs A) {
 // ---------------------------------------------------------------- launchers
 template <int NO>
 static cudaError_t launch_pi_w_no(const PiWArgs& a, int64_t nitems, cudaStream_t st) {
-  const int smem = (6 + kWE + 3 * kWE) * kWPairs * NO * NO * 16;
+  const int smem = (6 + 2 * kWE + 3 * kWE) * kWPairs * NO * NO * 16;
   cudaError_t e = cudaFuncSetAttribute(k_pi_w<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   k_pi_w<NO><<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);

@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
   extern __shared__ __align__(16) float2 w_sm[];
   float2* Hl = w_sm;                           // [kTWPairs][3][NN]  ∇_jH_{as}
   float2* Hr = Hl + kTWPairs * 3 * NN;         // [kTWPairs][3][NN]  ∇_iH_{br}
-  float2* Gb = Hr + kTWPairs * 3 * NN;         // [kTWPairs][kTWE][NN]
-  float2* T = Gb + kTWPairs * kTWE * NN;       // [kTWPairs][kTWE][3][NN]
+  double2* Gb = reinterpret_cast<double2*>(Hr + kTWPairs * 3 * NN);   // [2][kTWPairs][kTWE][NN] (FP64, cp.async)
+  float2* T = reinterpret_cast<float2*>(Gb + 2 * kTWPairs * kTWE * NN); // [kTWPairs][kTWE][3][NN]
   constexpr int NG = (kTcPiPairs + kTWPairs - 1) / kTWPairs;
   const int grp = blockIdx.x % NG;
   const int64_t r = blockIdx.x / NG;
@@ -118,13 +118,24 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
   const int64_t K = (int64_t)A.Nkz * A.NE * NNp;                    // row length
   const int64_t plane = (int64_t)kTcPiRows * K;
   float* Wi = Wp + (item - A.i0) * 4 * plane;
-  for (int e0 = 0; e0 < A.NE; e0 += kTWE) {
+  auto prefetch = [&](int e0, double2* dst) {
     const int ne = min(kTWE, A.NE - e0);
-    __syncthreads();
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      Gb[t * kTWE * NN + rem] = Cx<float>::from(A.GYam[(((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem]);
+      cp_async16(dst + t * kTWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem, true);
+    }
+    cp_async_commit();
+  };
+  prefetch(0, Gb);
+  for (int e0 = 0, itr = 0; e0 < A.NE; e0 += kTWE, ++itr) {
+    const int ne = min(kTWE, A.NE - e0);
+    const double2* Gc = Gb + (itr & 1) * kTWPairs * kTWE * NN;
+    if (e0 + kTWE < A.NE) {
+      prefetch(e0 + kTWE, Gb + ((itr + 1) & 1) * kTWPairs * kTWE * NN);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
     for (int u = threadIdx.x; u < P * ne * 3 * NO; u += blockDim.x) {   // T_i = G_b ∇_iH_{br}
@@ -132,7 +143,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
       float2 g[NO], s[NO];
 #pragma unroll
       for (int k = 0; k < NO; ++k) {
-        g[k] = Gb[(t * kTWE + e) * NN + q * NO + k];
+        g[k] = Cx<float>::from(Gc[(t * kTWE + e) * NN + q * NO + k]);
         s[k] = make_float2(0.f, 0.f);
       }
       const float2* h = Hr + (t * 3 + i) * NN;
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
 
 template <int NO>
 static cudaError_t launch_pi_w_tc_no(const PiWArgs& a, float* Wp, int NNp, int64_t nitems, cudaStream_t st) {
-  const int smem = (6 + kTWE + 3 * kTWE) * kTWPairs * NO * NO * 8;
+  const int smem = (6 + 3 * kTWE) * kTWPairs * NO * NO * 8 + 2 * kTWE * kTWPairs * NO * NO * 16;
   cudaError_t e = cudaFuncSetAttribute(k_pi_w_tc<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   constexpr int NG = (kTcPiPairs + kTWPairs - 1) / kTWPairs;
