@@ -107,6 +107,9 @@ def test_invalid_arguments_rejected_before_device_use():
     d = qt.make_desc(p, precision=qt.QT_PREC_FP32_MIXED)
     d.Norb = 11
     assert qt.lib.qt_sse_plan(ctypes.byref(d), nbr.ctypes.data, None, ctypes.byref(h)) == qt.QT_ERR_UNSUPPORTED
+    d = qt.make_desc(p, precision=qt.QT_PREC_FP32_MIXED)
+    d.Nw = 81                                      # > 80 = the UMMA N of the FP32-mode Π correlation
+    assert qt.lib.qt_sse_plan(ctypes.byref(d), nbr.ctypes.data, None, ctypes.byref(h)) == qt.QT_ERR_UNSUPPORTED
     d = qt.make_desc(p)
     d.precision = 7
     assert qt.lib.qt_sse_plan(ctypes.byref(d), nbr.ctypes.data, None, ctypes.byref(h)) == qt.QT_ERR_UNSUPPORTED
