@@ -19,9 +19,13 @@
  *   D≷, Π≷ : [Nqz][Nw][Na][Nb+1][3][3]      (slot 0 = self, slot s+1 = neighbour s)
  *   dH     : [Na][Nb][3][Norb][Norb]        dH[a][s][i] = ∇_i H_{a, nbr[a][s]}
  *   neighbors (host, int32): [Na][Nb], -1 = empty slot; must be symmetric.
- * With nranks > 1 (QT_SHARD_ATOM) the G/D/Σ/Π/dH pointers hold the rank's LOCAL atom
+ * With nranks > 1 and QT_SHARD_ATOM the G/D/Σ/Π/dH pointers hold the rank's LOCAL atom
  * window described by qt_sse_info (see qt_sse_query): atoms [w_lo, w_hi) for inputs
- * (owned atoms + neighbour halo), atoms [a_lo, a_hi) for outputs.
+ * (owned atoms + neighbour halo), atoms [a_lo, a_hi) for outputs. With QT_SHARD_ENERGY (the
+ * paper's T_E tiling) every rank holds all atoms; G≷ holds the energy window
+ * [ew_lo, ew_hi) (owned energies ± Dmax), Σ≷ the owned energies [e_lo, e_hi), D≷/∇H are
+ * replicated, and qt_sse_pi returns the full Π≷ on every rank (NCCL all-reduce of the
+ * per-rank partial sums over energies). Energy sharding needs Norb <= 10.
  *
  * Ownership: the caller owns every tensor; outputs are OVERWRITTEN (never accumulated);
  * inputs are never modified. The plan owns its device workspace, work lists and
@@ -76,7 +80,9 @@ typedef struct {
   size_t workspace_bytes;   /* device bytes owned by the plan                               */
   double flops_sigma;       /* algorithmic FP64 flops of one qt_sse_sigma call (both X)     */
   double flops_pi;          /* algorithmic FP64 flops of one qt_sse_pi call (both X)        */
-  double halo_bytes;        /* bytes received per call pair in the atom-halo exchange       */
+  double halo_bytes;        /* bytes received per call pair in the halo exchange            */
+  int64_t e_lo, e_hi;       /* output energies of this rank (all of [0, NE) unless energy-sharded)   */
+  int64_t ew_lo, ew_hi;     /* energy window of this rank's G inputs: [e_lo - Dmax, e_hi + Dmax) ∩ [0,NE) */
 } qt_sse_info;
 
 /* Validates desc + neighbours, builds the work lists, allocates the workspace. */

@@ -37,7 +37,8 @@ class Desc(ctypes.Structure):
 class Info(ctypes.Structure):
     _fields_ = [("a_lo", ctypes.c_int64), ("a_hi", ctypes.c_int64), ("w_lo", ctypes.c_int64),
                 ("w_hi", ctypes.c_int64), ("npairs", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t),
-                ("flops_sigma", ctypes.c_double), ("flops_pi", ctypes.c_double), ("halo_bytes", ctypes.c_double)]
+                ("flops_sigma", ctypes.c_double), ("flops_pi", ctypes.c_double), ("halo_bytes", ctypes.c_double),
+                ("e_lo", ctypes.c_int64), ("e_hi", ctypes.c_int64), ("ew_lo", ctypes.c_int64), ("ew_hi", ctypes.c_int64)]
 
 
 class QTError(RuntimeError):
@@ -119,9 +120,12 @@ def count_flops(p) -> dict:
                 total=sum(out))
 
 
-def shard_info(p, rank: int, nranks: int) -> dict:
-    """Host-only: owned atoms [a_lo,a_hi), input window [w_lo,w_hi), pairs, flops, halo bytes of a rank."""
-    d = make_desc(p, rank=rank, nranks=nranks, shard=QT_SHARD_ATOM if nranks > 1 else QT_SHARD_NONE)
+def shard_info(p, rank: int, nranks: int, shard=None) -> dict:
+    """Host-only: owned atoms [a_lo,a_hi) / energies [e_lo,e_hi), input windows [w_lo,w_hi) / [ew_lo,ew_hi),
+    pairs, flops and halo bytes of a rank (atom sharding unless shard=QT_SHARD_ENERGY)."""
+    if shard is None:
+        shard = QT_SHARD_ATOM if nranks > 1 else QT_SHARD_NONE
+    d = make_desc(p, rank=rank, nranks=nranks, shard=shard)
     i = Info()
     nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
     _check(_get_lib().qt_sse_shard_info(ctypes.byref(d), nbr.ctypes.data, ctypes.byref(i)), "qt_sse_shard_info")

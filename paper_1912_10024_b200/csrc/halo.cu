@@ -81,4 +81,9 @@ int nccl_exchange(void* comm, const std::vector<HaloPeer>& peers, const char* se
   return 0;
 }
 
+// in-place sum over ranks (energy sharding: each rank's Π holds the partial sum over its energies)
+int nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t st) {
+  return ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, (ncclComm_t)comm, st) == ncclSuccess ? 0 : 1;
+}
+
 }  // namespace qt

@@ -23,5 +23,6 @@ int nccl_comm_init(void** comm, int nranks, const void* id128, int rank);
 void nccl_comm_destroy(void* comm);
 int nccl_exchange(void* comm, const std::vector<HaloPeer>& peers, const char* sendbuf, char* recvbuf,
                   cudaStream_t st);
+int nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t st);
 
 }  // namespace qt

@@ -39,6 +39,7 @@ struct SigmaArgs {
   int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk, ntiles;
   int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin, ndc;
   int rows;              // Gt rows per (item, kz, E) block: 72 (items of <= 8 pairs) or 128 (FP32 mode, <= 14)
+  int E0, NEo;           // energy sharding: outputs for window energies [E0, E0 + NEo) (NE = the G window)
   int gt_f32;            // Gt scratch holds float2 (FP32 mixed mode: k_sigma_tc -> FP32 sandwich)
 };
 
@@ -52,6 +53,7 @@ struct PiWArgs {
   double2* W;                 // [item - i0][Nkz][xy chunk][NE][72 rows (t,ij)][20]
   int64_t p0, i0, Nwin, Nb;
   int NE, Nkz, Norb, NN, nEB;
+  int E0, NEo;                // energies of this rank's Π sum: window energies [E0, E0 + NEo)
 };
 
 struct PiCArgs {
@@ -64,6 +66,7 @@ struct PiCArgs {
   double2 scale;
   int64_t i0, nitems, Nwin, Nout, Nb;
   int NE, Nkz, Nqz, h, NN, Nw, NWP, shift0;
+  int E0, NEo;           // energies of this rank's Π sum: window energies [E0, E0 + NEo)
 };
 
 struct PiSelfArgs {

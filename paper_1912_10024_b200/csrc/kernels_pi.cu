@@ -45,23 +45,23 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
   }
   constexpr int XC = 20;                       // = PiCfg::XC
   constexpr int NXC = (NN + XC - 1) / XC;
-  const int64_t wblk = ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NE * kRows * XC;
+  const int64_t wblk = ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NEo * kRows * XC;   // W: energies from E0
   double2* Wdst = A.W + wblk;
   // G_b(kz, e0 .. e0+kWE-1) of the group's pairs: cp.async into one of two buffers, one step ahead
   auto prefetch = [&](int e0, double2* dst) {
-    const int ne = min(kWE, A.NE - e0);
+    const int ne = min(kWE, A.NEo - e0);
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      cp_async16(dst + t * kWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem, true);
+      cp_async16(dst + t * kWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + A.E0 + e0) * NN + rem, true);
     }
     cp_async_commit();
   };
   prefetch(0, Gb);
-  for (int e0 = 0, itr = 0; e0 < A.NE; e0 += kWE, ++itr) {
-    const int ne = min(kWE, A.NE - e0);
+  for (int e0 = 0, itr = 0; e0 < A.NEo; e0 += kWE, ++itr) {
+    const int ne = min(kWE, A.NEo - e0);
     const double2* Gc = Gb + (itr & 1) * kWPairs * kWE * NN;
-    if (e0 + kWE < A.NE) {
+    if (e0 + kWE < A.NEo) {
       prefetch(e0 + kWE, Gb + ((itr + 1) & 1) * kWPairs * kWE * NN);
       cp_async_wait<1>();
     } else {
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
 #pragma unroll
       for (int x = 0; x < NO; ++x) {
         const int xy = x * NO + y, xc = xy / XC, c = xy - xc * XC;
-        const int64_t o = (((int64_t)xc * A.NE + e0 + e) * kRows + (t0 + t) * 9 + ij) * XC + c;
+        const int64_t o = (((int64_t)xc * A.NEo + e0 + e) * kRows + (t0 + t) * 9 + ij) * XC + c;
         Wdst[o] = s[x];
       }
     }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   const int P = item.npair;
   const int NN = A.NN;
   const int nxc = (NN + C::XC - 1) / C::XC;
-  const int e_end = A.NE - A.shift0;                    // E with at least one in-window E + s_m (R7)
+  const int e_end = min(A.NEo, A.NE - A.shift0 - A.E0);   // energies E0 + e with an in-window E + s_m (R7)
   const int nec = e_end > 0 ? (e_end + C::EC - 1) / C::EC : 0;
   const int nst = A.Nkz * nxc * nec;
 
@@ -244,10 +244,10 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         mbar_arrive_expect_tx(&full[slot], T::STAGE_BYTES);
         double2* ws = smem + slot * T::STAGE;
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
-        const int64_t woff = ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NE + ec * C::EC) * kRows * C::XC;
+        const int64_t woff = ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NEo + ec * C::EC) * kRows * C::XC;
         bulk_load(ws, A.W + woff, C::W_STAGE * 16, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE + T::G_STAGE, &tmGS, xc * C::XC, ec * C::EC + A.shift0, k2, item.a_in,
+        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, A.E0 + ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE + T::G_STAGE, &tmGS, xc * C::XC, A.E0 + ec * C::EC + A.shift0, k2, item.a_in,
                     &full[slot]);
         if (++ec == nec) {
           ec = 0;
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const double2* ws = st0 + aoff;
         const double2* gs = st0 + C::W_STAGE + boff;
         const double* gss = reinterpret_cast<const double*>(st0 + C::W_STAGE + T::G_STAGE) + boff;
-        const int rem = A.NE - ec * C::EC - A.shift0;
+        const int rem = A.NE - A.E0 - ec * C::EC - A.shift0;
         if (upper) {
           if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, gs, gss, rem, f0);
         } else {

@@ -115,23 +115,24 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
     Hl[idx] = Cx<float>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem]);
     Hr[idx] = Cx<float>::from(A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + rem]);
   }
-  const int64_t K = (int64_t)A.Nkz * A.NE * NNp;                    // row length
+  const int KwB = ((A.NEo * NNp + kPKC - 1) / kPKC) * kPKC;       // per-kz block (whole K-chunks, zero tail)
+  const int64_t K = (int64_t)A.Nkz * KwB;                          // row length (energies from E0)
   const int64_t plane = (int64_t)kTcPiRows * K;
   float* Wi = Wp + (item - A.i0) * 4 * plane;
   auto prefetch = [&](int e0, double2* dst) {
-    const int ne = min(kTWE, A.NE - e0);
+    const int ne = min(kTWE, A.NEo - e0);
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      cp_async16(dst + t * kTWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + e0) * NN + rem, true);
+      cp_async16(dst + t * kTWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + A.E0 + e0) * NN + rem, true);
     }
     cp_async_commit();
   };
   prefetch(0, Gb);
-  for (int e0 = 0, itr = 0; e0 < A.NE; e0 += kTWE, ++itr) {
-    const int ne = min(kTWE, A.NE - e0);
+  for (int e0 = 0, itr = 0; e0 < A.NEo; e0 += kTWE, ++itr) {
+    const int ne = min(kTWE, A.NEo - e0);
     const double2* Gc = Gb + (itr & 1) * kTWPairs * kTWE * NN;
-    if (e0 + kTWE < A.NE) {
+    if (e0 + kTWE < A.NEo) {
       prefetch(e0 + kTWE, Gb + ((itr + 1) & 1) * kTWPairs * kTWE * NN);
       cp_async_wait<1>();
     } else {
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
       for (int q = 0; q < NO; ++q)
 #pragma unroll
         for (int x = 0; x < NO; ++x) cfma(s[x], hrow[q], tt[q * NO + x]);
-      float* o = Wi + (int64_t)((t0 + t) * 9 + ij) * K + ((int64_t)kz * A.NE + e0 + e) * NNp + y;
+      float* o = Wi + (int64_t)((t0 + t) * 9 + ij) * K + (int64_t)kz * KwB + (int64_t)(e0 + e) * NNp + y;
 #pragma unroll
       for (int x = 0; x < NO; ++x) {
         const float hr = tf32_rna_p(s[x].x), hi_ = tf32_rna_p(s[x].y);
@@ -185,9 +186,15 @@ __global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict
       for (int u = threadIdx.x; u < P * ne * 9 * npad * 4; u += blockDim.x) {
         const int c = u % npad, r1 = u / npad, pl = r1 % 4, r2 = r1 / 4, ij = r2 % 9, r3 = r2 / 9, e = r3 % ne,
                   t = r3 / ne;
-        Wi[pl * plane + (int64_t)((t0 + t) * 9 + ij) * K + ((int64_t)kz * A.NE + e0 + e) * NNp + NN + c] = 0.0f;
+        Wi[pl * plane + (int64_t)((t0 + t) * 9 + ij) * K + (int64_t)kz * KwB + (int64_t)(e0 + e) * NNp + NN + c] = 0.0f;
       }
     }
+  }
+  // zero the K tail of each of the group's rows for this kz (positions NEo·NNp .. KwB of the kz block)
+  for (int u = threadIdx.x; u < P * 9 * 4 * (KwB - A.NEo * NNp); u += blockDim.x) {
+    const int w = KwB - A.NEo * NNp;
+    const int c = u % w, r1 = u / w, pl = r1 % 4, row = r1 / 4;
+    Wi[pl * plane + (int64_t)(t0 * 9 + row) * K + (int64_t)kz * KwB + A.NEo * NNp + c] = 0.0f;
   }
 }
 
@@ -226,6 +233,7 @@ struct PiTcArgs {
   double2 scale;
   int64_t ntiles, Nout, Nb;
   int NE, Nkz, Nqz, h, Nw, shift0, NNp, nch;   // nch = K-chunks per kz
+  int E0, NEo;                                  // this rank's energies: window [E0, E0 + NEo)
 };
 
 __global__ void __launch_bounds__(kPThreads, 1)
@@ -277,8 +285,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           float* sa = stages + slot * kPStage;
           float* sb = sa + 4 * kPAPlane;
           for (int p = 0; p < 4; ++p) {
-            tma_load_4d(sa + p * kPAPlane, &tmA, kz * A.NE * A.NNp + kc, 0, p, il, &full[slot]);
-            tma_load_5d(sb + p * kPBPlane, &tmB, A.shift0 * A.NNp + kc, 0, p, k2, item.a_in, &full[slot]);
+            tma_load_4d(sa + p * kPAPlane, &tmA, kz * A.nch * kPKC + kc, 0, p, il, &full[slot]);
+            tma_load_5d(sb + p * kPBPlane, &tmB, (A.shift0 + A.E0) * A.NNp + kc, 0, p, k2, item.a_in, &full[slot]);
           }
         }
       }
@@ -399,7 +407,8 @@ cudaError_t launch_pi_contract_tc(const PiCArgs& a, const float* Wp, const float
     configured = true;
   }
   if (a.Nw > kPN || nitems == 0) return a.Nw > kPN ? cudaErrorInvalidValue : cudaSuccess;
-  const uint64_t Kw = (uint64_t)a.Nkz * a.NE * NNp;
+  const int KwB = ((a.NEo * NNp + kPKC - 1) / kPKC) * kPKC;
+  const uint64_t Kw = (uint64_t)a.Nkz * KwB;
   CUtensorMap tmA, tmB;
   {
     const uint64_t dims[4] = {Kw, kPM, 4, (uint64_t)nitems};
@@ -434,7 +443,9 @@ cudaError_t launch_pi_contract_tc(const PiCArgs& a, const float* Wp, const float
   p.shift0 = a.shift0;
   p.NNp = NNp;
   // chunks per kz: energies E < NE - shift0 have in-window terms (R7)
-  p.nch = (int)(((int64_t)std::max(0, a.NE - a.shift0) * NNp + kPKC - 1) / kPKC);
+  p.E0 = a.E0;
+  p.NEo = a.NEo;
+  p.nch = KwB / kPKC;   // every chunk of the kz block: the W tail past NEo·NNp is zero, energies past NE read zero G rows
   static int nsm = 0;
   if (nsm == 0) {
     int dev = 0;

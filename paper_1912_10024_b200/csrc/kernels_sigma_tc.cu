@@ -172,9 +172,9 @@ struct TcTile {
 };
 __device__ __forceinline__ TcTile tc_tile(const SigmaArgs& A, int64_t t) {
   TcTile T;
-  T.E = (int)(t % A.NE);
-  T.kz = (int)((t / A.NE) % A.Nkz);
-  T.il = (int)(t / ((int64_t)A.NE * A.Nkz));
+  T.E = A.E0 + (int)(t % A.NEo);              // output energy (window coordinates)
+  T.kz = (int)((t / A.NEo) % A.Nkz);
+  T.il = (int)(t / ((int64_t)A.NEo * A.Nkz));
   T.item = A.items[T.il];
   // shifts d (energy E + d - Dmax) inside the window (R7). Chunk c covers d = 32c - sh + j, j < 32, with
   // sh = (E - Dmax) mod 4, so its G rows start at the 16-byte aligned row E - Dmax + 32c - sh.
@@ -307,7 +307,8 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const uint32_t taddr = tm + ((uint32_t)(quarter * 32) << 16) + buf * kTcBufCols;
       const int rows = 9 * T.item.npair;
-      float2* out = reinterpret_cast<float2*>(A.Gt) + (((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E) * A.rows * A.NN + rc;
+      float2* out =
+          reinterpret_cast<float2*>(A.Gt) + (((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0) * A.rows * A.NN + rc;
       for (int n0 = 0; n0 < rows; n0 += 16) {
         float re[16], im[16];
         tmem_ld16(taddr + n0, re);
@@ -380,7 +381,7 @@ cudaError_t launch_sigma_tc(const SigmaArgs& a, const float* Gtp, int64_t NEp, c
     if (e != cudaSuccess) return e;
   }
   SigmaArgs b = a;
-  b.ntiles = nitems * a.Nkz * a.NE;
+  b.ntiles = nitems * a.Nkz * a.NEo;
   if (b.ntiles == 0) return cudaSuccess;
   static int nsm = 0;
   if (nsm == 0) {

@@ -150,15 +150,15 @@ __device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
   // even grid, ch = t & 1 would give every CTA the same half for the whole launch).
   T.ch = (int)((t ^ (t / gridDim.x)) & 1);
   t >>= 1;
-  T.E = (int)(t % A.NE);
-  T.kz = (int)((t / A.NE) % A.Nkz);
-  T.il = (int)(t / ((int64_t)A.NE * A.Nkz));
+  T.E = A.E0 + (int)(t % A.NEo);              // output energy (window coordinates)
+  T.kz = (int)((t / A.NEo) % A.Nkz);
+  T.il = (int)(t / ((int64_t)A.NEo * A.Nkz));
   T.item = A.items[T.il];
   // An item of n pairs fills F = ceil(9n/8) of the 9 m-fragments; small items process ept = 9/F
   // consecutive energies per tile (tiles with E % ept != 0 are empty), one energy per group of F.
   T.F = (9 * T.item.npair + 7) / 8;
   T.ept = min(kMaxEpt, 9 / T.F);
-  T.skip = (T.E % T.ept) != 0;
+  T.skip = ((T.E - A.E0) % T.ept) != 0;
   // K range: shifts d = 16*dc + k - Dmax with E+e+d in [0,NE) for some e < ept (R7), in whole 16-shift
   // chunks (rows outside the window are zero-filled by TMA; shifts beyond the table are zero coefficients).
   T.dc_lo = max(0, A.Dmax - (T.E + T.ept - 1)) / KC;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
     const int f0 = q ? n0 : 0;
     const int e = mi / T.F, ml = mi - e * T.F;      // energy E+e, m-fragment ml of the item's rows
     const int row = ml * 8 + (lane >> 2);
-    const bool active = e < T.ept && T.E + e < A.NE && nfw > 0;
+    const bool active = e < T.ept && T.E - A.E0 + e < A.NEo && nfw > 0;
     const bool multi = T.ept > 1;
     const int soff = multi ? C::G_STAGE_M : C::G_STAGE;
     const int coff = soff + (multi ? C::S_STAGE_M : C::S_STAGE);
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       if (++c == T.nchunk) c = 0;
     }
     if (active && row < 9 * T.item.npair) {
-      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NE + T.E + e) * A.rows + row) * A.NN;
+      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0 + e) * A.rows + row) * A.NN;
 #pragma unroll
       for (int f = 0; f < C::TMAXW; ++f) {
         if (f < nfw) {
@@ -327,14 +327,14 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
     Hr[idx] = Cx<R>::from(A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem]);
     Hl[idx] = Cx<R>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem]);
   }
-  const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)il * A.Nkz + kz) * A.NE * A.rows * NN;
+  const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)il * A.Nkz + kz) * A.NEo * A.rows * NN;
   const int nv = kSandE * P * 3 * NO;   // V rows (e, t, i, x)
   const int ns = kSandE * P * NO;       // S rows (e, t, x)
-  for (int e0 = 0; e0 < A.NE; e0 += kSandE) {
+  for (int e0 = 0; e0 < A.NEo; e0 += kSandE) {   // output energies (Gt and Σ are indexed from E0)
     __syncthreads();
     for (int u = threadIdx.x; u < nv; u += blockDim.x) {
       const int x = u % NO, r1 = u / NO, i = r1 % 3, r2 = r1 / 3, t = r2 % P, e = r2 / P;
-      if (e0 + e >= A.NE) continue;
+      if (e0 + e >= A.NEo) continue;
       C2 s[NO];
 #pragma unroll
       for (int y = 0; y < NO; ++y) s[y] = Cx<R>::zero();
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
     constexpr int NYG = (NO + kSandY - 1) / kSandY;
     for (int u = threadIdx.x; u < ns * NYG; u += blockDim.x) {
       const int yg = u % NYG, r0 = u / NYG, x = r0 % NO, r1 = r0 / NO, t = r1 % P, e = r1 / P;
-      if (e0 + e >= A.NE) continue;
+      if (e0 + e >= A.NEo) continue;
       const int y0 = yg * kSandY;
       C2 s[kSandY];
 #pragma unroll
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
       }
       const int a_out = A.pairs[item.pair0 + t0 + t].a;
       double* out =
-          reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NE + e0 + e) * A.Nout + a_out) * NN + x * NO + y0);
+          reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NEo + e0 + e) * A.Nout + a_out) * NN + x * NO + y0);
 #pragma unroll
       for (int y = 0; y < kSandY; ++y) {
         if (y0 + y < NO) {
@@ -446,7 +446,7 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
     }
   }
   SigmaArgs b = a;
-  b.ntiles = nitems * a.NE * a.Nkz * 2;
+  b.ntiles = nitems * a.NEo * a.Nkz * 2;
   if (b.ntiles == 0) return cudaSuccess;
   static int nsm = 0;
   if (nsm == 0) {

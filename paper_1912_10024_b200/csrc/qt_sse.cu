@@ -46,10 +46,14 @@ struct qt_sse_plan_s {
   float* ws_gpi = nullptr;      // FP32 mode: split G^X planes for Π [Nwin][Nkz][4][Epad][NNp] (one X at a time)
   int64_t Epad = 0, NNp = 0;
   int64_t sig_rows = kRows;     // Gt rows per (item, kz, E): 72, or 128 in FP32 mode (items of <= 14 pairs)
+  // energy window of this rank's inputs [ew_lo, ew_hi) (NEw energies; all of [0, NE) unless energy-sharded)
+  // and its output energies [e_lo, e_hi) = window energies [E0, E0 + NEo)
+  int64_t e_lo = 0, e_hi = 0, ew_lo = 0, ew_hi = 0, NEw = 0, NEo = 0, E0 = 0;
+  bool eshard = false;
   size_t gpi_elems() const { return (size_t)Nwin * d.Nkz * 4 * Epad * NNp; }
   int64_t NEp = 0, Kp = 0;      // FP32 mode: energy row length (multiple of 4), coefficient row length
   size_t gtp_elems() const { return (size_t)Nwin * d.Nkz * 4 * kTcRowsA * NEp; }
-  size_t gs_elems() const { return (size_t)d.Nkz * d.NE * Nwin * ((NN + 1) & ~int64_t(1)); }
+  size_t gs_elems() const { return (size_t)d.Nkz * NEw * Nwin * ((NN + 1) & ~int64_t(1)); }
   size_t gt_offset = 0;         // byte offset of the Σ Gt scratch inside ws
   bool sig_tma = true;          // Norb <= 10: TMA/3M k_sigma + separate sandwich
   int64_t ndc = 0;              // 16-shift chunks of the Σ coefficient window
@@ -129,7 +133,8 @@ qt_status validate_desc(const qt_sse_desc* d) {
     return QT_ERR_UNSUPPORTED;
   if (d->Norb > 12 || d->shift_step != 1 || d->Nw > 128) return QT_ERR_UNSUPPORTED;
   if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return QT_ERR_INVALID_ARG;
-  if (d->nranks > 1 && d->shard != QT_SHARD_ATOM) return QT_ERR_UNSUPPORTED;
+  if (d->nranks > 1 && d->shard != QT_SHARD_ATOM && d->shard != QT_SHARD_ENERGY) return QT_ERR_UNSUPPORTED;
+  if (d->shard == QT_SHARD_ENERGY && d->Norb > 10) return QT_ERR_UNSUPPORTED;   // the TMA / tcgen05 paths only
   return QT_OK;
 }
 
@@ -159,9 +164,10 @@ int64_t rev_slot(const int32_t* nbr, int64_t Nb, int64_t b, int64_t a) {
 }
 
 // valid (E, m) counts: V- = #{E - s_m >= 0}, V+ = #{E + s_m < NE}
-void window_counts(const qt_sse_desc* d, double* vm, double* vp) {
+void window_counts(const qt_sse_desc* d, double* vm, double* vp, int64_t e_lo = 0, int64_t e_hi = -1) {
   double a = 0, b = 0;
-  for (int64_t e = 0; e < d->NE; ++e)
+  if (e_hi < 0) e_hi = d->NE;
+  for (int64_t e = e_lo; e < e_hi; ++e)
     for (int64_t m = 0; m < d->Nw; ++m) {
       int64_t sm = d->shift0 + m * d->shift_step;
       if (e - sm >= 0) a += 1;
@@ -171,12 +177,14 @@ void window_counts(const qt_sse_desc* d, double* vm, double* vp) {
   *vp = b;
 }
 
-void count_flops(const qt_sse_desc* d, double npairs, double out[4]) {
+// algorithmic flops of the output energies [e_lo, e_hi) (default: all) for npairs valid pairs
+void count_flops(const qt_sse_desc* d, double npairs, double out[4], int64_t e_lo = 0, int64_t e_hi = -1) {
   double vm, vp;
-  window_counts(d, &vm, &vp);
+  if (e_hi < 0) e_hi = d->NE;
+  window_counts(d, &vm, &vp, e_lo, e_hi);
   const double NN = (double)d->Norb * d->Norb, No3 = NN * d->Norb;
   out[0] = 2.0 * d->Nkz * d->Nqz * npairs * (vm + vp) * 9.0 * NN * 8.0;
-  out[1] = 2.0 * d->Nkz * d->NE * npairs * 12.0 * No3 * 8.0;
+  out[1] = 2.0 * d->Nkz * (double)(e_hi - e_lo) * npairs * 12.0 * No3 * 8.0;
   out[2] = out[1];
   out[3] = 2.0 * d->Nkz * d->Nqz * npairs * vp * 9.0 * NN * 8.0;
 }
@@ -200,6 +208,29 @@ void owned_range(const qt_sse_desc* d, const int32_t* nbr, int64_t* lo, int64_t*
   };
   *lo = d->rank == 0 ? 0 : cut(d->rank);
   *hi = d->rank == d->nranks - 1 ? d->Na : cut(d->rank + 1);
+}
+
+// Energy sharding (the paper's T_E tiling): rank r owns output energies [e_lo, e_hi), split by the
+// Σ/Π work per energy (valid shifts + sandwich), and reads the window [e_lo - Dmax, e_hi + Dmax) ∩ [0, NE).
+void energy_range(const qt_sse_desc* d, int r, int64_t* lo, int64_t* hi, int64_t* wlo, int64_t* whi) {
+  std::vector<double> cum(d->NE + 1, 0.0);
+  const int64_t Dmax = d->shift0 + (d->Nw - 1) * d->shift_step;
+  for (int64_t e = 0; e < d->NE; ++e) {
+    double w = 1.0;
+    for (int64_t m = 0; m < d->Nw; ++m) {
+      const int64_t sm = d->shift0 + m * d->shift_step;
+      w += (e - sm >= 0) + 2.0 * (e + sm < d->NE);   // Σ absorption + emission, Π correlation
+    }
+    cum[e + 1] = cum[e] + w;
+  }
+  auto cut = [&](int k) -> int64_t {
+    const double target = cum[d->NE] * k / d->nranks;
+    return (int64_t)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+  };
+  *lo = r == 0 ? 0 : cut(r);
+  *hi = r == d->nranks - 1 ? d->NE : cut(r + 1);
+  *wlo = std::max<int64_t>(0, *lo - Dmax);
+  *whi = std::min<int64_t>(d->NE, *hi + Dmax);
 }
 
 // input window of a rank: its owned atoms plus every neighbour of them (contiguous hull)
@@ -262,12 +293,21 @@ extern "C" qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* n
   if (st != QT_OK) return st;
   if (!o) return QT_ERR_INVALID_ARG;
   if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
-  rank_window(desc, nbr, desc->rank, &o->a_lo, &o->a_hi, &o->w_lo, &o->w_hi);
+  const bool eshard = desc->shard == QT_SHARD_ENERGY && desc->nranks > 1;
+  if (eshard) {
+    o->a_lo = o->w_lo = 0;
+    o->a_hi = o->w_hi = desc->Na;
+    energy_range(desc, desc->rank, &o->e_lo, &o->e_hi, &o->ew_lo, &o->ew_hi);
+  } else {
+    rank_window(desc, nbr, desc->rank, &o->a_lo, &o->a_hi, &o->w_lo, &o->w_hi);
+    o->e_lo = o->ew_lo = 0;
+    o->e_hi = o->ew_hi = desc->NE;
+  }
   double np = 0;
   for (int64_t a = o->a_lo; a < o->a_hi; ++a)
     for (int64_t s = 0; s < desc->Nb; ++s) np += nbr[a * desc->Nb + s] >= 0;
   double f[4];
-  count_flops(desc, np, f);
+  count_flops(desc, np, f, o->e_lo, o->e_hi);
   o->npairs = (int64_t)np;
   o->workspace_bytes = 0;
   o->flops_sigma = f[0] + f[1];
@@ -275,7 +315,14 @@ extern "C" qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* n
   double recv = 0;
   const double per_atom = 2.0 * desc->Nkz * desc->NE * desc->Norb * desc->Norb * 16 +
                           2.0 * desc->Nqz * desc->Nw * (desc->Nb + 1) * 9 * 16;
-  for (int r = 0; r < desc->nranks; ++r) {
+  const double per_e = 2.0 * desc->Nkz * desc->Na * desc->Norb * desc->Norb * 16;
+  for (int r = 0; eshard && r < desc->nranks; ++r) {
+    if (r == desc->rank) continue;
+    int64_t elo, ehi, wlo, whi;
+    energy_range(desc, r, &elo, &ehi, &wlo, &whi);
+    recv += std::max<int64_t>(0, std::min(o->ew_hi, ehi) - std::max(o->ew_lo, elo)) * per_e;
+  }
+  for (int r = 0; !eshard && r < desc->nranks; ++r) {
     if (r == desc->rank) continue;
     int64_t alo, ahi, wlo, whi;
     rank_window(desc, nbr, r, &alo, &ahi, &wlo, &whi);
@@ -333,9 +380,44 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   p->DWp = (p->Dwin + 3) & ~3LL;
   p->NWP = (d.Nw + 7) & ~7LL;
   p->nbr.assign(nbr, nbr + d.Na * d.Nb);
-  rank_window(&d, nbr, d.rank, &p->a_lo, &p->a_hi, &p->w_lo, &p->w_hi);
+  p->eshard = d.shard == QT_SHARD_ENERGY && d.nranks > 1;
+  if (p->eshard) {
+    // energy sharding: all atoms, an energy window; halo = window energies owned by peers (G only: D and
+    // ∇H do not depend on energy and are replicated)
+    p->a_lo = p->w_lo = 0;
+    p->a_hi = p->w_hi = d.Na;
+    energy_range(&d, d.rank, &p->e_lo, &p->e_hi, &p->ew_lo, &p->ew_hi);
+    const size_t per_e = 2 * (size_t)d.Nkz * d.Na * d.Norb * d.Norb * 16;
+    for (int r = 0; r < d.nranks; ++r) {
+      if (r == d.rank) continue;
+      int64_t elo, ehi, wlo, whi;
+      energy_range(&d, r, &elo, &ehi, &wlo, &whi);
+      HaloPeer h;
+      h.rank = r;
+      const int64_t rl = std::max(p->ew_lo, elo), rh = std::min(p->ew_hi, ehi);
+      const int64_t sl = std::max(p->e_lo, wlo), sh = std::min(p->e_hi, whi);
+      h.recv_lo = rl - p->ew_lo;
+      h.recv_n = std::max<int64_t>(0, rh - rl);
+      h.send_lo = sl - p->ew_lo;
+      h.send_n = std::max<int64_t>(0, sh - sl);
+      h.recv_bytes = h.recv_n * per_e;
+      h.send_bytes = h.send_n * per_e;
+      h.recv_off = p->recv_total;
+      h.send_off = p->send_total;
+      p->recv_total += h.recv_bytes;
+      p->send_total += h.send_bytes;
+      if (h.recv_n || h.send_n) p->peers.push_back(h);
+    }
+  } else {
+    rank_window(&d, nbr, d.rank, &p->a_lo, &p->a_hi, &p->w_lo, &p->w_hi);
+    p->e_lo = p->ew_lo = 0;
+    p->e_hi = p->ew_hi = d.NE;
+  }
+  p->NEw = p->ew_hi - p->ew_lo;
+  p->NEo = p->e_hi - p->e_lo;
+  p->E0 = p->e_lo - p->ew_lo;
   // halo exchange plan: receive window atoms owned by peers, send owned atoms in the peers' windows
-  if (d.nranks > 1) {
+  if (d.nranks > 1 && !p->eshard) {
     const size_t per_atom = 2 * (size_t)d.Nkz * d.NE * d.Norb * d.Norb * 16 + 2 * (size_t)d.Nqz * d.Nw * (d.Nb + 1) * 9 * 16;
     for (int r = 0; r < d.nranks; ++r) {
       if (r == d.rank) continue;
@@ -427,18 +509,18 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     }
   }
   p->n_pi_pairs = (int64_t)pp.size();
-  count_flops(&d, (double)p->n_pi_pairs, p->flops);
+  count_flops(&d, (double)p->n_pi_pairs, p->flops, p->e_lo, p->e_hi);
 
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
   // Π W scratch per item: complex tiles + Re+Im plane (24 bytes per element)
   p->sig_rows = d.precision == QT_PREC_FP32_MIXED ? kTcRows : kRows;   // Gt rows per (item, kz, E)
-  const size_t gt_per_item = (size_t)d.Nkz * d.NE * p->sig_rows * ((p->NN + 19) / 20) * 20 *
+  const size_t gt_per_item = (size_t)d.Nkz * p->NEo * p->sig_rows * ((p->NN + 19) / 20) * 20 *
                              (d.precision == QT_PREC_FP32_MIXED ? sizeof(float2) : sizeof(double2));
   p->NNp = (p->NN + 3) & ~int64_t(3);
-  p->Epad = d.NE + d.shift0 + 80 + 1;
+  p->Epad = p->NEw + d.shift0 + 80 + 1;
   const size_t w_per_item = d.precision == QT_PREC_FP32_MIXED
-                                ? (size_t)4 * kTcPiRows * d.Nkz * d.NE * p->NNp * sizeof(float)
+                                ? (size_t)4 * kTcPiRows * d.Nkz * (((p->NEo * p->NNp + 31) / 32) * 32) * sizeof(float)
                                 : gt_per_item;
   size_t budget = d.workspace_limit;
   if (budget == 0) {
@@ -450,7 +532,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
   }
   p->fp32 = d.precision == QT_PREC_FP32_MIXED;
-  p->NEp = std::max<int64_t>(32, (d.NE + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
+  p->NEp = std::max<int64_t>(32, (p->NEw + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
   p->Kp = (p->Dwin + 3 + 31) & ~int64_t(31);   // delayed coefficient rows (d + s, s <= 3), whole 32-chunks
   const size_t coef_item_t = p->fp32 ? (size_t)d.Nqz * 16 * kTcRows * p->Kp * sizeof(float)
                                      : (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * kCoefKCP * sizeof(double2);
@@ -511,7 +593,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     qt_sse_destroy(p);
     return s2;
   }
-  p->g_elems = (size_t)d.Nkz * d.NE * p->Nwin * p->NN;
+  p->g_elems = (size_t)d.Nkz * p->NEw * p->Nwin * p->NN;
   if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess ||
       cudaMalloc(&p->ws_gs, 2 * p->gs_elems() * sizeof(double)) != cudaSuccess ||
       (p->fp32 && cudaMalloc(&p->ws_gtp, 2 * p->gtp_elems() * sizeof(float)) != cudaSuccess) ||
@@ -564,6 +646,10 @@ extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
   o->flops_sigma = p->flops[0] + p->flops[1];
   o->flops_pi = p->flops[2] + p->flops[3];
   o->halo_bytes = (double)p->recv_total;
+  o->e_lo = p->e_lo;
+  o->e_hi = p->e_hi;
+  o->ew_lo = p->ew_lo;
+  o->ew_hi = p->ew_hi;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? QT_OK : cuda_status(e);
 }
@@ -579,14 +665,14 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
     if (q == SL || q == SG) return QT_ERR_INVALID_ARG;
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
-  const size_t sig_bytes = (size_t)d.Nkz * d.NE * p->Nout * p->NN * sizeof(double2);
+  const size_t sig_bytes = (size_t)d.Nkz * p->NEo * p->Nout * p->NN * sizeof(double2);
   if (p->fp32) {
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GL, p->ws_gtp, d.Nkz, d.NE, p->NEp, p->Nwin, (int)p->NN, cs));
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GG, p->ws_gtp + p->gtp_elems(), d.Nkz, d.NE, p->NEp, p->Nwin,
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GL, p->ws_gtp, d.Nkz, p->NEw, p->NEp, p->Nwin, (int)p->NN, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GG, p->ws_gtp + p->gtp_elems(), d.Nkz, p->NEw, p->NEp, p->Nwin,
                                                 (int)p->NN, cs));
   } else {
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, d.NE, p->Nwin, p->NN, cs));
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, d.NE, p->Nwin, p->NN, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, p->NEw, p->Nwin, p->NN, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, p->NEw, p->Nwin, p->NN, cs));
   }
   for (int X = 0; X < 2; ++X) {
     void* S = X == 0 ? SL : SG;
@@ -636,7 +722,9 @@ extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* G
       sa.Nout = p->Nout;
       sa.Nb = d.Nb;
       sa.DWp = p->DWp;
-      sa.NE = (int)d.NE;
+      sa.NE = (int)p->NEw;
+      sa.E0 = (int)p->E0;
+      sa.NEo = (int)p->NEo;
       sa.Nkz = (int)d.Nkz;
       sa.Nqz = (int)d.Nqz;
       sa.h = (int)p->h;
@@ -670,14 +758,14 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
     if (q == PL || q == PG) return QT_ERR_INVALID_ARG;
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, d.NE, p->Nwin, p->NN, cs));
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, d.NE, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, p->NEw, p->Nwin, p->NN, cs));
+  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, p->NEw, p->Nwin, p->NN, cs));
   for (int X = 0; X < 2; ++X) {
     const double2* GXam = p->ws_g + (X == 0 ? 0 : p->g_elems);
     const double2* GY = (const double2*)(X == 0 ? GG : GL);
     double2* P = (double2*)(X == 0 ? PL : PG);
     if (p->fp32)
-      QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_pi_tc((const double2*)(X == 0 ? GL : GG), p->ws_gpi, d.Nkz, d.NE, p->Epad,
+      QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_pi_tc((const double2*)(X == 0 ? GL : GG), p->ws_gpi, d.Nkz, p->NEw, p->Epad,
                                                      p->Nwin, (int)p->NN, (int)p->NNp, cs));
     for (size_t c = 0; c + 1 < p->pi_chunks.size(); ++c) {
       const int64_t i0 = p->pi_chunks[c], i1 = p->pi_chunks[c + 1];
@@ -696,11 +784,13 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       wa.i0 = i0;
       wa.Nwin = p->Nwin;
       wa.Nb = d.Nb;
-      wa.NE = (int)d.NE;
+      wa.NE = (int)p->NEw;
+      wa.E0 = (int)p->E0;
+      wa.NEo = (int)p->NEo;
       wa.Nkz = (int)d.Nkz;
       wa.Norb = (int)d.Norb;
       wa.NN = (int)p->NN;
-      wa.nEB = (int)((d.NE + kEB - 1) / kEB);
+      wa.nEB = (int)((p->NEw + kEB - 1) / kEB);
       if (p->fp32) {
         QT_LAUNCH(QT_K_PI_W, launch_pi_w_tc(wa, reinterpret_cast<float*>(p->ws), (int)p->NNp, i1 - i0, cs));
       } else {
@@ -719,7 +809,9 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
       ca.Nwin = p->Nwin;
       ca.Nout = p->Nout;
       ca.Nb = d.Nb;
-      ca.NE = (int)d.NE;
+      ca.NE = (int)p->NEw;
+      ca.E0 = (int)p->E0;
+      ca.NEo = (int)p->NEo;
       ca.Nkz = (int)d.Nkz;
       ca.Nqz = (int)d.Nqz;
       ca.h = (int)p->h;
@@ -743,6 +835,11 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
     sa.Nw = d.Nw;
     sa.a_off = p->a_lo - p->w_lo;
     QT_LAUNCH(QT_K_PI_SELF, launch_pi_self(sa, cs));
+    if (p->eshard) {   // Π is a sum over energies: add the ranks' partial sums (NCCL over NVLink)
+      if (!p->comm) return QT_ERR_UNSUPPORTED;
+      const size_t n = (size_t)d.Nqz * d.Nw * p->Nout * (d.Nb + 1) * 9 * 2;
+      if (nccl_allreduce_sum(p->comm, reinterpret_cast<double*>(P), n, cs) != 0) return QT_ERR_NCCL;
+    }
   }
   return QT_OK;
 }
@@ -754,9 +851,9 @@ extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const 
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
   const size_t b_dH = (size_t)p->Nwin * d.Nb * 3 * p->NN * 16;
-  const size_t b_G = (size_t)d.Nkz * d.NE * p->Nwin * p->NN * 16;
+  const size_t b_G = (size_t)d.Nkz * p->NEw * p->Nwin * p->NN * 16;
   const size_t b_D = (size_t)d.Nqz * d.Nw * p->Nwin * (d.Nb + 1) * 9 * 16;
-  const size_t b_S = (size_t)d.Nkz * d.NE * p->Nout * p->NN * 16;
+  const size_t b_S = (size_t)d.Nkz * p->NEo * p->Nout * p->NN * 16;
   const size_t b_P = (size_t)d.Nqz * d.Nw * p->Nout * (d.Nb + 1) * 9 * 16;
   const size_t total = b_dH + 2 * b_G + 2 * b_D + 2 * b_S + 2 * b_P;
   if (p->h_dev_bytes < total) {
@@ -795,20 +892,26 @@ extern "C" qt_status qt_sse_halo_exchange(qt_sse_plan_t p, void* GL, void* GG, v
     if (!aligned16(t)) return QT_ERR_INVALID_ARG;
   cudaStream_t cs = (cudaStream_t)stream;
   const qt_sse_desc& d = p->d;
-  const int64_t outer[4] = {d.Nkz * d.NE, d.Nkz * d.NE, d.Nqz * d.Nw, d.Nqz * d.Nw};
-  const int64_t inner[4] = {p->NN * 16, p->NN * 16, (d.Nb + 1) * 9 * 16, (d.Nb + 1) * 9 * 16};
+  // atom sharding: G≷ [Nkz·NE][atoms][NN] and D≷ [Nqz·Nω][atoms][Nb+1][9] along atoms; energy sharding:
+  // G≷ [Nkz][energies][Na·NN] along energies (D≷ replicated)
+  const int nt = p->eshard ? 2 : 4;
+  const int64_t outer[4] = {p->eshard ? d.Nkz : d.Nkz * d.NE, p->eshard ? d.Nkz : d.Nkz * d.NE, d.Nqz * d.Nw,
+                            d.Nqz * d.Nw};
+  const int64_t inner[4] = {p->eshard ? d.Na * p->NN * 16 : p->NN * 16, p->eshard ? d.Na * p->NN * 16 : p->NN * 16,
+                            (d.Nb + 1) * 9 * 16, (d.Nb + 1) * 9 * 16};
+  const int64_t span = p->eshard ? p->NEw : p->Nwin;
   for (const HaloPeer& h : p->peers) {
     size_t off = h.send_off;
-    for (int k = 0; k < 4; ++k) {
-      QT_LAUNCH(QT_K_HALO, launch_pack(ts[k], p->sendbuf + off, outer[k], p->Nwin, h.send_lo, h.send_n, inner[k], false, cs));
+    for (int k = 0; k < nt; ++k) {
+      QT_LAUNCH(QT_K_HALO, launch_pack(ts[k], p->sendbuf + off, outer[k], span, h.send_lo, h.send_n, inner[k], false, cs));
       off += (size_t)outer[k] * h.send_n * inner[k];
     }
   }
   if (nccl_exchange(p->comm, p->peers, p->sendbuf, p->recvbuf, cs) != 0) return QT_ERR_NCCL;
   for (const HaloPeer& h : p->peers) {
     size_t off = h.recv_off;
-    for (int k = 0; k < 4; ++k) {
-      QT_LAUNCH(QT_K_HALO, launch_pack(p->recvbuf + off, ts[k], outer[k], p->Nwin, h.recv_lo, h.recv_n, inner[k], true, cs));
+    for (int k = 0; k < nt; ++k) {
+      QT_LAUNCH(QT_K_HALO, launch_pack(p->recvbuf + off, ts[k], outer[k], span, h.recv_lo, h.recv_n, inner[k], true, cs));
       off += (size_t)outer[k] * h.recv_n * inner[k];
     }
   }

@@ -102,3 +102,52 @@ def test_atom_sharding_matches_single_process_oracle(world):
         ref = np.concatenate([np.ascontiguousarray(x[:, :, a_lo:a_hi]).view(np.float64).ravel()
                               for x in (SL, SG, PL, PG)])
         assert np.array_equal(buf, ref)   # integer mode: bit-exact
+
+
+def _eworker(rank, world, port, result_q):
+    """Energy sharding (the paper's T_E tiling): the oracle on this rank's energy window reproduces the owned
+    energies of Σ exactly; the owned energies partition [0, NE); windows are owned ± Dmax."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1912_10024_b200 as qt
+    p = qtgen.problem("tiny")
+    inp = qtgen.host_inputs(p, qtgen.INTEGER)
+    info = qt.shard_info(p, rank, world, shard=qt.QT_SHARD_ENERGY)
+    e_lo, e_hi, ew_lo, ew_hi = info["e_lo"], info["e_hi"], info["ew_lo"], info["ew_hi"]
+    dmax = p.shift0 + p.Nw - 1
+    assert ew_lo == max(0, e_lo - dmax) and ew_hi == min(p.NE, e_hi + dmax)
+    assert info["a_lo"] == 0 and info["a_hi"] == p.Na
+    wp = Problem(p.nbr, p.Norb, ew_hi - ew_lo, p.Nw, p.Nkz, Nqz=p.Nqz, shift0=p.shift0)
+    win = dict(inp)
+    win["G_less"] = inp["G_less"][:, ew_lo:ew_hi]
+    win["G_gtr"] = inp["G_gtr"][:, ew_lo:ew_hi]
+    SL, SG = oracle.sigma(wp, win, 1.0)
+    own = slice(e_lo - ew_lo, e_hi - ew_lo)
+    mine = [np.ascontiguousarray(SL[:, own]), np.ascontiguousarray(SG[:, own])]
+    objs = [None] * world
+    dist.all_gather_object(objs, (e_lo, e_hi, info["halo_bytes"], mine))
+    if rank == 0:
+        result_q.put(objs)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_energy_sharding_matches_single_process_oracle(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_eworker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    objs = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=600)
+        assert pr.exitcode == 0
+    p = qtgen.problem("tiny")
+    inp = qtgen.host_inputs(p, qtgen.INTEGER)
+    SL, SG = oracle.sigma(p, inp, 1.0)
+    assert objs[0][0] == 0 and objs[-1][1] == p.NE
+    assert all(objs[r][1] == objs[r + 1][0] for r in range(world - 1))
+    assert all(o[2] > 0 for o in objs)
+    for e_lo, e_hi, _, (sl, sg) in objs:
+        assert np.array_equal(sl, SL[:, e_lo:e_hi]) and np.array_equal(sg, SG[:, e_lo:e_hi])
