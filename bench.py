@@ -154,6 +154,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-oracle sample time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", default="atom", choices=["atom", "energy"],
+                    help="N>1 partition: atom slabs + neighbour halo, or energy slabs + Nω halo and a Π all-reduce")
     ap.add_argument("--workspace-gb", type=float, default=0.0, help="plan scratch cap (0 = min(48 GB, 30%% of HBM))")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 = QT_PREC_FP32_MIXED (reported separately: Σ contraction on tcgen05 tf32x3)")
@@ -181,7 +183,9 @@ def main():
 
     # ---- plan (atom shard of this rank) and resident inputs for its window
     total_mem = torch.cuda.get_device_properties(local).total_memory
-    desc_kw = dict(rank=rank, nranks=world, shard=qt.QT_SHARD_ATOM if world > 1 else qt.QT_SHARD_NONE,
+    eshard = world > 1 and args.shard == "energy"
+    desc_kw = dict(rank=rank, nranks=world,
+                   shard=(qt.QT_SHARD_ENERGY if eshard else qt.QT_SHARD_ATOM) if world > 1 else qt.QT_SHARD_NONE,
                    workspace_limit=int(args.workspace_gb * (1 << 30)) if args.workspace_gb > 0
                    else int(min(48 << 30, 0.3 * total_mem)))
     uid = None
@@ -194,32 +198,34 @@ def main():
                    **desc_kw)
     info = plan.info()
     w_lo, w_hi, a_lo, a_hi = info["w_lo"], info["w_hi"], info["a_lo"], info["a_hi"]
+    e_lo, e_hi, ew_lo, ew_hi = info["e_lo"], info["e_hi"], info["ew_lo"], info["ew_hi"]
     nwin, nout = w_hi - w_lo, a_hi - a_lo
     NN = p.Norb ** 2
     c128 = torch.complex128
     nbr_dev = torch.from_numpy(p.nbr).to(dev)
-    G_less = torch.empty((p.Nkz, p.NE, nwin, p.Norb, p.Norb), dtype=c128, device=dev)
+    G_less = torch.empty((p.Nkz, ew_hi - ew_lo, nwin, p.Norb, p.Norb), dtype=c128, device=dev)
     G_gtr = torch.empty_like(G_less)
     D_less = torch.empty((p.Nqz, p.Nw, nwin, p.Nb + 1, 3, 3), dtype=c128, device=dev)
     D_gtr = torch.empty_like(D_less)
     dH_full = torch.empty((p.Na, p.Nb, 3, p.Norb, p.Norb), dtype=c128, device=dev)
-    qtgen.dev_G(p, qtgen.ID_GL, G_less, a_lo=w_lo, a_hi=w_hi)
-    qtgen.dev_G(p, qtgen.ID_GG, G_gtr, a_lo=w_lo, a_hi=w_hi)
+    qtgen.dev_G(p, qtgen.ID_GL, G_less, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
+    qtgen.dev_G(p, qtgen.ID_GG, G_gtr, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
     qtgen.dev_D(p, qtgen.ID_DL, D_less, nbr_dev, a_lo=w_lo, a_hi=w_hi)
     qtgen.dev_D(p, qtgen.ID_DG, D_gtr, nbr_dev, a_lo=w_lo, a_hi=w_hi)
     qtgen.dev_dH(p, dH_full, nbr_dev)
     dH = dH_full[w_lo:w_hi].contiguous()
     del dH_full
-    S_less = torch.empty((p.Nkz, p.NE, nout, p.Norb, p.Norb), dtype=c128, device=dev)
+    S_less = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
     S_gtr = torch.empty_like(S_less)
     P_less = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
     P_gtr = torch.empty_like(P_less)
     torch.cuda.synchronize()
     in_bytes = sum(t.numel() * 16 for t in (G_less, G_gtr, D_less, D_gtr, dH))
     out_bytes = sum(t.numel() * 16 for t in (S_less, S_gtr, P_less, P_gtr))
+    allreduce_bytes = 2 * P_less.numel() * 16 if eshard else 0     # Π≷ partial sums, energy sharding
 
     def step():
-        if world > 1:   # halo atoms (owned by neighbouring ranks) over NCCL, inside the timed step
+        if world > 1:   # halo atoms / energies (owned by other ranks) over NCCL, inside the timed step
             plan.halo_exchange(G_less, G_gtr, D_less, D_gtr, stream)
         plan.sigma(dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, 1j, stream)
         plan.pi(dH, G_less, G_gtr, P_less, P_gtr, -1j, stream)
@@ -266,6 +272,12 @@ def main():
     sig_ms, sig_n = kern["k_sigma"]
     share = info["npairs"] / max(1, int((p.nbr >= 0).sum()))          # this rank's share of the pairs
     contr_step = qt.count_flops(p)["sigma_contraction"] * share        # F_alg of k_sigma per step (both X)
+    if eshard:   # this rank's energies: valid (E, ±shift) pairs of [e_lo, e_hi) over all of them
+        sm = p.shift0 + np.arange(p.Nw)
+        def valid(lo, hi):
+            e = np.arange(lo, hi)[:, None]
+            return float(((e - sm >= 0).sum() + (e + sm < p.NE).sum()))
+        contr_step = qt.count_flops(p)["sigma_contraction"] * valid(e_lo, e_hi) / valid(0, p.NE)
     per_launch = contr_step * args.steps / max(sig_n, 1)
     achieved = per_launch / (sig_ms / max(sig_n, 1) * 1e-3) / 1e12
     prof_traffic = None
@@ -352,10 +364,12 @@ def main():
                "data": "synthetic",
                "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
                                       f"NE={p.NE}, Nω={p.Nw}, Nkz=Nqz={p.Nkz}",
-                          "flops_per_step": flops_step, "parallelism": f"atom-shard x{world}",
+                          "flops_per_step": flops_step,
+                          "parallelism": f"{'energy' if eshard else 'atom'}-shard x{world}",
                           "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (in_bytes / 1e9)},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "halo_bytes_per_rank": info["halo_bytes"],
+               "comm_bytes_per_rank_per_step": info["halo_bytes"] + allreduce_bytes,
                "clocks": clk, "pct_fp64_peak": None if fp32 else round(value / (FP64_PEAK_TFLOPS * world) * 100, 2)}
         print(json.dumps(out), file=out_stream, flush=True)
     plan.close()
