@@ -65,7 +65,8 @@ typedef struct {
                                                /* ≤1e-5 per block for conditioned blocks); the ∇H  */
                                                /* sandwiches and Π stay FP64 (SURVEY §8(f) NEXT(1),*/
                                                /* PAPER.md §4.4)                         */
-  qt_shard shard;                              /* QT_SHARD_NONE, or QT_SHARD_ATOM with nranks > 1   */
+  qt_shard shard;                              /* QT_SHARD_NONE, or with nranks > 1 QT_SHARD_ATOM  */
+                                               /* (default; fewer bytes moved) or QT_SHARD_ENERGY  */
   int32_t rank, nranks;
   const void* nccl_unique_id;                  /* host ptr to a 128-byte ncclUniqueId (nranks > 1)  */
   size_t workspace_limit;                      /* bytes of device scratch the plan may use; 0 = auto */
@@ -108,11 +109,12 @@ qt_status qt_sse_execute_host(qt_sse_plan_t plan, const void* dH, const void* G_
 
 qt_status qt_sse_query(qt_sse_plan_t plan, qt_sse_info* out);
 
-/* Halo exchange (nranks > 1, QT_SHARD_ATOM, plan created with an NCCL unique id — then qt_sse_plan is
- * collective over the ranks): fills the halo atoms of the local input window (atoms owned by other ranks)
- * from their owners with one grouped ncclSend/ncclRecv round on `cuda_stream`. In-place on the caller's
- * window buffers; only halo atoms are written, owned atoms are only read. Returns QT_ERR_UNSUPPORTED
- * when the plan has no communicator, QT_ERR_NCCL on NCCL failure. */
+/* Halo exchange (nranks > 1, plan created with an NCCL unique id — then qt_sse_plan is collective over
+ * the ranks): fills the halo of the local input window from the owners with one grouped ncclSend/ncclRecv
+ * round on `cuda_stream`: with QT_SHARD_ATOM the halo atoms of G≷ and D≷, with QT_SHARD_ENERGY the halo
+ * energies of G≷ (D≷ is replicated and not touched). In-place on the caller's window buffers; only halo
+ * entries are written, owned ones are only read. With QT_SHARD_ENERGY, qt_sse_pi also all-reduces Π≷ over
+ * the ranks. Returns QT_ERR_UNSUPPORTED when the plan has no communicator, QT_ERR_NCCL on NCCL failure. */
 qt_status qt_sse_halo_exchange(qt_sse_plan_t plan, void* G_less, void* G_gtr, void* D_less, void* D_gtr,
                                void* cuda_stream);
 
