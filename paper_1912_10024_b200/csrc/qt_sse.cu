@@ -278,12 +278,15 @@ extern "C" qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* 
   if (st != QT_OK) return st;
   if (!out) return QT_ERR_INVALID_ARG;
   if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
-  int64_t lo, hi;
-  owned_range(desc, nbr, &lo, &hi);
+  int64_t lo = 0, hi = desc->Na, e_lo = 0, e_hi = desc->NE, wlo, whi;
+  if (desc->shard == QT_SHARD_ENERGY && desc->nranks > 1)
+    energy_range(desc, desc->rank, &e_lo, &e_hi, &wlo, &whi);   // all atoms, this rank's energies
+  else
+    owned_range(desc, nbr, &lo, &hi);
   double np = 0;
   for (int64_t a = lo; a < hi; ++a)
     for (int64_t s = 0; s < desc->Nb; ++s) np += nbr[a * desc->Nb + s] >= 0;
-  count_flops(desc, np, out);
+  count_flops(desc, np, out, e_lo, e_hi);
   return QT_OK;
 }
 

@@ -151,3 +151,19 @@ def test_energy_sharding_matches_single_process_oracle(world):
     assert all(o[2] > 0 for o in objs)
     for e_lo, e_hi, _, (sl, sg) in objs:
         assert np.array_equal(sl, SL[:, e_lo:e_hi]) and np.array_equal(sg, SG[:, e_lo:e_hi])
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_per_rank_flops_partition_the_total(nranks):
+    """qt_sse_shard_info: the ranks' algorithmic flops add up to the unsharded count for both partitions
+    (atoms: owned pairs; energies: owned (E, shift) pairs and sandwiches)."""
+    import paper_1912_10024_b200 as qt
+    p = qtgen.problem("small")
+    f = qt.count_flops(p)
+    for shard in (qt.QT_SHARD_ATOM, qt.QT_SHARD_ENERGY):
+        infos = [qt.shard_info(p, r, nranks, shard=shard) for r in range(nranks)]
+        tot = sum(i["flops_sigma"] + i["flops_pi"] for i in infos)
+        assert abs(tot - f["total"]) <= 1e-9 * f["total"], (shard, tot, f["total"])
+        if shard == qt.QT_SHARD_ENERGY:
+            assert [i["e_lo"] for i in infos][0] == 0 and infos[-1]["e_hi"] == p.NE
+            assert all(infos[r]["e_hi"] == infos[r + 1]["e_lo"] for r in range(nranks - 1))
