@@ -300,9 +300,12 @@ def main():
         # nominal tf32/bf16 ratio (1.1 / 2.25 PF dense).
         mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
         tf32_peak = round(mp.get("bf16_tflops_sustained", 1385.4) * 1.1 / 2.25, 1)
+        tc_traffic = None
+        if tf.exists():
+            tc_traffic = json.loads(tf.read_text()).get(args.config, {}).get("k_sigma_tc")
         roofline = {"bound": "tensor", "kernel": "k_sigma_tc (Σ D-contraction, tcgen05.mma kind::tf32, 3xTF32)",
                     "achieved": round(3 * achieved, 3), "peak": tf32_peak, "unit": "TFLOP/s",
-                    "frac": round(3 * achieved / tf32_peak, 4), "traffic": None,
+                    "frac": round(3 * achieved / tf32_peak, 4), "traffic": tc_traffic,
                     "flops_basis": "useful tf32 flops: 3 x algorithmic (24 tf32 flops per complex MAC), padding "
                                    "(Norb² of 128 UMMA rows, 72 of 80 columns) not counted",
                     "algorithmic_tflops": round(achieved, 3),
