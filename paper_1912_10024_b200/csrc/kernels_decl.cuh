@@ -13,7 +13,7 @@ struct CoefArgs {
   double2* coef;
   int64_t npairs, Nw, Nwin, Nb, Nqz, DWp;
   int Dmax, shift0;
-  // tiled layout (TMA path): [item - item0][q][dc][72 rows (t,ij)][20], d = 16*dc + k - Dmax
+  // tiled layout (TMA path): [item - item0][q][dc][72 rows (t,ij)][kCoefKCP], d = 16*dc + k - Dmax
   bool tiled;
   int64_t item0, nitems, ndc, Dwin;
 };

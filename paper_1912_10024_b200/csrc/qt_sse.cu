@@ -516,7 +516,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
 
   // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
   const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
-  // Π W scratch per item: complex tiles + Re+Im plane (24 bytes per element)
+  // Π W scratch per item: complex tiles (FP64 mode) or four fp32 split planes (FP32 mode)
   p->sig_rows = d.precision == QT_PREC_FP32_MIXED ? kTcRows : kRows;   // Gt rows per (item, kz, E)
   const size_t gt_per_item = (size_t)d.Nkz * p->NEo * p->sig_rows * ((p->NN + 19) / 20) * 20 *
                              (d.precision == QT_PREC_FP32_MIXED ? sizeof(float2) : sizeof(double2));
@@ -562,7 +562,7 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
     bounds.push_back((int64_t)items.size());
   };
   make_chunks(p->pi_items, w_per_item, false, p->pi_chunks);
-  // Σ chunks. TMA path (Norb <= 10): per item a tiled coefficient block [q][16-shift chunk][72][20] +
+  // Σ chunks. TMA path (Norb <= 10): per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] +
   // its Gt scratch; cp.async path (Norb 11, 12): per pair coefficient rows. Workspace = [coef | Gt].
   {
     p->sig_tma = d.Norb <= 10;
