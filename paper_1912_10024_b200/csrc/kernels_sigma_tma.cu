@@ -299,12 +299,19 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 // shared memory. Compile-time Norb: a V-thread owns a row (e, t, i, x) of V^i = Σ_j Gt^{ij}∇_jH_{br}
 // (Gt row loaded into registers, ∇H broadcast from shared memory, Norb accumulators); an S-thread owns
 // a row (e, t, x) of S = Σ_i ∇_iH_{as} V^i and adds scale·S into Σ_a with RED.F64.
-constexpr int kSandPairs = 4;   // pairs per CTA
+#ifndef QT_SAND_P
+#define QT_SAND_P 2
+#endif
+#ifndef QT_SAND_T
+#define QT_SAND_T 128
+#endif
+constexpr int kSandPairs = QT_SAND_P;   // pairs per CTA
+constexpr int kSandThreads = QT_SAND_T;
 constexpr int kSandE = 2;       // energies per iteration
 constexpr int kSandY = 5;       // S columns per thread
 
 template <int NO, class R>
-__global__ void __launch_bounds__(256, 2) k_sigma_sand(SigmaArgs A) {
+__global__ void __launch_bounds__(kSandThreads, 512 / kSandThreads) k_sigma_sand(SigmaArgs A) {
   using C2 = typename Cx<R>::T;
   constexpr int NN = NO * NO;
   extern __shared__ __align__(16) double2 sand_raw[];
@@ -465,7 +472,7 @@ static cudaError_t launch_sand_nr(const SigmaArgs& a, int64_t nitems, cudaStream
   cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int ngrp = (a.rows / 9 + kSandPairs - 1) / kSandPairs;
-  k_sigma_sand<NO, R><<<(unsigned)(nitems * a.Nkz * ngrp), 256, smem, st>>>(a);
+  k_sigma_sand<NO, R><<<(unsigned)(nitems * a.Nkz * ngrp), kSandThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 // FP64 Gt scratch (72-row items) or, in the FP32 mixed mode (128-row items), FP32 Gt and an FP32 sandwich
