@@ -18,19 +18,27 @@ namespace qt {
 // T-threads own a row (t, e, i, q) of T_i = G^Y_b ∇_iH_{br}, W-threads own a column set (t, e, i, j, y):
 // W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x] for all x. The W block of (item, kz, E) is 72 contiguous
 // rows per 20-wide xy chunk; each thread's stores fill part of it (L2 merges the partial lines).
-constexpr int kWPairs = 4;
+#ifndef QT_PIW_P
+#define QT_PIW_P 2
+#endif
+#ifndef QT_PIW_T
+#define QT_PIW_T 128
+#endif
+constexpr int kWPairs = QT_PIW_P;
+constexpr int kWThreads = QT_PIW_T;
+constexpr int kWGroups = (kMaxPairs + kWPairs - 1) / kWPairs;   // CTAs per (item, kz)
 constexpr int kWE = 2;
 
 template <int NO>
-__global__ void __launch_bounds__(256, 2) k_pi_w(PiWArgs A) {
+__global__ void __launch_bounds__(kWThreads, 512 / kWThreads) k_pi_w(PiWArgs A) {
   constexpr int NN = NO * NO;
   extern __shared__ __align__(16) double2 w_sm[];
   double2* Hl = w_sm;                          // [kWPairs][3][NN]  ∇_jH_{as}
   double2* Hr = Hl + kWPairs * 3 * NN;         // [kWPairs][3][NN]  ∇_iH_{br}
   double2* Gb = Hr + kWPairs * 3 * NN;         // [2 buffers][kWPairs][kWE][NN]
   double2* T = Gb + 2 * kWPairs * kWE * NN;    // [kWPairs][kWE][3][NN]
-  const int half = blockIdx.x & 1;
-  const int64_t r = blockIdx.x >> 1;
+  const int half = blockIdx.x % kWGroups;
+  const int64_t r = blockIdx.x / kWGroups;
   const int kz = (int)(r % A.Nkz);
   const int64_t item = A.i0 + r / A.Nkz;
   const PiItem it = A.items[item];
@@ -391,7 +399,7 @@ static cudaError_t launch_pi_w_no(const PiWArgs& a, int64_t nitems, cudaStream_t
   const int smem = (6 + 2 * kWE + 3 * kWE) * kWPairs * NO * NO * 16;
   cudaError_t e = cudaFuncSetAttribute(k_pi_w<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_pi_w<NO><<<(unsigned)(nitems * a.Nkz * 2), 256, smem, st>>>(a);
+  k_pi_w<NO><<<(unsigned)(nitems * a.Nkz * kWGroups), kWThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

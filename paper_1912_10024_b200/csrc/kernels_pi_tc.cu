@@ -89,11 +89,18 @@ cudaError_t launch_relayout_pi_tc(const double2* G, float* out, int64_t Nkz, int
 // same order as k_pi_w) written as split planes
 // Wp[il][plane][row = t·9+ij][k = (kz·NE + E)·NNp + x·Norb + y]; xy padding columns are zero. One CTA per
 // (item, kz, group of 4 pairs), looping over energy pairs.
-constexpr int kTWPairs = 4;
+#ifndef QT_PIWTC_P
+#define QT_PIWTC_P 4
+#endif
+#ifndef QT_PIWTC_T
+#define QT_PIWTC_T 256
+#endif
+constexpr int kTWPairs = QT_PIWTC_P;
+constexpr int kTWThreads = QT_PIWTC_T;
 constexpr int kTWE = 2;
 
 template <int NO>
-__global__ void __launch_bounds__(256, 2) k_pi_w_tc(PiWArgs A, float* __restrict__ Wp, int NNp) {
+__global__ void __launch_bounds__(kTWThreads, 512 / kTWThreads) k_pi_w_tc(PiWArgs A, float* __restrict__ Wp, int NNp) {
   constexpr int NN = NO * NO;
   extern __shared__ __align__(16) float2 w_sm[];
   float2* Hl = w_sm;                           // [kTWPairs][3][NN]  ∇_jH_{as}
@@ -204,7 +211,7 @@ static cudaError_t launch_pi_w_tc_no(const PiWArgs& a, float* Wp, int NNp, int64
   cudaError_t e = cudaFuncSetAttribute(k_pi_w_tc<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   constexpr int NG = (kTcPiPairs + kTWPairs - 1) / kTWPairs;
-  k_pi_w_tc<NO><<<(unsigned)(nitems * a.Nkz * NG), 256, smem, st>>>(a, Wp, NNp);
+  k_pi_w_tc<NO><<<(unsigned)(nitems * a.Nkz * NG), kTWThreads, smem, st>>>(a, Wp, NNp);
   return cudaGetLastError();
 }
 
