@@ -5,11 +5,15 @@ workload (default cfg3: Si FinFET slice, 4,864 atoms, Nb=34, Norb=10, NE=176, NÏ
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one rank per GPU). Ranks own contiguous atom slabs (atom sharding,
-the paper's Ta tiling); every step first receives the neighbour halo (atoms owned
-by other ranks) with one grouped NCCL send/recv round inside the library, then computes Î£/Î  for its own
-atoms (owner-computes: no reduction). `value` is the total algorithmic flops of all ranks Ã· the max
-over ranks of the device time (strong scaling: cfg3's total work is fixed).
+N > 1 runs one rank per GPU: under torchrun (RANK/WORLD_SIZE set by the launcher), or, when started
+plainly with --gpus N, bench.py launches `torch.distributed.run --nproc-per-node N` on itself. The ranks
+form the paper's Ta x TE grid (PAPER.md P:816-841; --shard atom = Ta x 1, the default by measured bytes;
+energy = 1 x TE; 2d = --grid-atoms x N/Ta). One step is one qt_sse_sigma_pi call per rank: the library
+receives the window halo over NCCL on its communication stream (overlapped with the interior sources),
+computes Î£/Î  for the rank's block and, with TE > 1, reduces the Î  partial sums to their owners. `value`
+is the total algorithmic flops of all ranks Ã· the max over ranks of the device time of the K timed steps
+(strong scaling: cfg3's total work is fixed); `step_ms` adds the median and a 95% confidence interval of
+the per-step times (paper protocol).
 """
 from __future__ import annotations
 
@@ -28,7 +32,26 @@ sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
 
-FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 sustained, profiles/r01_fp64_peak.jsonl (nominal 37.2)
+FP64_PEAK_NOMINAL = 37.2   # 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+
+
+def fp64_peak():
+    """Measured FP64 roofline denominator: the 3-s sustained DMMA m8n8k4 run of tools/fp64_peak.cu
+    (profiles/r01_fp64_peak.jsonl; MEASURED_PEAKS.json has no FP64 entry). A kernel timed inside a step of
+    seconds runs at the sustained, not the burst, rate."""
+    f = ROOT / "profiles" / "r01_fp64_peak.jsonl"
+    burst = sust = None
+    if f.exists():
+        for line in f.read_text().splitlines():
+            r = json.loads(line)
+            if r.get("test") == "dmma_sustained":
+                sust = r["tflops"]
+            elif r.get("test") == "dmma_m8n8k4":
+                burst = max(burst or 0.0, r["tflops"])
+    if sust is None:
+        return FP64_PEAK_NOMINAL, "nominal 37.2 TF (148 SMs x 64 FMA/clk x 2 x 1.965 GHz): no measured FP64 peak found", None
+    return sust, ("measured: DMMA m8n8k4 sustained for 3 s on this pool's B200 (profiles/r01_fp64_peak.jsonl, "
+                  "tools/fp64_peak.cu); MEASURED_PEAKS.json has no FP64 entry"), burst
 METRIC = "SSE Î£+Î  FP64 Tflop/s and % of FP64 roofline at 1/2/4/8 B200 vs CPU oracle"
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                  0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -116,6 +139,91 @@ def oracle_sample(p, host, n_sig, n_pi, seed):
     return block_flops(p, sb, pb), dt, len(sb), len(pb)
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def median_ci(xs, conf=0.95, nboot=4000, seed=0):
+    """Median of xs and a bootstrap percentile confidence interval of the median."""
+    xs = np.asarray(xs, dtype=np.float64)
+    med = float(np.median(xs))
+    if xs.size < 2:
+        return med, [med, med]
+    rng = np.random.default_rng(seed)
+    boots = np.median(rng.choice(xs, size=(nboot, xs.size), replace=True), axis=1)
+    lo, hi = np.percentile(boots, [100 * (1 - conf) / 2, 100 * (1 + conf) / 2])
+    return med, [float(lo), float(hi)]
+
+
+def stratified_oracle(p, host, target_s, seed=7):
+    """Stratified sample of the full oracle (SURVEY Â§8(d)): Î£ blocks by (edge / interior energy) x (surface /
+    bulk atom), Î  blocks by (self / neighbour slot) x (low / high frequency); each stratum timed on its own.
+    Returns the sampled F_alg, time, block counts and the EXTRAPOLATED full-oracle time = Î£ over strata of
+    (mean block time x block count)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    deg = (p.nbr >= 0).sum(1)
+    surface, bulk = np.nonzero(deg < p.Nb)[0], np.nonzero(deg == p.Nb)[0]
+    e_all = np.arange(p.NE)
+    e_edge = e_all[(e_all < p.Nw) | (e_all >= p.NE - p.Nw)]
+    e_int = e_all[(e_all >= p.Nw) & (e_all < p.NE - p.Nw)]
+    strata = []
+    for ename, es in (("edge E", e_edge), ("interior E", e_int)):
+        for aname, ats in (("surface", surface), ("bulk", bulk)):
+            if es.size and ats.size:
+                strata.append(("sigma", f"{ename}/{aname}", es, ats, 2 * p.Nkz * es.size * ats.size))
+    npairs_nb = int((p.nbr >= 0).sum())
+    m_all = np.arange(p.Nw)
+    for mname, ms in (("low m", m_all[: max(1, p.Nw // 2)]), ("high m", m_all[max(1, p.Nw // 2):])):
+        if ms.size:
+            strata.append(("pi", f"self/{mname}", ms, None, 2 * p.Nqz * ms.size * p.Na))
+            strata.append(("pi", f"nbr/{mname}", ms, None, 2 * p.Nqz * ms.size * npairs_nb))
+    # calibration pass: one block per stratum sized for ~target_s in total
+    per = max(2, host_cores())
+    out, f_tot, t_tot, t_full, nsig, npi = [], 0.0, 0.0, 0.0, 0, 0
+    for pas in range(2):
+        out, f_tot, t_tot, t_full, nsig, npi = [], 0.0, 0.0, 0.0, 0, 0
+        for kind, name, idx, ats, count in strata:
+            n = per
+            if pas == 1:
+                n = int(max(per, min(64 * per, per * target_s / max(t_cal * len(strata), 1e-3))))
+            if kind == "sigma":
+                blk = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nkz, n), rng.choice(idx, n),
+                                rng.choice(ats, n)], 1)
+                t0 = time.perf_counter()
+                oracle.sigma_blocks(p, host, blk)
+                dt = time.perf_counter() - t0
+                f = block_flops(p, blk, [])
+                nsig += n
+            else:
+                a = rng.integers(0, p.Na, n)
+                if name.startswith("self"):
+                    slot = np.zeros(n, dtype=np.int64)
+                else:
+                    a = rng.choice(np.nonzero(deg > 0)[0], n)
+                    slot = np.array([1 + rng.choice(np.nonzero(p.nbr[x] >= 0)[0]) for x in a])
+                blk = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nqz, n), rng.choice(idx, n), a, slot], 1)
+                t0 = time.perf_counter()
+                oracle.pi_blocks(p, host, blk)
+                dt = time.perf_counter() - t0
+                f = block_flops(p, [], blk[blk[:, 4] > 0])   # self slots: no algorithmic work of their own
+                npi += n
+            out.append({"stratum": f"{kind} {name}", "blocks": n, "seconds": round(dt, 3), "population": int(count)})
+            f_tot += f
+            t_tot += dt
+            t_full += dt / n * count
+        if pas == 0:
+            t_cal = t_tot / max(1, len(strata))
+    return f_tot, t_tot, nsig, npi, t_full, out
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -143,27 +251,47 @@ def _claim_stdout():
     return os.fdopen(real, "w")
 
 
+def _relaunch(args) -> int:
+    """`bench.py --gpus N` without a launcher: run torch.distributed.run with N ranks on this script."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("bench: launching", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
 def main():
-    out_stream = _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-oracle sample time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--shard", default="atom", choices=["atom", "energy"],
-                    help="N>1 partition: atom slabs + neighbour halo, or energy slabs + NÏ‰ halo and a Î  all-reduce")
+    ap.add_argument("--shard", default="atom", choices=["atom", "energy", "2d"],
+                    help="N>1 grid: atom slabs + neighbour halo (Ta=N), energy slabs + NÏ‰ halo + Î  reduction "
+                         "(TE=N), or a Ta x TE grid (2d, Ta = --grid-atoms)")
+    ap.add_argument("--grid-atoms", type=int, default=2)
     ap.add_argument("--workspace-gb", type=float, default=0.0, help="plan scratch cap (0 = min(48 GB, 30%% of HBM))")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
-                    help="fp32 = QT_PREC_FP32_MIXED (reported separately: Î£ contraction on tcgen05 tf32x3)")
+                    help="fp32 = QT_PREC_FP32_MIXED (reported separately: contractions on tcgen05 tf32x3)")
+    ap.add_argument("--separate", action="store_true", help="qt_sse_sigma + qt_sse_pi instead of the fused call")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(_relaunch(args))
+    out_stream = _claim_stdout()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and args.impl == "ours":
+        log(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+        sys.exit(2)
 
     import qtgen
     p = qtgen.problem(args.config)
@@ -181,11 +309,11 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
-    # ---- plan (atom shard of this rank) and resident inputs for its window
+    # ---- plan (this rank's block of the Ta x TE grid) and resident inputs for its window
     total_mem = torch.cuda.get_device_properties(local).total_memory
-    eshard = world > 1 and args.shard == "energy"
-    desc_kw = dict(rank=rank, nranks=world,
-                   shard=(qt.QT_SHARD_ENERGY if eshard else qt.QT_SHARD_ATOM) if world > 1 else qt.QT_SHARD_NONE,
+    shard = {"atom": qt.QT_SHARD_ATOM, "energy": qt.QT_SHARD_ENERGY, "2d": qt.QT_SHARD_2D}[args.shard] \
+        if world > 1 else qt.QT_SHARD_NONE
+    desc_kw = dict(rank=rank, nranks=world, shard=shard, grid_atoms=args.grid_atoms if args.shard == "2d" else 0,
                    workspace_limit=int(args.workspace_gb * (1 << 30)) if args.workspace_gb > 0
                    else int(min(48 << 30, 0.3 * total_mem)))
     uid = None
@@ -199,8 +327,8 @@ def main():
     info = plan.info()
     w_lo, w_hi, a_lo, a_hi = info["w_lo"], info["w_hi"], info["a_lo"], info["a_hi"]
     e_lo, e_hi, ew_lo, ew_hi = info["e_lo"], info["e_hi"], info["ew_lo"], info["ew_hi"]
+    pa_lo, pa_hi = info["pa_lo"], info["pa_hi"]
     nwin, nout = w_hi - w_lo, a_hi - a_lo
-    NN = p.Norb ** 2
     c128 = torch.complex128
     nbr_dev = torch.from_numpy(p.nbr).to(dev)
     G_less = torch.empty((p.Nkz, ew_hi - ew_lo, nwin, p.Norb, p.Norb), dtype=c128, device=dev)
@@ -208,31 +336,50 @@ def main():
     D_less = torch.empty((p.Nqz, p.Nw, nwin, p.Nb + 1, 3, 3), dtype=c128, device=dev)
     D_gtr = torch.empty_like(D_less)
     dH_full = torch.empty((p.Na, p.Nb, 3, p.Norb, p.Norb), dtype=c128, device=dev)
-    qtgen.dev_G(p, qtgen.ID_GL, G_less, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
-    qtgen.dev_G(p, qtgen.ID_GG, G_gtr, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
-    qtgen.dev_D(p, qtgen.ID_DL, D_less, nbr_dev, a_lo=w_lo, a_hi=w_hi)
-    qtgen.dev_D(p, qtgen.ID_DG, D_gtr, nbr_dev, a_lo=w_lo, a_hi=w_hi)
+    # each rank generates only its OWNED block; the halo region is left as garbage (NaN) for the library's
+    # exchange to fill inside every timed step
+    G_less.fill_(float("nan"))
+    G_gtr.fill_(float("nan"))
+    D_less.fill_(float("nan"))
+    D_gtr.fill_(float("nan"))
+    for t, tid in ((G_less, qtgen.ID_GL), (G_gtr, qtgen.ID_GG)):
+        own = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
+        qtgen.dev_G(p, tid, own, e_lo=e_lo, e_hi=e_hi, a_lo=a_lo, a_hi=a_hi)
+        t[:, e_lo - ew_lo:e_hi - ew_lo, a_lo - w_lo:a_hi - w_lo] = own
+        del own
+    for t, tid in ((D_less, qtgen.ID_DL), (D_gtr, qtgen.ID_DG)):
+        own = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
+        qtgen.dev_D(p, tid, own, nbr_dev, a_lo=a_lo, a_hi=a_hi)
+        t[:, :, a_lo - w_lo:a_hi - w_lo] = own
+        del own
+    if world == 1:
+        assert not torch.isnan(G_less).any()
     qtgen.dev_dH(p, dH_full, nbr_dev)
     dH = dH_full[w_lo:w_hi].contiguous()
     del dH_full
     S_less = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
     S_gtr = torch.empty_like(S_less)
-    P_less = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
+    P_less = torch.empty((p.Nqz, p.Nw, pa_hi - pa_lo, p.Nb + 1, 3, 3), dtype=c128, device=dev)
     P_gtr = torch.empty_like(P_less)
     torch.cuda.synchronize()
     in_bytes = sum(t.numel() * 16 for t in (G_less, G_gtr, D_less, D_gtr, dH))
     out_bytes = sum(t.numel() * 16 for t in (S_less, S_gtr, P_less, P_gtr))
-    allreduce_bytes = 2 * P_less.numel() * 16 if eshard else 0     # Î â‰· partial sums, energy sharding
 
     def step():
-        if world > 1:   # halo atoms / energies (owned by other ranks) over NCCL, inside the timed step
-            plan.halo_exchange(G_less, G_gtr, D_less, D_gtr, stream)
-        plan.sigma(dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, 1j, stream)
-        plan.pi(dH, G_less, G_gtr, P_less, P_gtr, -1j, stream)
+        if args.separate:
+            if world > 1:
+                plan.halo_exchange(G_less, G_gtr, D_less, D_gtr, stream)
+            plan.sigma(dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, 1j, stream)
+            plan.pi(dH, G_less, G_gtr, P_less, P_gtr, -1j, stream)
+        else:
+            plan.sigma_pi(dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr, 1j, -1j, stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if torch.isnan(S_less).any() or torch.isnan(P_less).any():
+        log("bench: NaN in the outputs (halo not filled?)")
+        sys.exit(3)
 
     # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the launching stream
     clocks = Clocks(local)
@@ -243,41 +390,39 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     n0 = qt.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for k in range(args.steps):
         step()
-    ev1.record(stream)
+        evs[k + 1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     launches = qt.launch_count() - n0
-    ms_total = ev0.elapsed_time(ev1)
+    ms_total = evs[0].elapsed_time(evs[-1])
+    per_step = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     kern = plan.timing_read()
     plan.timing(False)
 
-    t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    t_local = torch.tensor([ms_total] + per_step, dtype=torch.float64, device=dev)
     f_local = torch.tensor([info["flops_sigma"] + info["flops_pi"]], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
         dist.all_reduce(f_local, op=dist.ReduceOp.SUM)
-    ms_step = float(t_local.item()) / args.steps
+    tl = t_local.cpu().tolist()
+    ms_step = tl[0] / args.steps
     flops_step = float(f_local.item())
     value = flops_step / (ms_step * 1e-3) / 1e12
+    med, ci = median_ci(tl[1:])
+    peak, peak_src, peak_burst = fp64_peak()
 
     # ---- roofline: dominant kernel (k_sigma = the Î£ D-contraction), algorithmic flops per launch Ã· its
     # average launch time (library CUDA events on the launching stream, timed region only).
-    fl = qt.count_flops(p) if world == 1 else None
     sig_ms, sig_n = kern["k_sigma"]
-    share = info["npairs"] / max(1, int((p.nbr >= 0).sum()))          # this rank's share of the pairs
-    contr_step = qt.count_flops(p)["sigma_contraction"] * share        # F_alg of k_sigma per step (both X)
-    if eshard:   # this rank's energies: valid (E, Â±shift) pairs of [e_lo, e_hi) over all of them
-        sm = p.shift0 + np.arange(p.Nw)
-        def valid(lo, hi):
-            e = np.arange(lo, hi)[:, None]
-            return float(((e - sm >= 0).sum() + (e + sm < p.NE).sum()))
-        contr_step = qt.count_flops(p)["sigma_contraction"] * valid(e_lo, e_hi) / valid(0, p.NE)
+    fl_all = qt.count_flops(p)
+    contr_step = qt.count_flops(p, rank=rank, nranks=world, shard=shard,
+                                grid_atoms=desc_kw["grid_atoms"])["sigma_contraction"]   # this rank's share
     per_launch = contr_step * args.steps / max(sig_n, 1)
     achieved = per_launch / (sig_ms / max(sig_n, 1) * 1e-3) / 1e12
     prof_traffic = None
@@ -286,14 +431,14 @@ def main():
         prof_traffic = json.loads(tf.read_text()).get(args.config, {}).get("k_sigma")
     if not fp32:
         roofline = {"bound": "tensor", "kernel": "k_sigma (Î£ D-contraction, DMMA.8x8x4 FP64)",
-                    "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": prof_traffic,
+                    "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+                    "frac": round(achieved / peak, 4), "traffic": prof_traffic,
                     "flops_basis": "algorithmic: 8 real flops per complex MAC, in-window valid-pair work only",
                     "executed_dmma_tflops": round(achieved * 0.75, 3),
+                    "executed_frac": round(achieved * 0.75 / peak, 4),
                     "executed_note": "Gauss 3M complex product: the tensor pipe executes 3 real 8x8x4 DMMAs (6 flops) "
-                                     "per complex MAC; executed = 0.75 x achieved",
-                    "peak_source": "measured FP64 DMMA m8n8k4 sustained (profiles/r01_fp64_peak.jsonl); "
-                                   "MEASURED_PEAKS.json has no FP64 entry"}
+                                     "per complex MAC, so executed = 0.75 x achieved and frac can reach 1.33",
+                    "peak_source": peak_src, "peak_burst": peak_burst, "peak_nominal": FP64_PEAK_NOMINAL}
     else:
         # tcgen05 kind::tf32: 4 real products per complex MAC, each as 3 tf32 MMAs (hiÂ·hi + hiÂ·lo + loÂ·hi) =
         # 24 tf32 flops per complex MAC = 3 x the algorithmic 8; peak = measured sustained bf16 x the guide's
@@ -307,7 +452,7 @@ def main():
                     "achieved": round(3 * achieved, 3), "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": round(3 * achieved / tf32_peak, 4), "traffic": tc_traffic,
                     "flops_basis": "useful tf32 flops: 3 x algorithmic (24 tf32 flops per complex MAC), padding "
-                                   "(NorbÂ² of 128 UMMA rows, 72 of 80 columns) not counted",
+                                   "(NorbÂ² of 128 UMMA rows, 126 of 128 columns) not counted",
                     "algorithmic_tflops": round(achieved, 3),
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (tf32/bf16 dense nominal)"}
     roofline.update({"launches_per_step": sig_n / args.steps, "share_of_step": round(sig_ms / ms_total, 4),
@@ -315,18 +460,17 @@ def main():
 
     # ---- e2e through the public C-ABI call on pinned HOST buffers (H2D + compute + D2H every step)
     e2e = None
+    hin = None
     if not args.no_e2e:
         hin = {k: torch.empty(v.shape, dtype=c128, pin_memory=True)
                for k, v in (("dH", dH), ("G_less", G_less), ("G_gtr", G_gtr), ("D_less", D_less), ("D_gtr", D_gtr))}
         for k, v in (("dH", dH), ("G_less", G_less), ("G_gtr", G_gtr), ("D_less", D_less), ("D_gtr", D_gtr)):
             hin[k].copy_(v)
+        hout = {k: torch.empty(v.shape, dtype=c128, pin_memory=True)
+                for k, v in (("S_less", S_less), ("S_gtr", S_gtr), ("P_less", P_less), ("P_gtr", P_gtr))}
         # free the device-resident copies: execute_host stages through plan-owned buffers
         del G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr
         torch.cuda.empty_cache()
-        hout = {k: torch.empty(s, dtype=c128, pin_memory=True) for k, s in
-                (("S_less", (p.Nkz, p.NE, nout, p.Norb, p.Norb)), ("S_gtr", (p.Nkz, p.NE, nout, p.Norb, p.Norb)),
-                 ("P_less", (p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3)),
-                 ("P_gtr", (p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3)))}
         args_h = (hin["dH"], hin["G_less"], hin["G_gtr"], hin["D_less"], hin["D_gtr"],
                   hout["S_less"], hout["S_gtr"], hout["P_less"], hout["P_gtr"])
         plan.execute_host(*args_h, stream=stream)       # warm (allocates the plan's staging buffers)
@@ -341,43 +485,59 @@ def main():
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         e2e = {"value": round(flops_step / float(t_e2e.item()) / 1e12, 3), "unit": "Tflop/s",
                "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(out_bytes), "steps": e2e_steps,
-               "api": "qt_sse_execute_host (pinned host buffers)"}
+               "api": "qt_sse_execute_host (pinned host buffers; qt_sse_sigma_pi inside)"}
 
-    # ---- CPU oracle baseline (rank 0, N=1 only), bounded sample of the same workload
+    # ---- CPU oracle baseline (rank 0, N=1 only): stratified bounded sample of the same workload
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        host = hin if e2e is not None else None
-        if host is None:
-            host = qtgen.host_inputs(p)
+        host = hin if hin is not None else qtgen.host_inputs(p)
         hnp = {k: (v.numpy() if hasattr(v, "numpy") else v) for k, v in host.items()}
         os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
-        fs, dt, ns, npi = calibrated_oracle(p, hnp, args.cpu_seconds)
-        cpu = {"value": round(fs / dt / 1e12, 6), "unit": "Tflop/s", "cores": host_cores(), "kind": "oracle",
-               "sample": f"{ns} Î£ blocks + {npi} Î  blocks of {args.config} (random (X,kz,E,a) / (X,qz,m,a,s)), "
-                         f"{dt:.1f} s, F_alg of the sampled blocks Ã· wall time",
-               "seconds": round(dt, 2)}
+        fs, dt, ns, npi, t_full, strata = stratified_oracle(p, hnp, args.cpu_seconds)
+        cpu = {"value": round(fl_all["total"] / t_full / 1e12, 6), "unit": "Tflop/s", "cores": host_cores(),
+               "cpu_model": cpu_model(), "kind": "oracle",
+               "sample": f"stratified: {ns} Î£ blocks + {npi} Î  blocks of {args.config} in {dt:.1f} s "
+                         f"({len(strata)} strata); value = F_alg of the whole step Ã· the extrapolated full-oracle time",
+               "seconds": round(dt, 2), "extrapolated_full_oracle_s": round(t_full, 1),
+               "sample_rate_tflops": round(fs / dt / 1e12, 6), "strata": strata}
 
     if rank == 0:
+        f_paper = oracle_paper_flops(p)
         out = {"metric": METRIC if not fp32 else METRIC.replace("FP64 Tflop/s", "Tflop/s (FP32 mixed mode)"),
                "value": round(value, 3), "unit": "Tflop/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None,
                "dtype": "f64" if not fp32 else "f32-mixed (Î£ and Î  contractions tf32x3 on tcgen05, FP32 sandwiches; "
-                                               "FP64 inputs/outputs, Î  re-accumulated in FP64)",
+                                               "FP64 inputs/outputs, FP64 re-accumulation)",
                "data": "synthetic",
                "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
                                       f"NE={p.NE}, NÏ‰={p.Nw}, Nkz=Nqz={p.Nkz}",
                           "flops_per_step": flops_step,
-                          "parallelism": f"{'energy' if eshard else 'atom'}-shard x{world}",
+                          "parallelism": f"{args.shard}-shard Ta{info['Ta']} x TE{info['TE']}" if world > 1 else "1 GPU",
+                          "call": "qt_sse_halo_exchange + qt_sse_sigma + qt_sse_pi" if args.separate
+                                  else "qt_sse_sigma_pi (in-library halo + Î  reduction)",
                           "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (in_bytes / 1e9)},
+               "step_ms": {"median": round(med, 3), "ci95": [round(ci[0], 3), round(ci[1], 3)], "n": args.steps,
+                           "method": "bootstrap percentile CI of the median of per-step CUDA-event times (max over ranks)"},
+               "value_median": round(flops_step / (med * 1e-3) / 1e12, 3),
+               "paper_model_tflops": round(f_paper / (ms_step * 1e-3) / 1e12, 3),
+               "paper_model_note": "F_paper / t with the paper's DaCe SSE flop model (PAPER.md Â§5.1.1 P:756-764, "
+                                   "printed +1 form): %.1f Tflop per step vs F_alg %.1f" % (f_paper / 1e12, flops_step / 1e12),
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-               "halo_bytes_per_rank": info["halo_bytes"],
-               "comm_bytes_per_rank_per_step": info["halo_bytes"] + allreduce_bytes,
-               "clocks": clk, "pct_fp64_peak": None if fp32 else round(value / (FP64_PEAK_TFLOPS * world) * 100, 2)}
+               "halo_bytes_per_rank": info["halo_bytes"], "reduce_bytes_per_rank": info["reduce_bytes"],
+               "comm_bytes_per_rank_per_step": info["halo_bytes"] + info["reduce_bytes"],
+               "mem_bytes_per_rank": info["mem_bytes"],
+               "clocks": clk, "pct_fp64_peak": None if fp32 else round(value / (peak * world) * 100, 2)}
         print(json.dumps(out), file=out_stream, flush=True)
     plan.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def oracle_paper_flops(p):
+    """The paper's DaCe SSE flop model for this workload (reporting only; the formula lives in oracle/)."""
+    import oracle
+    return oracle.paper_flops_dace(p.Na, p.Nb, 3, p.Nkz, p.Nqz, p.NE, p.Nw, p.Norb)
 
 
 def run_reference(args, p, rank, world, out_stream=sys.stdout):
@@ -404,6 +564,7 @@ def run_reference(args, p, rank, world, out_stream=sys.stdout):
            "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
                                   f"NE={p.NE}, NÏ‰={p.Nw}, Nkz=Nqz={p.Nkz}"},
            "cpu_baseline": {"value": round(v, 6), "unit": "Tflop/s", "kind": "oracle", "cores": host_cores(),
+                            "cpu_model": cpu_model(),
                             "sample": f"per step {ns} Î£ blocks + ~{npi} Î  blocks (random); "
                                       f"{nsig} + {npis} blocks in {tt:.1f} s total"},
            "e2e": {"value": round(v, 6), "unit": "Tflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -19,21 +19,36 @@
  *   D≷, Π≷ : [Nqz][Nw][Na][Nb+1][3][3]      (slot 0 = self, slot s+1 = neighbour s)
  *   dH     : [Na][Nb][3][Norb][Norb]        dH[a][s][i] = ∇_i H_{a, nbr[a][s]}
  *   neighbors (host, int32): [Na][Nb], -1 = empty slot; must be symmetric.
- * With nranks > 1 and QT_SHARD_ATOM the G/D/Σ/Π/dH pointers hold the rank's LOCAL atom
- * window described by qt_sse_info (see qt_sse_query): atoms [w_lo, w_hi) for inputs
- * (owned atoms + neighbour halo), atoms [a_lo, a_hi) for outputs. With QT_SHARD_ENERGY (the
- * paper's T_E tiling) every rank holds all atoms; G≷ holds the energy window
- * [ew_lo, ew_hi) (owned energies ± Dmax), Σ≷ the owned energies [e_lo, e_hi), D≷/∇H are
- * replicated, and qt_sse_pi returns the full Π≷ on every rank (NCCL all-reduce of the
- * per-rank partial sums over energies). Energy sharding needs Norb <= 10.
  *
- * Ownership: the caller owns every tensor; outputs are OVERWRITTEN (never accumulated);
- * inputs are never modified. The plan owns its device workspace, work lists and
- * (nranks > 1) its NCCL communicator.
- * Execution: calls are stream-ordered and asynchronous on `stream`; argument and
- * launch errors are returned synchronously; asynchronous device faults surface as
- * QT_ERR_CUDA on a later call. No exceptions cross the ABI. One plan per host thread.
- * A plan is reusable with new tensor pointers of the same dimensions.
+ * Multi-GPU (nranks > 1): the ranks form a Ta x TE grid (the paper's Ta x TE tiling),
+ * rank = ta·TE + te. QT_SHARD_ATOM is Ta = nranks (TE = 1), QT_SHARD_ENERGY is TE = nranks (Ta = 1),
+ * QT_SHARD_2D takes Ta = desc.grid_atoms (TE = nranks / Ta). Rank (ta, te) owns the atoms
+ * [a_lo, a_hi) (slab ta of contiguous atoms balanced by pair count) and the energies [e_lo, e_hi)
+ * (slab te balanced by per-energy work), and every pointer holds the rank's LOCAL WINDOW
+ * (see qt_sse_query / qt_sse_shard_info):
+ *   G≷  : [Nkz][ew_hi-ew_lo][w_hi-w_lo][Norb][Norb]   owned block + halo (window atoms x window energies)
+ *   D≷  : [Nqz][Nw][w_hi-w_lo][Nb+1][3][3]            owned atoms + atom halo
+ *   dH  : [w_hi-w_lo][Nb][3][Norb][Norb]
+ *   Σ≷  : [Nkz][e_hi-e_lo][a_hi-a_lo][Norb][Norb]      owned block only
+ *   Π≷  : [Nqz][Nw][pa_hi-pa_lo][Nb+1][3][3]          Π sums over all energies: with TE > 1 the TE ranks of
+ *         an atom slab each own one sub-slab [pa_lo, pa_hi) of it and receive the sum of the slab's partial
+ *         sums by ncclReduce (overlapped with the next sub-slab's compute); a plan without a communicator
+ *         ("loopback": one process emulating a rank) returns this rank's PARTIAL sum over its own energies
+ *         for the whole atom slab, pa = [a_lo, a_hi).
+ * The window is the halo contract: the OWNED region of G≷/D≷ is input (read only); the HALO region
+ * (window entries owned by other ranks) is written by the library's NCCL exchange (qt_sse_sigma_pi and
+ * qt_sse_halo_exchange) before it is read. This keeps one G window per rank instead of an owned copy plus
+ * a second, library-owned window (the difference decides whether BASELINE cfg4/cfg5 fit).
+ *
+ * Ownership: the caller owns every tensor; outputs are OVERWRITTEN (never accumulated); apart from the
+ * halo region above, inputs are never modified. The plan owns its device workspace, work lists, halo
+ * staging, Π partial buffers, its communicators and its communication stream.
+ * Execution: calls are stream-ordered and asynchronous on `stream`; argument and launch errors are
+ * returned synchronously; asynchronous device faults surface as QT_ERR_CUDA and asynchronous NCCL
+ * failures (ncclCommGetAsyncError) as QT_ERR_NCCL on a later call or on qt_sse_query. Calls of one plan on
+ * different streams are ordered by the plan (each call waits for the previous one's completion event).
+ * No exceptions cross the ABI. One plan per host thread. A plan is reusable with new tensor pointers of the
+ * same dimensions.
  */
 #ifndef QT_SSE_H
 #define QT_SSE_H
@@ -45,8 +60,8 @@ extern "C" {
 
 typedef enum {
   QT_OK = 0,
-  QT_ERR_INVALID_ARG = 1,   /* bad dims, neighbour table, null/misaligned/aliased pointer */
-  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12 (> 10 in FP32 mode), shift_step != 1, Nω > 128 */
+  QT_ERR_INVALID_ARG = 1,   /* bad dims, neighbour table, grid, null/misaligned/aliased pointer          */
+  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12 (> 10 in FP32 mode or with TE > 1), Nω·shift_step > 128 (80)     */
   QT_ERR_OUT_OF_MEMORY = 3,
   QT_ERR_CUDA = 4,
   QT_ERR_NCCL = 5,
@@ -54,53 +69,74 @@ typedef enum {
 } qt_status;
 
 typedef enum { QT_PREC_FP64 = 0, QT_PREC_FP32_MIXED = 1 } qt_precision;
-typedef enum { QT_SHARD_NONE = 0, QT_SHARD_ENERGY = 1, QT_SHARD_ATOM = 2 } qt_shard;
+typedef enum { QT_SHARD_NONE = 0, QT_SHARD_ENERGY = 1, QT_SHARD_ATOM = 2, QT_SHARD_2D = 3 } qt_shard;
+
+/* desc.flags */
+#define QT_FLAG_DETERMINISTIC 1u   /* Σ neighbour sum in a fixed order (no floating-point atomics): the FP64 */
+                                   /* result is bitwise reproducible run to run; slower sandwich             */
 
 typedef struct {
-  int64_t Na, Nb, Norb, N3D, NE, Nw, Nkz, Nqz; /* paper symbols; N3D must be 3; Nkz == Nqz          */
-  int32_t shift0, shift_step;                  /* ħω_m/ΔE = shift0 + m·shift_step; shift0 ≥ 1        */
-  qt_precision precision;                      /* QT_PREC_FP64, or QT_PREC_FP32_MIXED (Norb <= 10): */
-                                               /* the Σ D-contraction on tcgen05 (kind::tf32, each */
-                                               /* operand split hi+lo, FP32 accumulation in TMEM,  */
-                                               /* ≤1e-5 per block for conditioned blocks); the ∇H  */
-                                               /* sandwiches and Π stay FP64 (SURVEY §8(f) NEXT(1),*/
-                                               /* PAPER.md §4.4)                         */
-  qt_shard shard;                              /* QT_SHARD_NONE, or with nranks > 1 QT_SHARD_ATOM  */
-                                               /* (default; fewer bytes moved) or QT_SHARD_ENERGY  */
+  int64_t Na, Nb, Norb, N3D, NE, Nw, Nkz, Nqz; /* paper symbols; N3D must be 3; Nkz == Nqz                    */
+  int32_t shift0, shift_step;                  /* ħω_m/ΔE = shift0 + m·shift_step; shift0, shift_step ≥ 1     */
+  qt_precision precision;                      /* QT_PREC_FP64, or QT_PREC_FP32_MIXED (Norb <= 10): both      */
+                                               /* contractions on tcgen05 (kind::tf32, operands split hi+lo,  */
+                                               /* FP32 products and TMEM segments re-accumulated in FP64), the */
+                                               /* ∇H sandwiches in FP32; ≤1e-5 per block (SURVEY §8(f)      */
+                                               /* NEXT(1), §4.4)                           */
+  qt_shard shard;                              /* QT_SHARD_NONE, or with nranks > 1 ATOM / ENERGY / 2D        */
   int32_t rank, nranks;
-  const void* nccl_unique_id;                  /* host ptr to a 128-byte ncclUniqueId (nranks > 1)  */
-  size_t workspace_limit;                      /* bytes of device scratch the plan may use; 0 = auto */
+  const void* nccl_unique_id;                  /* host ptr to a 128-byte ncclUniqueId (nranks > 1), or NULL:  */
+                                               /* loopback plan (no exchange, partial Π; see above)           */
+  size_t workspace_limit;                      /* bytes of device scratch the plan may use; 0 = auto          */
+  int32_t grid_atoms;                          /* QT_SHARD_2D: Ta (divides nranks); ignored otherwise         */
+  uint32_t flags;                              /* QT_FLAG_*                                                   */
 } qt_sse_desc;
 
 typedef struct qt_sse_plan_s* qt_sse_plan_t;
 
 typedef struct {
-  int64_t a_lo, a_hi;       /* atoms whose Σ/Π this rank computes (outputs)               */
-  int64_t w_lo, w_hi;       /* atom window of this rank's input tensors (owned + halo)    */
-  int64_t npairs;           /* valid (a,s) pairs with a in [a_lo,a_hi)                      */
-  size_t workspace_bytes;   /* device bytes owned by the plan                               */
-  double flops_sigma;       /* algorithmic FP64 flops of one qt_sse_sigma call (both X)     */
-  double flops_pi;          /* algorithmic FP64 flops of one qt_sse_pi call (both X)        */
-  double halo_bytes;        /* bytes received per call pair in the halo exchange            */
-  int64_t e_lo, e_hi;       /* output energies of this rank (all of [0, NE) unless energy-sharded)   */
+  int64_t a_lo, a_hi;       /* atoms whose Σ this rank computes (outputs)                              */
+  int64_t w_lo, w_hi;       /* atom window of this rank's input tensors (owned + halo)                 */
+  int64_t npairs;           /* valid (a,s) pairs with a in [a_lo,a_hi)                                  */
+  size_t workspace_bytes;   /* device bytes owned by the plan                                           */
+  double flops_sigma;       /* algorithmic FP64 flops of one qt_sse_sigma call (both X)                 */
+  double flops_pi;          /* algorithmic FP64 flops of one qt_sse_pi call (both X)                    */
+  double halo_bytes;        /* bytes received per exchange (G≷ + D≷ halo)                               */
+  int64_t e_lo, e_hi;       /* output energies of this rank                                             */
   int64_t ew_lo, ew_hi;     /* energy window of this rank's G inputs: [e_lo - Dmax, e_hi + Dmax) ∩ [0,NE) */
+  int64_t pa_lo, pa_hi;     /* atoms of this rank's Π output                                            */
+  int32_t Ta, TE, ta, te;   /* rank grid and this rank's coordinates                                    */
+  double reduce_bytes;      /* bytes this rank sends in the Π reduction per qt_sse_pi call              */
+  double mem_bytes;         /* device bytes per rank: caller tensors (window inputs, outputs) + plan    */
 } qt_sse_info;
 
-/* Validates desc + neighbours, builds the work lists, allocates the workspace. */
+/* Validates desc + neighbours, builds the work lists, allocates the workspace. With an NCCL unique id and
+ * nranks > 1 the call is collective over the ranks (creates the communicators). */
 qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* neighbors_host, void* cuda_stream,
                       qt_sse_plan_t* plan_out);
 
-/* Σ^<, Σ^> (Eq. 3). scale = complex ∫dħω/2π weight (default i·ΔE/2π, R8). */
+/* Σ^<, Σ^> (Eq. 3) from window inputs whose halo is already filled. scale = complex ∫dħω/2π weight
+ * (default i·ΔE/2π, R8). */
 qt_status qt_sse_sigma(qt_sse_plan_t plan, const void* dH, const void* G_less, const void* G_gtr,
                        const void* D_less, const void* D_gtr, double scale_re, double scale_im,
                        void* Sig_less, void* Sig_gtr, void* cuda_stream);
 
-/* Π^<, Π^> (Eq. 4). scale = complex ∫dE/2π weight (default -i·ΔE/2π, R8). */
+/* Π^<, Π^> (Eq. 4) from window inputs whose halo is already filled (TE > 1 with a communicator: the
+ * partial sums are reduced to the sub-slab owners). scale = complex ∫dE/2π weight (default -i·ΔE/2π). */
 qt_status qt_sse_pi(qt_sse_plan_t plan, const void* dH, const void* G_less, const void* G_gtr,
                     double scale_re, double scale_im, void* Pi_less, void* Pi_gtr, void* cuda_stream);
 
-/* End-to-end call on HOST buffers (pinned or pageable): copies inputs to device
- * buffers owned by the plan, runs qt_sse_sigma + qt_sse_pi, copies Σ≷, Π≷ back,
+/* The whole hot path in one call: halo exchange (nranks > 1 with a communicator)
+ * on the plan's communication stream, overlapped with the work that reads no halo entry (interior source
+ * atoms, owned-atom re-layout, coefficient tables); Σ≷ and Π≷ sharing one re-layout of G≷; the Π
+ * reduction (TE > 1) overlapped with the next sub-slab. Same results as halo_exchange + sigma + pi. */
+qt_status qt_sse_sigma_pi(qt_sse_plan_t plan, const void* dH, void* G_less, void* G_gtr, void* D_less,
+                          void* D_gtr, double sig_scale_re, double sig_scale_im, double pi_scale_re,
+                          double pi_scale_im, void* Sig_less, void* Sig_gtr, void* Pi_less, void* Pi_gtr,
+                          void* cuda_stream);
+
+/* End-to-end call on HOST buffers (pinned or pageable) holding the window inputs and the outputs:
+ * copies inputs to device buffers owned by the plan, runs qt_sse_sigma_pi, copies Σ≷, Π≷ back,
  * and synchronizes `cuda_stream` before returning. */
 qt_status qt_sse_execute_host(qt_sse_plan_t plan, const void* dH, const void* G_less, const void* G_gtr,
                               const void* D_less, const void* D_gtr, double sig_scale_re, double sig_scale_im,
@@ -109,28 +145,29 @@ qt_status qt_sse_execute_host(qt_sse_plan_t plan, const void* dH, const void* G_
 
 qt_status qt_sse_query(qt_sse_plan_t plan, qt_sse_info* out);
 
-/* Halo exchange (nranks > 1, plan created with an NCCL unique id — then qt_sse_plan is collective over
- * the ranks): fills the halo of the local input window from the owners with one grouped ncclSend/ncclRecv
- * round on `cuda_stream`: with QT_SHARD_ATOM the halo atoms of G≷ and D≷, with QT_SHARD_ENERGY the halo
- * energies of G≷ (D≷ is replicated and not touched). In-place on the caller's window buffers; only halo
- * entries are written, owned ones are only read. With QT_SHARD_ENERGY, qt_sse_pi also all-reduces Π≷ over
- * the ranks. Returns QT_ERR_UNSUPPORTED when the plan has no communicator, QT_ERR_NCCL on NCCL failure. */
+/* Halo exchange alone (nranks > 1 with a communicator): fills the halo region of the window buffers from
+ * their owners — G≷ boxes (window atoms x window energies owned by a peer) and, with Ta > 1, D≷ atom halos —
+ * with one grouped ncclSend/ncclRecv round on `cuda_stream` (energy-only splits send the contiguous energy
+ * ranges in place; atom splits pack). Owned entries are only read. QT_OK with nranks == 1;
+ * QT_ERR_UNSUPPORTED for a loopback plan; QT_ERR_NCCL on NCCL failure. */
 qt_status qt_sse_halo_exchange(qt_sse_plan_t plan, void* G_less, void* G_gtr, void* D_less, void* D_gtr,
                                void* cuda_stream);
 
 /* Writes a fresh 128-byte ncclUniqueId into out128 (call on one rank, broadcast to the others). */
 qt_status qt_sse_nccl_unique_id(void* out128);
 
-void qt_sse_destroy(qt_sse_plan_t plan);   /* NULL-safe; frees workspace (+ NCCL comm) */
+void qt_sse_destroy(qt_sse_plan_t plan);   /* NULL-safe; frees workspace, streams, events, NCCL comms */
 const char* qt_sse_status_string(qt_status s);
 
-/* Host-only (no device needed): algorithmic flop counts for desc + neighbours:
- * out[0] Σ contraction, out[1] Σ sandwich, out[2] Π sandwich, out[3] Π contraction
+/* Host-only (no device needed): algorithmic flop counts for desc + neighbours (the rank's share when
+ * nranks > 1): out[0] Σ contraction, out[1] Σ sandwich, out[2] Π sandwich, out[3] Π contraction
  * (both X, 8 real flops per complex multiply-add, in-window valid-pair work only). */
 qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* neighbors_host, double out[4]);
 
 /* Host-only (no device needed): the qt_sse_info a plan for desc (incl. rank/nranks) would report:
- * owned atoms, input window, valid pairs, flops, halo bytes received per exchange (workspace = 0). */
+ * owned atoms/energies, windows, Π sub-slab, pairs, flops, halo and reduction bytes, and mem_bytes, the
+ * device footprint per rank (caller window tensors + outputs + the plan's allocations for
+ * desc.workspace_limit, or the automatic workspace cap of min(48 GiB, Σ/Π scratch need) when 0). */
 qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* neighbors_host, qt_sse_info* out);
 
 /* Number of this library's kernel launches issued since load (for bench accounting). */

@@ -16,9 +16,10 @@ _HERE = Path(__file__).resolve().parent
 _LIB_PATH = _HERE / "libqtsse.so"
 
 QT_OK, QT_ERR_INVALID_ARG, QT_ERR_UNSUPPORTED, QT_ERR_OUT_OF_MEMORY, QT_ERR_CUDA, QT_ERR_NCCL, QT_ERR_INTERNAL = range(7)
-QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM = range(3)
+QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM, QT_SHARD_2D = range(4)
+QT_FLAG_DETERMINISTIC = 1
 QT_PREC_FP64, QT_PREC_FP32_MIXED = 0, 1
-EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
+EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_sigma_pi", "qt_sse_execute_host", "qt_sse_query",
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
             "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read", "qt_sse_nccl_unique_id",
             "qt_sse_shard_info"]
@@ -31,14 +32,18 @@ class Desc(ctypes.Structure):
                 ("NE", ctypes.c_int64), ("Nw", ctypes.c_int64), ("Nkz", ctypes.c_int64), ("Nqz", ctypes.c_int64),
                 ("shift0", ctypes.c_int32), ("shift_step", ctypes.c_int32), ("precision", ctypes.c_int),
                 ("shard", ctypes.c_int), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p), ("workspace_limit", ctypes.c_size_t)]
+                ("nccl_unique_id", ctypes.c_void_p), ("workspace_limit", ctypes.c_size_t),
+                ("grid_atoms", ctypes.c_int32), ("flags", ctypes.c_uint32)]
 
 
 class Info(ctypes.Structure):
     _fields_ = [("a_lo", ctypes.c_int64), ("a_hi", ctypes.c_int64), ("w_lo", ctypes.c_int64),
                 ("w_hi", ctypes.c_int64), ("npairs", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t),
                 ("flops_sigma", ctypes.c_double), ("flops_pi", ctypes.c_double), ("halo_bytes", ctypes.c_double),
-                ("e_lo", ctypes.c_int64), ("e_hi", ctypes.c_int64), ("ew_lo", ctypes.c_int64), ("ew_hi", ctypes.c_int64)]
+                ("e_lo", ctypes.c_int64), ("e_hi", ctypes.c_int64), ("ew_lo", ctypes.c_int64), ("ew_hi", ctypes.c_int64),
+                ("pa_lo", ctypes.c_int64), ("pa_hi", ctypes.c_int64), ("Ta", ctypes.c_int32), ("TE", ctypes.c_int32),
+                ("ta", ctypes.c_int32), ("te", ctypes.c_int32), ("reduce_bytes", ctypes.c_double),
+                ("mem_bytes", ctypes.c_double)]
 
 
 class QTError(RuntimeError):
@@ -54,6 +59,7 @@ def _load():
     lib.qt_sse_plan.argtypes = [ctypes.POINTER(Desc), P, P, ctypes.POINTER(P)]
     lib.qt_sse_sigma.argtypes = [P, P, P, P, P, P, D, D, P, P, P]
     lib.qt_sse_pi.argtypes = [P, P, P, P, D, D, P, P, P]
+    lib.qt_sse_sigma_pi.argtypes = [P, P, P, P, P, P, D, D, D, D, P, P, P, P, P]
     lib.qt_sse_execute_host.argtypes = [P, P, P, P, P, P, D, D, D, D, P, P, P, P, P]
     lib.qt_sse_query.argtypes = [P, ctypes.POINTER(Info)]
     lib.qt_sse_halo_exchange.argtypes = [P, P, P, P, P, P]
@@ -68,7 +74,7 @@ def _load():
     lib.qt_sse_shard_info.argtypes = [ctypes.POINTER(Desc), P, ctypes.POINTER(Info)]
     lib.qt_sse_timing_enable.argtypes = [P, I]
     lib.qt_sse_timing_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
-    for f in ("qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
+    for f in ("qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_sigma_pi", "qt_sse_execute_host", "qt_sse_query",
               "qt_sse_halo_exchange", "qt_sse_count_flops", "qt_sse_timing_enable", "qt_sse_timing_read",
               "qt_sse_nccl_unique_id", "qt_sse_shard_info"):
         getattr(lib, f).restype = I
@@ -98,10 +104,10 @@ def _check(rc: int, what: str) -> None:
 
 
 def make_desc(p, rank=0, nranks=1, shard=QT_SHARD_NONE, workspace_limit=0, unique_id=None,
-              precision=QT_PREC_FP64) -> Desc:
+              precision=QT_PREC_FP64, grid_atoms=0, flags=0) -> Desc:
     """Desc from a qtgen.Problem-like object (Na, Nb, Norb, NE, Nw, Nkz, Nqz, shift0, shift_step)."""
     return Desc(p.Na, p.Nb, p.Norb, 3, p.NE, p.Nw, p.Nkz, p.Nqz, p.shift0, p.shift_step, precision, shard, rank,
-                nranks, unique_id, workspace_limit)
+                nranks, unique_id, workspace_limit, grid_atoms, flags)
 
 
 def nccl_unique_id() -> bytes:
@@ -111,8 +117,9 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def count_flops(p) -> dict:
-    d = make_desc(p)
+def count_flops(p, rank=0, nranks=1, shard=QT_SHARD_NONE, grid_atoms=0) -> dict:
+    """Algorithmic flops (F_alg) of the whole problem, or of one rank's block."""
+    d = make_desc(p, rank=rank, nranks=nranks, shard=shard if nranks > 1 else QT_SHARD_NONE, grid_atoms=grid_atoms)
     out = (ctypes.c_double * 4)()
     nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
     _check(_get_lib().qt_sse_count_flops(ctypes.byref(d), nbr.ctypes.data, out), "qt_sse_count_flops")
@@ -120,12 +127,15 @@ def count_flops(p) -> dict:
                 total=sum(out))
 
 
-def shard_info(p, rank: int, nranks: int, shard=None) -> dict:
+def shard_info(p, rank: int, nranks: int, shard=None, grid_atoms=0, workspace_limit=0,
+               precision=QT_PREC_FP64) -> dict:
     """Host-only: owned atoms [a_lo,a_hi) / energies [e_lo,e_hi), input windows [w_lo,w_hi) / [ew_lo,ew_hi),
-    pairs, flops and halo bytes of a rank (atom sharding unless shard=QT_SHARD_ENERGY)."""
+    Π output atoms [pa_lo,pa_hi), grid (Ta, TE, ta, te), pairs, flops, halo and reduction bytes, and the
+    per-rank device footprint mem_bytes (atom sharding unless shard says otherwise)."""
     if shard is None:
         shard = QT_SHARD_ATOM if nranks > 1 else QT_SHARD_NONE
-    d = make_desc(p, rank=rank, nranks=nranks, shard=shard)
+    d = make_desc(p, rank=rank, nranks=nranks, shard=shard, grid_atoms=grid_atoms, workspace_limit=workspace_limit,
+                  precision=precision)
     i = Info()
     nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
     _check(_get_lib().qt_sse_shard_info(ctypes.byref(d), nbr.ctypes.data, ctypes.byref(i)), "qt_sse_shard_info")
@@ -150,11 +160,11 @@ class Plan:
     """Owns a qt_sse_plan_t (workspace, work lists) for one problem shape."""
 
     def __init__(self, p, stream=None, workspace_limit=0, rank=0, nranks=1, shard=QT_SHARD_NONE, unique_id=None,
-                 precision=QT_PREC_FP64):
+                 precision=QT_PREC_FP64, grid_atoms=0, flags=0):
         self._uid = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
         self.desc = make_desc(p, rank=rank, nranks=nranks, shard=shard, workspace_limit=workspace_limit,
                               unique_id=None if self._uid is None else ctypes.addressof(self._uid),
-                              precision=precision)
+                              precision=precision, grid_atoms=grid_atoms, flags=flags)
         self._nbr = np.ascontiguousarray(p.nbr, dtype=np.int32)
         h = ctypes.c_void_p()
         _check(_get_lib().qt_sse_plan(ctypes.byref(self.desc), self._nbr.ctypes.data, _stream(stream), ctypes.byref(h)),
@@ -174,6 +184,14 @@ class Plan:
         _check(_get_lib().qt_sse_pi(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), scale.real, scale.imag, _ptr(P_less),
                              _ptr(P_gtr), _stream(stream)), "qt_sse_pi")
 
+    def sigma_pi(self, dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr, sig_scale=1j, pi_scale=-1j,
+                 stream=None):
+        """The whole hot path in one call: halo exchange (sharded plans with a communicator) overlapped with the
+        interior work, Σ≷ and Π≷ (G/D window halos are filled in place)."""
+        _check(_get_lib().qt_sse_sigma_pi(self.h, _ptr(dH), _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
+                                          sig_scale.real, sig_scale.imag, pi_scale.real, pi_scale.imag, _ptr(S_less),
+                                          _ptr(S_gtr), _ptr(P_less), _ptr(P_gtr), _stream(stream)), "qt_sse_sigma_pi")
+
     def execute_host(self, dH, G_less, G_gtr, D_less, D_gtr, S_less, S_gtr, P_less, P_gtr, sig_scale=1j,
                      pi_scale=-1j, stream=None):
         """End-to-end on host buffers (numpy / pinned torch CPU tensors)."""
@@ -183,7 +201,7 @@ class Plan:
                "qt_sse_execute_host")
 
     def halo_exchange(self, G_less, G_gtr, D_less, D_gtr, stream=None):
-        """Fill the halo atoms of this rank's input window from their owners (NCCL, in place)."""
+        """Fill the halo region of this rank's input windows from their owners (NCCL, in place)."""
         _check(_get_lib().qt_sse_halo_exchange(self.h, _ptr(G_less), _ptr(G_gtr), _ptr(D_less), _ptr(D_gtr),
                                                _stream(stream)), "qt_sse_halo_exchange")
 
@@ -209,18 +227,24 @@ class Plan:
             pass
 
 
-def run(p, t: dict, sig_scale=1j, pi_scale=-1j, plan: Plan | None = None, precision=QT_PREC_FP64):
-    """Σ≷, Π≷ for device inputs t (dict of complex128 CUDA tensors as made by qtgen.dev_inputs)."""
+def run(p, t: dict, sig_scale=1j, pi_scale=-1j, plan: Plan | None = None, precision=QT_PREC_FP64, fused=False,
+        workspace_limit=0, flags=0):
+    """Σ≷, Π≷ for device inputs t (dict of complex128 CUDA tensors as made by qtgen.dev_inputs); separate
+    qt_sse_sigma + qt_sse_pi calls, or the fused qt_sse_sigma_pi."""
     import torch
     own = plan is None
-    plan = Plan(p, precision=precision) if own else plan
+    plan = Plan(p, precision=precision, workspace_limit=workspace_limit, flags=flags) if own else plan
     sh = p.shapes()
     out = dict(S_less=torch.empty(sh["G"], dtype=torch.complex128, device="cuda"),
                S_gtr=torch.empty(sh["G"], dtype=torch.complex128, device="cuda"),
                P_less=torch.empty(sh["D"], dtype=torch.complex128, device="cuda"),
                P_gtr=torch.empty(sh["D"], dtype=torch.complex128, device="cuda"))
-    plan.sigma(t["dH"], t["G_less"], t["G_gtr"], t["D_less"], t["D_gtr"], out["S_less"], out["S_gtr"], sig_scale)
-    plan.pi(t["dH"], t["G_less"], t["G_gtr"], out["P_less"], out["P_gtr"], pi_scale)
+    if fused:
+        plan.sigma_pi(t["dH"], t["G_less"], t["G_gtr"], t["D_less"], t["D_gtr"], out["S_less"], out["S_gtr"],
+                      out["P_less"], out["P_gtr"], sig_scale, pi_scale)
+    else:
+        plan.sigma(t["dH"], t["G_less"], t["G_gtr"], t["D_less"], t["D_gtr"], out["S_less"], out["S_gtr"], sig_scale)
+        plan.pi(t["dH"], t["G_less"], t["G_gtr"], out["P_less"], out["P_gtr"], pi_scale)
     if own:
         torch.cuda.synchronize()
         plan.close()

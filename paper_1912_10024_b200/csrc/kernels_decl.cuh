@@ -12,7 +12,7 @@ struct CoefArgs {
   const int32_t* pair_item;
   double2* coef;
   int64_t npairs, Nw, Nwin, Nb, Nqz, DWp;
-  int Dmax, shift0;
+  int Dmax, shift0, step;   // shifts s_m = shift0 + m·step; other |d| in the window get zero coefficients
   // tiled layout (TMA path): [item - item0][q][dc][72 rows (t,ij)][kCoefKCP], d = 16*dc + k - Dmax
   bool tiled;
   int64_t item0, nitems, ndc, Dwin;
@@ -26,9 +26,8 @@ struct CoefArgs {
 constexpr int kCoefKCP = QT_SIG_CSUM ? 28 : 20;
 
 struct SigmaArgs {
-  const double2* G;      // G^X, paper layout [Nkz][NE][Nwin][NN]
-  const double2* Gam;    // G^X, atom-major copy [Nwin][Nkz][NE][NN] (TMA path)
-  const double* Gsum;    // Re + Im of Gam (same layout, doubles)
+  const double2* G;      // G^X window, paper layout [Nkz][NE][Nwin][NN] (TMA boxes read it in place)
+  const double* Gsum;    // Re + Im of G^X, atom-major [Nwin][Nkz][NE][NN rounded up to even] (k_relayout)
   const double2* coef;   // coefficient table of the current chunk: pair index p - cp0
   const double2* dH;
   const SigItem* items;
@@ -44,8 +43,7 @@ struct SigmaArgs {
 };
 
 struct PiWArgs {
-  const double2* GY;
-  const double2* GYam;        // G^Y atom-major [Nwin][Nkz][NE][NN]
+  const double2* GY;          // G^Y window, paper layout [Nkz][NE][Nwin][NN]
   const double2* dH;
   const PiPair* pairs;
   const PiItem* items;
@@ -57,8 +55,8 @@ struct PiWArgs {
 };
 
 struct PiCArgs {
-  const double2* GX;     // G^X atom-major [Nwin][Nkz][NE][NN]
-  const double* GXsum;   // Re + Im of GX, row stride NN rounded up to even
+  const double2* GX;     // G^X window, paper layout [Nkz][NE][Nwin][NN]
+  const double* GXsum;   // Re + Im of G^X, atom-major [Nwin][Nkz][NE][NN rounded up to even]
   const double2* W;
   const PiItem* items;
   const PiPair* pairs;
@@ -66,6 +64,8 @@ struct PiCArgs {
   double2 scale;
   int64_t i0, nitems, Nwin, Nout, Nb;
   int NE, Nkz, Nqz, h, NN, Nw, NWP, shift0;
+  int NWv, step;         // GEMM columns = every shift shift0 + c (c < NWv); column c is frequency m = c / step
+                         // when c % step == 0 (shift_step > 1: the other columns are computed and dropped)
   int E0, NEo;           // energies of this rank's Π sum: window energies [E0, E0 + NEo)
 };
 
@@ -89,7 +89,7 @@ constexpr int kTcPiPairs = 14;   // FP32-mode Π items: <= 14 pairs of one desti
 constexpr int kTcPiRows = 128;
 constexpr int kTcRowsA = 128;   // G plane rows (Norb² padded to the UMMA M)
 cudaError_t launch_relayout_tc(const double2* G, float* out, int64_t Nkz, int64_t NE, int64_t NEp, int64_t Nwin, int NN,
-                               cudaStream_t st);
+                               int64_t a0, int64_t a1, cudaStream_t st);
 cudaError_t launch_sigma_coef_tc(const CoefArgs& a, int Kp, cudaStream_t st);
 cudaError_t launch_relayout_pi_tc(const double2* G, float* out, int64_t Nkz, int64_t NE, int64_t Epad, int64_t Nwin, int NN,
                                   int NNp, cudaStream_t st);
@@ -101,8 +101,9 @@ cudaError_t launch_sigma_tc(const SigmaArgs& a, const float* Gtp, int64_t NEp, c
 cudaError_t launch_pi_w(const PiWArgs& a, int64_t npairs_chunk, cudaStream_t st);
 cudaError_t launch_pi_contract(const PiCArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_pi_self(const PiSelfArgs& a, cudaStream_t st);
-// G [Nkz][NE][Nwin][NN] (paper layout) -> [Nwin][Nkz][NE][NN] (atom-major: every TMA box contiguous)
-cudaError_t launch_relayout(const double2* in, double2* out, double* osum, int64_t Nkz, int64_t NE, int64_t Nwin,
-                            int64_t NN, cudaStream_t st);
+// Re + Im of G [Nkz][NE][Nwin][NN] (paper layout) for window atoms [a0, a1) -> osum [Nwin][Nkz][NE][NN even]
+// (the B-side sums of the Gauss 3M products, so the DMMA consumers issue no FP64 adds)
+cudaError_t launch_relayout(const double2* in, double* osum, int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN,
+                            int64_t a0, int64_t a1, cudaStream_t st);
 
 }  // namespace qt

@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(kWThreads, 512 / kWThreads) k_pi_w(PiWArgs A) 
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      cp_async16(dst + t * kWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + A.E0 + e0) * NN + rem, true);
+      const int e = rem / NN, uv = rem - e * NN;
+      cp_async16(dst + t * kWE * NN + rem, A.GY + (((int64_t)kz * A.NE + A.E0 + e0 + e) * A.Nwin + b_in) * NN + uv, true);
     }
     cp_async_commit();
   };
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
         const int64_t woff = ((((int64_t)il * A.Nkz + kz) * nxc + xc) * A.NEo + ec * C::EC) * kRows * C::XC;
         bulk_load(ws, A.W + woff, C::W_STAGE * 16, &full[slot]);
-        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, A.E0 + ec * C::EC + A.shift0, k2, item.a_in, &full[slot]);
+        tma_load_4d(ws + C::W_STAGE, &tmG, 2 * xc * C::XC, item.a_in, A.E0 + ec * C::EC + A.shift0, k2, &full[slot]);
         tma_load_4d(ws + C::W_STAGE + T::G_STAGE, &tmGS, xc * C::XC, A.E0 + ec * C::EC + A.shift0, k2, item.a_in,
                     &full[slot]);
         if (++ec == nec) {
@@ -300,11 +301,13 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
 #pragma unroll
         for (int f = 0; f < T::NF0; ++f) {
           if (f < nfw) {
-            const int m0 = (f0 + 2 * f) * 8 + 2 * (lane & 3);
-            if (m0 < A.Nw)
-              A.Pi[((int64_t)qz * A.Nw + m0) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(0));
-            if (m0 + 1 < A.Nw)
-              A.Pi[((int64_t)qz * A.Nw + m0 + 1) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(1));
+            const int c0 = (f0 + 2 * f) * 8 + 2 * (lane & 3);   // shift columns c0, c0 + 1 (shift0 + c)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int c = c0 + k, m = c / A.step;
+              if (c < A.NWv && c == m * A.step)
+                A.Pi[((int64_t)qz * A.Nw + m) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(k));
+            }
           }
         }
       }
@@ -318,12 +321,8 @@ cudaError_t make_tmap_f64(CUtensorMap* m, const void* base, int rank, const uint
 template <int NFM>
 static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
   using T = PiTma<NFM>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_pi_contract<NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t ea = cudaFuncSetAttribute(k_pi_contract<NFM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM);
+  if (ea != cudaSuccess) return ea;
   const uint64_t NN = (uint64_t)a.NN;
   CUtensorMap tmG, tmGS;
   {
@@ -334,10 +333,10 @@ static cudaError_t launch_pi_nfm(const PiCArgs& a, cudaStream_t st) {
     cudaError_t e = make_tmap_f64(&tmGS, a.GXsum, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
-  {
-    const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
-    const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
-    const uint32_t box[4] = {2 * PiCfg::XC, (uint32_t)T::GROWS, 1, 1};
+  {   // G^X window in the paper layout [Nkz][NE][Nwin][NN]: box = the GROWS-energy Hankel window of one atom
+    const uint64_t dims[4] = {2 * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
+    const uint64_t strides[3] = {NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
+    const uint32_t box[4] = {2 * PiCfg::XC, 1, (uint32_t)T::GROWS, 1};
     cudaError_t e = make_tmap_f64(&tmG, a.GX, 4, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
@@ -422,13 +421,11 @@ cudaError_t launch_pi_w(const PiWArgs& a, int64_t nitems_chunk, cudaStream_t st)
   }
 }
 
-// one CTA per (atom, kz): copies the NE x NN block of that atom into its contiguous atom-major slot
-// also writes osum = Re + Im (the B-side sum of the Gauss 3M product, so consumers need no DADD)
-__global__ void __launch_bounds__(256) k_relayout(const double2* __restrict__ in, double2* __restrict__ out,
-                                                  double* __restrict__ osum, int64_t Nkz, int64_t NE, int64_t Nwin,
-                                                  int64_t NN) {
-  const int64_t a = blockIdx.x / Nkz, kz = blockIdx.x % Nkz;
-  double2* o = out + (a * Nkz + kz) * NE * NN;
+// one CTA per (window atom, kz): Re + Im of the NE x NN block of G^X (paper layout) into the atom-major sum plane
+// (the B-side sum of the Gauss 3M product, so the DMMA consumers need no DADD); atoms a0 + blockIdx / Nkz
+__global__ void __launch_bounds__(256) k_relayout(const double2* __restrict__ in, double* __restrict__ osum, int64_t Nkz,
+                                                  int64_t NE, int64_t Nwin, int64_t NN, int64_t a0) {
+  const int64_t a = a0 + blockIdx.x / Nkz, kz = blockIdx.x % Nkz;
   const int64_t NS = (NN + 1) & ~int64_t(1);   // sum-plane row stride: even, so TMA strides are 16-byte multiples
   double* os = osum + (a * Nkz + kz) * NE * NS;
   const double2* src = in + (kz * NE * Nwin + a) * NN;
@@ -436,15 +433,14 @@ __global__ void __launch_bounds__(256) k_relayout(const double2* __restrict__ in
   for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
     const int64_t e = idx / NN, uv = idx - e * NN;
     const double2 v = __ldg(src + e * Nwin * NN + uv);
-    o[idx] = v;
     os[e * NS + uv] = v.x + v.y;
   }
 }
 
-cudaError_t launch_relayout(const double2* in, double2* out, double* osum, int64_t Nkz, int64_t NE, int64_t Nwin,
-                            int64_t NN, cudaStream_t st) {
-  if (Nkz * Nwin == 0) return cudaSuccess;
-  k_relayout<<<(unsigned)(Nkz * Nwin), 256, 0, st>>>(in, out, osum, Nkz, NE, Nwin, NN);
+cudaError_t launch_relayout(const double2* in, double* osum, int64_t Nkz, int64_t NE, int64_t Nwin, int64_t NN, int64_t a0,
+                            int64_t a1, cudaStream_t st) {
+  if (Nkz * (a1 - a0) <= 0) return cudaSuccess;
+  k_relayout<<<(unsigned)(Nkz * (a1 - a0)), 256, 0, st>>>(in, osum, Nkz, NE, Nwin, NN, a0);
   return cudaGetLastError();
 }
 

@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kTWThreads, 512 / kTWThreads) k_pi_w_tc(PiWArg
     for (int idx = threadIdx.x; idx < P * ne * NN; idx += blockDim.x) {
       const int t = idx / (ne * NN), rem = idx - t * ne * NN;
       const int b_in = A.pairs[it.pair0 + t0 + t].b_in;
-      cp_async16(dst + t * kTWE * NN + rem, A.GYam + (((int64_t)b_in * A.Nkz + kz) * A.NE + A.E0 + e0) * NN + rem, true);
+      const int e = rem / NN, uv = rem - e * NN;
+      cp_async16(dst + t * kTWE * NN + rem, A.GY + (((int64_t)kz * A.NE + A.E0 + e0 + e) * A.Nwin + b_in) * NN + uv, true);
     }
     cp_async_commit();
   };
@@ -240,6 +241,7 @@ struct PiTcArgs {
   double2 scale;
   int64_t ntiles, Nout, Nb;
   int NE, Nkz, Nqz, h, Nw, shift0, NNp, nch;   // nch = K-chunks per kz
+  int NWv, step;                                // shift columns c < NWv; column c is frequency c / step if c % step == 0
   int E0, NEo;                                  // this rank's energies: window [E0, E0 + NEo)
 };
 
@@ -384,8 +386,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int64_t mstride = A.Nout * (A.Nb + 1) * 9;
 #pragma unroll
         for (int i = 0; i < kPCols; ++i) {
-          const int m = cg * kPCols + i;
-          if (m < A.Nw)
+          const int c = cg * kPCols + i, m = c / A.step;
+          if (c < A.NWv && c == m * A.step)
             A.Pi[((int64_t)qz * A.Nw + m) * mstride + base] =
                 make_double2(A.scale.x * ar[i] - A.scale.y * ai[i], A.scale.x * ai[i] + A.scale.y * ar[i]);
         }
@@ -407,13 +409,9 @@ cudaError_t make_tmap_f32_sw128(CUtensorMap* m, const void* base, int rank, cons
 // Wp: [nitems][4][128][Kw] (Kw = Nkz·NE·NNp); Gp: [Nwin][Nkz][4][Epad][NNp].
 cudaError_t launch_pi_contract_tc(const PiCArgs& a, const float* Wp, const float* Gp, int64_t Epad, int NNp, int64_t nitems,
                                   cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_pi_contract_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  if (a.Nw > kPN || nitems == 0) return a.Nw > kPN ? cudaErrorInvalidValue : cudaSuccess;
+  cudaError_t ea = cudaFuncSetAttribute(k_pi_contract_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
+  if (ea != cudaSuccess) return ea;
+  if (a.NWv > kPN || nitems == 0) return a.NWv > kPN ? cudaErrorInvalidValue : cudaSuccess;
   const int KwB = ((a.NEo * NNp + kPKC - 1) / kPKC) * kPKC;
   const uint64_t Kw = (uint64_t)a.Nkz * KwB;
   CUtensorMap tmA, tmB;
@@ -448,17 +446,16 @@ cudaError_t launch_pi_contract_tc(const PiCArgs& a, const float* Wp, const float
   p.h = a.h;
   p.Nw = a.Nw;
   p.shift0 = a.shift0;
+  p.NWv = a.NWv;
+  p.step = a.step;
   p.NNp = NNp;
   // chunks per kz: energies E < NE - shift0 have in-window terms (R7)
   p.E0 = a.E0;
   p.NEo = a.NEo;
   p.nch = KwB / kPKC;   // every chunk of the kz block: the W tail past NEo·NNp is zero, energies past NE read zero G rows
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(p.ntiles, nsm);
   k_pi_contract_tc<<<(unsigned)grid, kPThreads, kPSmem, st>>>(tmA, tmB, p);
   return cudaGetLastError();

@@ -27,8 +27,8 @@ __global__ void k_sigma_coef(CoefArgs A) {
     int64_t d = dd - A.Dmax;
     double2 v = make_double2(0.0, 0.0);
     int64_t ad = d < 0 ? -d : d;
-    if (ad >= A.shift0 && ad <= A.Dmax) {
-      int64_t m = ad - A.shift0;
+    if (ad >= A.shift0 && ad <= A.Dmax && (ad - A.shift0) % A.step == 0) {
+      int64_t m = (ad - A.shift0) / A.step;
       // absorption (E - ħω): Dc^X_{ij}; emission (E + ħω): Dc^Y_{ji} (reading R3)
       const double2* D = d < 0 ? A.DX : A.DY;
       int e = d < 0 ? ij : (ij % 3) * 3 + ij / 3;
@@ -213,12 +213,8 @@ cudaError_t launch_sigma_coef(const CoefArgs& a, cudaStream_t st) {
 template <int NF>
 static cudaError_t launch_sigma_nf(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
   using C = SigmaCfg<NF>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sigma_cp<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t ea = cudaFuncSetAttribute(k_sigma_cp<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (ea != cudaSuccess) return ea;
   int64_t nblk = nitems * a.NE * a.Nkz;
   if (nblk == 0) return cudaSuccess;
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidConfiguration;

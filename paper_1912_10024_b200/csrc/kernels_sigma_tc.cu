@@ -56,9 +56,10 @@ __device__ __forceinline__ void split3(double x, float& hi, float& lo) {
 // (re_hi, re_lo, im_hi, im_lo); rows rc >= NN and energies >= NE are zero (every TMA box lies inside
 // the tensor: NEp >= 32 and 128 rows).
 __global__ void __launch_bounds__(256) k_relayout_tc(const double2* __restrict__ G, float* __restrict__ out,
-                                                     int64_t Nkz, int64_t NE, int64_t NEp, int64_t Nwin, int NN) {
+                                                     int64_t Nkz, int64_t NE, int64_t NEp, int64_t Nwin, int NN,
+                                                     int64_t a0) {
   __shared__ float tile[4][32][33];
-  const int64_t a = blockIdx.x / Nkz, kz = blockIdx.x % Nkz;
+  const int64_t a = a0 + blockIdx.x / Nkz, kz = blockIdx.x % Nkz;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
   float* o = out + (a * Nkz + kz) * 4 * (int64_t)kTcRowsA * NEp;
   for (int64_t e0 = 0; e0 < NEp; e0 += 32) {
@@ -91,9 +92,9 @@ __global__ void __launch_bounds__(256) k_relayout_tc(const double2* __restrict__
 }
 
 cudaError_t launch_relayout_tc(const double2* G, float* out, int64_t Nkz, int64_t NE, int64_t NEp, int64_t Nwin, int NN,
-                               cudaStream_t st) {
-  if (Nkz * Nwin == 0) return cudaSuccess;
-  k_relayout_tc<<<(unsigned)(Nkz * Nwin), 256, 0, st>>>(G, out, Nkz, NE, NEp, Nwin, NN);
+                               int64_t a0, int64_t a1, cudaStream_t st) {
+  if (Nkz * (a1 - a0) <= 0) return cudaSuccess;
+  k_relayout_tc<<<(unsigned)(Nkz * (a1 - a0)), 256, 0, st>>>(G, out, Nkz, NE, NEp, Nwin, NN, a0);
   return cudaGetLastError();
 }
 
@@ -123,9 +124,9 @@ __global__ void k_sigma_coef_tc(CoefArgs A, int Kp) {
     double2 c = make_double2(0.0, 0.0);
     if (t < item.npair && d < A.Dwin) {
       const int64_t dd = d - A.Dmax, ad = dd < 0 ? -dd : dd;
-      if (ad >= A.shift0 && ad <= A.Dmax) {
+      if (ad >= A.shift0 && ad <= A.Dmax && (ad - A.shift0) % A.step == 0) {
         const SigPair pr = A.pairs[item.pair0 - pp0 + t];
-        const int64_t b = item.b_in, m = ad - A.shift0, ns = A.Nb + 1;
+        const int64_t b = item.b_in, m = (ad - A.shift0) / A.step, ns = A.Nb + 1;
         const double2* D = dd < 0 ? A.DX : A.DY;
         const int e = dd < 0 ? ij : (ij % 3) * 3 + ij / 3;
         const int64_t base = (q * A.Nw + m) * A.Nwin;
@@ -356,12 +357,8 @@ cudaError_t make_tmap_f32_sw128(CUtensorMap* m, const void* base, int rank, cons
 // Gtp: [Nwin][Nkz][4][128][NEp] fp32; coef: [nitems][Nqz][4 delays][4 planes][80][Kp] fp32.
 cudaError_t launch_sigma_tc(const SigmaArgs& a, const float* Gtp, int64_t NEp, const float* coef, int Kp, int64_t nitems,
                             cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sigma_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t ea = cudaFuncSetAttribute(k_sigma_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+  if (ea != cudaSuccess) return ea;
   if (a.NN > kTcM || NEp < kTcKC || Kp < kTcKC || (Kp & 31)) return cudaErrorInvalidValue;
   CUtensorMap tmA, tmB;
   {
@@ -383,12 +380,9 @@ cudaError_t launch_sigma_tc(const SigmaArgs& a, const float* Gtp, int64_t NEp, c
   SigmaArgs b = a;
   b.ntiles = nitems * a.Nkz * a.NEo;
   if (b.ntiles == 0) return cudaSuccess;
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(b.ntiles, nsm);
   k_sigma_tc<<<(unsigned)grid, 192, kTcSmem, st>>>(tmA, tmB, b);
   return cudaGetLastError();

@@ -4,10 +4,10 @@
 // Same GEMM as kernels_sigma.cu (rows (pair t, ij): 72 = 9 DMMA m-fragments; columns rc = Norb²;
 // K = (q, d) with a Hankel G_b operand), reorganized so that the FP64 tensor pipe never waits on
 // block-wide barriers or address arithmetic:
-//   warp 18          : producer. One elected lane issues, per stage, two cp.async.bulk.tensor loads:
-//                      the G_b rows E-Dmax+d0 .. +KC from the atom-major copy of G (one contiguous block;
-//                      TMA zero-fills rows outside [0,NE): reading R7,
-//                      and the padding columns Norb²..NPS) and the 72 x KCP coefficient tile.
+//   warp 18          : producer. One elected lane issues, per stage, three bulk loads: the G_b rows
+//                      E-Dmax+d0 .. +KC straight from the caller's G window in the paper layout (a 4-D box of
+//                      one atom x KC energies; TMA zero-fills rows outside [0,NE): reading R7, and the padding
+//                      columns Norb²..NPS), the same rows of the Re+Im plane, and the 72 x KCP coefficient tile.
 //   warps 0..17      : consumers. Warp w owns m-fragment w%9 and half of the n-fragments; it waits on the
 //                      stage's `full` mbarrier, runs DMMA.8x8x4, and releases the stage on `empty`.
 // Epilogue (all warps): Gt -> smem, V^i = Σ_j Gt^{ij} ∇_jH_{br}, S = Σ_i ∇_iH_{as} V^i, Σ_a += scale·S.
@@ -49,9 +49,9 @@ __global__ void k_sigma_coef_tiled(CoefArgs A) {
     double2 c = make_double2(0.0, 0.0);
     if ((k < 16 || is_sum) && t < item.npair && dd < A.Dwin) {
       const int64_t d = dd - A.Dmax, ad = d < 0 ? -d : d;
-      if (ad >= A.shift0 && ad <= A.Dmax) {
+      if (ad >= A.shift0 && ad <= A.Dmax && (ad - A.shift0) % A.step == 0) {
         const SigPair pr = A.pairs[item.pair0 - pp0 + t];
-        const int64_t b = item.b_in, m = ad - A.shift0, ns = A.Nb + 1;
+        const int64_t b = item.b_in, m = (ad - A.shift0) / A.step, ns = A.Nb + 1;
         const double2* D = d < 0 ? A.DX : A.DY;
         const int e = d < 0 ? ij : (ij % 3) * 3 + ij / 3;
         const int64_t base = (q * A.Nw + m) * A.Nwin;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
           const int soff = multi ? C::G_STAGE_M : C::G_STAGE;
           const int coff = soff + (multi ? C::S_STAGE_M : C::S_STAGE);
           const int r0 = T.E - A.Dmax + dc * C::KC;
-          tma_load_4d(gs, multi ? &tmGm : &tmG, T.ch * C::NFH0 * 16, r0, kp, T.item.b_in, &full[slot]);
+          tma_load_4d(gs, multi ? &tmGm : &tmG, T.ch * C::NFH0 * 16, T.item.b_in, r0, kp, &full[slot]);
           tma_load_4d(gs + soff, multi ? &tmSm : &tmS, T.ch * C::NFH0 * 8, r0, kp, T.item.b_in, &full[slot]);
           bulk_load(gs + coff, A.coef + (((int64_t)T.il * A.Nqz + q) * A.ndc + dc) * C::C_STAGE,
                     (multi ? T.F * 8 : kRows) * C::KCP * 16, &full[slot]);
@@ -426,21 +426,18 @@ cudaError_t make_tmap_f64(CUtensorMap* m, const void* base, int rank, const uint
 template <int NF>
 static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
   using C = SigTmaCfg<NF>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sigma<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  // function attributes are per device context: set on every launch (cheap) instead of once per process
+  cudaError_t ea = cudaFuncSetAttribute(k_sigma<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (ea != cudaSuccess) return ea;
   CUtensorMap tmG, tmS, tmGm, tmSm;
   const uint64_t NN = (uint64_t)a.NN;
   for (int m = 0; m < 2; ++m) {
     const uint32_t rows = m ? C::GROWS_M : C::KC;
-    {
-      const uint64_t dims[4] = {2 * NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
-      const uint64_t strides[3] = {NN * 16, (uint64_t)a.NE * NN * 16, (uint64_t)a.Nkz * a.NE * NN * 16};
-      const uint32_t box[4] = {2 * C::NPS, rows, 1, 1};
-      cudaError_t e = make_tmap_f64(m ? &tmGm : &tmG, a.Gam, 4, dims, strides, box);
+    {   // G^X window in the paper layout [Nkz][NE][Nwin][NN]: box = KC (or GROWS) energies of one atom
+      const uint64_t dims[4] = {2 * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
+      const uint64_t strides[3] = {NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
+      const uint32_t box[4] = {2 * C::NPS, 1, rows, 1};
+      cudaError_t e = make_tmap_f64(m ? &tmGm : &tmG, a.G, 4, dims, strides, box);
       if (e != cudaSuccess) return e;
     }
     {
@@ -455,12 +452,9 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
   SigmaArgs b = a;
   b.ntiles = nitems * a.NEo * a.Nkz * 2;
   if (b.ntiles == 0) return cudaSuccess;
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(b.ntiles, nsm) & ~int64_t(1);   // even: sig_tile pairs t = 2u, 2u+1 in one round
   k_sigma<NF><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmS, tmGm, tmSm, b);
   return cudaGetLastError();

@@ -1,5 +1,6 @@
-// qt_sse.cu — C ABI of libqtsse.so (include/qt_sse.h): plan validation, work lists,
-// workspace, and the stream-ordered kernel sequence for Σ≷ (Eq. 3) and Π≷ (Eq. 4).
+// qt_sse.cu — C ABI of libqtsse.so (include/qt_sse.h): plan validation, the Ta x TE rank grid, work lists,
+// workspace, halo exchange and Π reduction scheduling, and the stream-ordered kernel sequence for Σ≷ (Eq. 3,
+// PAPER.md P:355-365) and Π≷ (Eq. 4).
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -18,108 +19,58 @@ using namespace qt;
 
 static std::atomic<uint64_t> g_launches{0};
 
-struct qt_sse_plan_s {
-  qt_sse_desc d{};
-  int64_t NN = 0, h = 0, Dmax = 0, Dwin = 0, DWp = 0, NWP = 0;
-  int64_t a_lo = 0, a_hi = 0, w_lo = 0, w_hi = 0, Nwin = 0, Nout = 0;
-  std::vector<int32_t> nbr;          // global [Na][Nb]
-  std::vector<int32_t> nbr_win;      // window [Nwin][Nb] (local indices, -1 outside/empty)
-  // device
-  int32_t* d_nbr_win = nullptr;
-  SigItem* d_sig_items = nullptr;
-  SigPair* d_sig_pairs = nullptr;
-  int32_t* d_sig_pair_item = nullptr;
-  PiItem* d_pi_items = nullptr;
-  PiPair* d_pi_pairs = nullptr;
-  int32_t* d_pi_pair_item = nullptr;
-  std::vector<SigItem> sig_items;
-  std::vector<PiItem> pi_items;
-  int64_t n_sig_pairs = 0, n_pi_pairs = 0;
-  // chunks: item ranges [lo, hi) and their pair ranges
-  std::vector<int64_t> sig_chunks, pi_chunks;   // item boundaries
-  double2* ws = nullptr;
-  size_t ws_bytes = 0;
-  double2* ws_g = nullptr;      // atom-major copies of G^<, G^> [2][Nwin][Nkz][NE][NN]
-  double* ws_gs = nullptr;      // their Re + Im planes [2][Nwin][Nkz][NE][NN rounded up to even]
-  bool fp32 = false;            // QT_PREC_FP32_MIXED: Σ contraction on tcgen05 (kind::tf32, 3xTF32 split)
-  float* ws_gtp = nullptr;      // FP32 mode: split G planes [2][Nwin][Nkz][4][NN][NEp]
-  float* ws_gpi = nullptr;      // FP32 mode: split G^X planes for Π [Nwin][Nkz][4][Epad][NNp] (one X at a time)
-  int64_t Epad = 0, NNp = 0;
-  int64_t sig_rows = kRows;     // Gt rows per (item, kz, E): 72, or 128 in FP32 mode (items of <= 14 pairs)
-  // energy window of this rank's inputs [ew_lo, ew_hi) (NEw energies; all of [0, NE) unless energy-sharded)
-  // and its output energies [e_lo, e_hi) = window energies [E0, E0 + NEo)
-  int64_t e_lo = 0, e_hi = 0, ew_lo = 0, ew_hi = 0, NEw = 0, NEo = 0, E0 = 0;
-  bool eshard = false;
-  size_t gpi_elems() const { return (size_t)Nwin * d.Nkz * 4 * Epad * NNp; }
-  int64_t NEp = 0, Kp = 0;      // FP32 mode: energy row length (multiple of 4), coefficient row length
-  size_t gtp_elems() const { return (size_t)Nwin * d.Nkz * 4 * kTcRowsA * NEp; }
-  size_t gs_elems() const { return (size_t)d.Nkz * NEw * Nwin * ((NN + 1) & ~int64_t(1)); }
-  size_t gt_offset = 0;         // byte offset of the Σ Gt scratch inside ws
-  bool sig_tma = true;          // Norb <= 10: TMA/3M k_sigma + separate sandwich
-  int64_t ndc = 0;              // 16-shift chunks of the Σ coefficient window
-  size_t g_elems = 0;
-  double flops[4] = {0, 0, 0, 0};
-  // host-execute staging
-  void* h_dev = nullptr;
-  size_t h_dev_bytes = 0;
-  // atom-halo exchange (nranks > 1)
-  void* comm = nullptr;
-  std::vector<HaloPeer> peers;
-  char* sendbuf = nullptr;
-  char* recvbuf = nullptr;
-  size_t send_total = 0, recv_total = 0;
-  // per-kernel timing (qt_sse_timing_*)
-  bool timing = false;
-  std::vector<cudaEvent_t> ev_pool;
-  struct Rec { int kind; cudaEvent_t a, b; };
-  std::vector<Rec> recs;
-  size_t ev_used = 0;
-};
-
 namespace {
 
-qt_status cuda_status(cudaError_t e) {
-  if (e == cudaSuccess) return QT_OK;
-  if (e == cudaErrorMemoryAllocation) return QT_ERR_OUT_OF_MEMORY;
-  return QT_ERR_CUDA;
-}
-// a failed kernel launch: the status, plus (with QT_DEBUG set in the environment) the CUDA error on stderr
-qt_status launch_fail(int kind, cudaError_t e, int line) {
-  static const bool dbg = getenv("QT_DEBUG") != nullptr;
-  if (dbg) fprintf(stderr, "qt_sse: launch of kernel kind %d failed (qt_sse.cu:%d): %s\n", kind, line, cudaGetErrorString(e));
-  return cuda_status(e);
-}
-#define QT_CUDA(call)                           \
-  do {                                          \
-    cudaError_t e_ = (call);                    \
-    if (e_ != cudaSuccess) return cuda_status(e_); \
-  } while (0)
-cudaEvent_t take_event(qt_sse_plan_s* p) {
-  if (p->ev_used == p->ev_pool.size()) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-    p->ev_pool.push_back(e);
-  }
-  return p->ev_pool[p->ev_used++];
-}
-#define QT_LAUNCH(kind, call)                                            \
-  do {                                                                   \
-    g_launches.fetch_add(1);                                             \
-    cudaEvent_t ea_ = nullptr, eb_ = nullptr;                            \
-    if (p->timing) {                                                     \
-      ea_ = take_event(p);                                               \
-      eb_ = take_event(p);                                               \
-      if (ea_ && eb_) cudaEventRecord(ea_, cs);                          \
-    }                                                                    \
-    cudaError_t e_ = (call);                                             \
-    if (e_ != cudaSuccess) return launch_fail(kind, e_, __LINE__);      \
-    if (ea_ && eb_) {                                                    \
-      cudaEventRecord(eb_, cs);                                          \
-      p->recs.push_back({kind, ea_, eb_});                               \
-    }                                                                    \
-  } while (0)
+// ---------------------------------------------------------------- host-only layout of one rank
+// Everything a plan needs that does not touch the device: the rank's place in the Ta x TE grid (the paper's
+// Ta x TE tiling), its owned atoms/energies and input windows, the work lists, the workspace chunks,
+// the halo boxes per peer and the footprint. Built identically by qt_sse_plan and the host-only queries.
+struct Geom {
+  int Ta = 1, TE = 1, ta = 0, te = 0;
+  int64_t a_lo = 0, a_hi = 0, w_lo = 0, w_hi = 0;   // owned atoms, atom window
+  int64_t e_lo = 0, e_hi = 0, ew_lo = 0, ew_hi = 0; // owned energies, energy window
+  int64_t pa_lo = 0, pa_hi = 0;                     // Π output atoms
+};
 
-bool aligned16(const void* p) { return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+struct PiGroup {            // Π output group: atoms [lo, hi) of the owned slab
+  int64_t lo = 0, hi = 0;
+  int root = -1;            // TE-communicator rank receiving the reduced group (-1: written in place)
+  std::vector<int64_t> chunks;   // item bounds
+};
+
+struct SigChunk {
+  int64_t i0 = 0, i1 = 0;
+  bool coef_halo = false;   // the coefficient tables read D of halo atoms
+  bool g_halo = false;      // the contraction reads G entries of the halo
+};
+
+struct Layout {
+  qt_sse_desc d{};
+  Geom g;
+  int64_t NN = 0, h = 0, Dmax = 0, Dwin = 0, DWp = 0, NWv = 0, NWP = 0;
+  int64_t Nwin = 0, Nout = 0, NEw = 0, NEo = 0, E0 = 0;
+  bool fp32 = false, sig_tma = true, reduce = false;
+  std::vector<int32_t> nbr_win;
+  std::vector<SigItem> sig_items;
+  std::vector<SigPair> sig_pairs;
+  std::vector<int32_t> sig_pair_item;
+  std::vector<PiItem> pi_items;
+  std::vector<PiPair> pi_pairs;
+  std::vector<int32_t> pi_pair_item;
+  std::vector<SigChunk> sig_chunks;
+  std::vector<PiGroup> groups;
+  int64_t n_interior_items = 0;
+  int64_t sig_rows = kRows, ndc = 0, NNp = 0, Epad = 0, NEp = 0, Kp = 0;
+  size_t ws_bytes = 0, gt_offset = 0, part_bytes = 0;
+  std::vector<HaloPeer> peers;
+  size_t send_total = 0, recv_total = 0;
+  double flops[4] = {0, 0, 0, 0};
+  double npairs = 0;
+  size_t gs_elems() const { return (size_t)d.Nkz * NEw * Nwin * ((NN + 1) & ~int64_t(1)); }
+  size_t gtp_elems() const { return (size_t)Nwin * d.Nkz * 4 * kTcRowsA * NEp; }
+  size_t gpi_elems() const { return (size_t)Nwin * d.Nkz * 4 * Epad * NNp; }
+  double halo_recv = 0, reduce_bytes = 0;
+};
 
 qt_status validate_desc(const qt_sse_desc* d) {
   if (!d) return QT_ERR_INVALID_ARG;
@@ -127,14 +78,16 @@ qt_status validate_desc(const qt_sse_desc* d) {
     return QT_ERR_INVALID_ARG;
   if (d->N3D != 3 || d->Nkz != d->Nqz) return QT_ERR_INVALID_ARG;
   if (d->shift0 < 1 || d->shift_step < 1) return QT_ERR_INVALID_ARG;     // S:287 grid alignment
-  if (d->Na > (1LL << 30) || d->Nb > 4096) return QT_ERR_INVALID_ARG;
-  if (d->precision != QT_PREC_FP64 && d->precision != QT_PREC_FP32_MIXED) return QT_ERR_UNSUPPORTED;
-  if (d->precision == QT_PREC_FP32_MIXED && (d->Norb > 10 || d->Nw > 80))   // UMMA M = Norb² <= 128, N = Nω <= 80
-    return QT_ERR_UNSUPPORTED;
-  if (d->Norb > 12 || d->shift_step != 1 || d->Nw > 128) return QT_ERR_UNSUPPORTED;
+  if (d->Na > (1LL << 30) || d->Nb > 4096 || d->NE > (1LL << 24)) return QT_ERR_INVALID_ARG;
   if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return QT_ERR_INVALID_ARG;
-  if (d->nranks > 1 && d->shard != QT_SHARD_ATOM && d->shard != QT_SHARD_ENERGY) return QT_ERR_UNSUPPORTED;
-  if (d->shard == QT_SHARD_ENERGY && d->Norb > 10) return QT_ERR_UNSUPPORTED;   // the TMA / tcgen05 paths only
+  if (d->shard == QT_SHARD_2D && (d->grid_atoms < 1 || d->nranks % d->grid_atoms != 0)) return QT_ERR_INVALID_ARG;
+  if (d->flags & ~QT_FLAG_DETERMINISTIC) return QT_ERR_INVALID_ARG;
+  if (d->precision != QT_PREC_FP64 && d->precision != QT_PREC_FP32_MIXED) return QT_ERR_UNSUPPORTED;
+  const int64_t nwv = (d->Nw - 1) * d->shift_step + 1;   // Π columns: every shift between s_0 and s_{Nω-1}
+  if (d->precision == QT_PREC_FP32_MIXED && (d->Norb > 10 || nwv > 80))   // UMMA M = Norb² <= 128, N <= 80
+    return QT_ERR_UNSUPPORTED;
+  if (d->Norb > 12 || nwv > 128) return QT_ERR_UNSUPPORTED;
+  if (d->nranks > 1 && d->shard == QT_SHARD_NONE) return QT_ERR_UNSUPPORTED;
   return QT_OK;
 }
 
@@ -163,13 +116,14 @@ int64_t rev_slot(const int32_t* nbr, int64_t Nb, int64_t b, int64_t a) {
   return -1;
 }
 
-// valid (E, m) counts: V- = #{E - s_m >= 0}, V+ = #{E + s_m < NE}
-void window_counts(const qt_sse_desc* d, double* vm, double* vp, int64_t e_lo = 0, int64_t e_hi = -1) {
+int64_t shift_of(const qt_sse_desc* d, int64_t m) { return d->shift0 + m * d->shift_step; }
+
+// valid (E, m) counts over output energies [e_lo, e_hi): V- = #{E - s_m >= 0}, V+ = #{E + s_m < NE}
+void window_counts(const qt_sse_desc* d, double* vm, double* vp, int64_t e_lo, int64_t e_hi) {
   double a = 0, b = 0;
-  if (e_hi < 0) e_hi = d->NE;
   for (int64_t e = e_lo; e < e_hi; ++e)
     for (int64_t m = 0; m < d->Nw; ++m) {
-      int64_t sm = d->shift0 + m * d->shift_step;
+      const int64_t sm = shift_of(d, m);
       if (e - sm >= 0) a += 1;
       if (e + sm < d->NE) b += 1;
     }
@@ -177,10 +131,9 @@ void window_counts(const qt_sse_desc* d, double* vm, double* vp, int64_t e_lo = 
   *vp = b;
 }
 
-// algorithmic flops of the output energies [e_lo, e_hi) (default: all) for npairs valid pairs
-void count_flops(const qt_sse_desc* d, double npairs, double out[4], int64_t e_lo = 0, int64_t e_hi = -1) {
+// algorithmic flops of the output energies [e_lo, e_hi) for npairs valid pairs (SURVEY §8(d) F_alg)
+void count_flops(const qt_sse_desc* d, double npairs, double out[4], int64_t e_lo, int64_t e_hi) {
   double vm, vp;
-  if (e_hi < 0) e_hi = d->NE;
   window_counts(d, &vm, &vp, e_lo, e_hi);
   const double NN = (double)d->Norb * d->Norb, No3 = NN * d->Norb;
   out[0] = 2.0 * d->Nkz * d->Nqz * npairs * (vm + vp) * 9.0 * NN * 8.0;
@@ -189,65 +142,737 @@ void count_flops(const qt_sse_desc* d, double npairs, double out[4], int64_t e_l
   out[3] = 2.0 * d->Nkz * d->Nqz * npairs * vp * 9.0 * NN * 8.0;
 }
 
-// Atom ranges of a rank for atom sharding: contiguous owned slabs balanced by valid-pair count.
-void owned_range(const qt_sse_desc* d, const int32_t* nbr, int64_t* lo, int64_t* hi) {
-  if (d->nranks == 1) {
-    *lo = 0;
-    *hi = d->Na;
-    return;
-  }
-  std::vector<double> cum(d->Na + 1, 0.0);
-  for (int64_t a = 0; a < d->Na; ++a) {
-    int c = 0;
-    for (int64_t s = 0; s < d->Nb; ++s) c += nbr[a * d->Nb + s] >= 0;
-    cum[a + 1] = cum[a] + c + 1;
-  }
-  auto cut = [&](int r) -> int64_t {
-    double target = cum[d->Na] * r / d->nranks;
+// cut a cumulative weight table into n contiguous ranges; range k
+void cut_range(const std::vector<double>& cum, int n, int k, int64_t* lo, int64_t* hi) {
+  const int64_t N = (int64_t)cum.size() - 1;
+  auto cut = [&](int j) -> int64_t {
+    const double target = cum[N] * j / n;
     return (int64_t)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
   };
-  *lo = d->rank == 0 ? 0 : cut(d->rank);
-  *hi = d->rank == d->nranks - 1 ? d->Na : cut(d->rank + 1);
+  *lo = k == 0 ? 0 : cut(k);
+  *hi = k == n - 1 ? N : cut(k + 1);
+  if (*hi < *lo) *hi = *lo;
 }
 
-// Energy sharding (the paper's T_E tiling): rank r owns output energies [e_lo, e_hi), split by the
-// Σ/Π work per energy (valid shifts + sandwich), and reads the window [e_lo - Dmax, e_hi + Dmax) ∩ [0, NE).
-void energy_range(const qt_sse_desc* d, int r, int64_t* lo, int64_t* hi, int64_t* wlo, int64_t* whi) {
+// atom slab k of n over [lo0, hi0): contiguous, balanced by valid-pair count (+1 per atom)
+void atom_slab(const qt_sse_desc* d, const int32_t* nbr, int64_t lo0, int64_t hi0, int n, int k, int64_t* lo,
+               int64_t* hi) {
+  std::vector<double> cum(hi0 - lo0 + 1, 0.0);
+  for (int64_t a = lo0; a < hi0; ++a) {
+    int c = 0;
+    for (int64_t s = 0; s < d->Nb; ++s) c += nbr[a * d->Nb + s] >= 0;
+    cum[a - lo0 + 1] = cum[a - lo0] + c + 1;
+  }
+  cut_range(cum, n, k, lo, hi);
+  *lo += lo0;
+  *hi += lo0;
+}
+
+// energy slab k of n (the paper's T_E tiling), balanced by the Σ/Π work per energy (valid shifts +
+// sandwich); its input window is [lo - Dmax, hi + Dmax) ∩ [0, NE)
+void energy_slab(const qt_sse_desc* d, int n, int k, int64_t* lo, int64_t* hi, int64_t* wlo, int64_t* whi) {
   std::vector<double> cum(d->NE + 1, 0.0);
-  const int64_t Dmax = d->shift0 + (d->Nw - 1) * d->shift_step;
+  const int64_t Dmax = shift_of(d, d->Nw - 1);
   for (int64_t e = 0; e < d->NE; ++e) {
     double w = 1.0;
     for (int64_t m = 0; m < d->Nw; ++m) {
-      const int64_t sm = d->shift0 + m * d->shift_step;
+      const int64_t sm = shift_of(d, m);
       w += (e - sm >= 0) + 2.0 * (e + sm < d->NE);   // Σ absorption + emission, Π correlation
     }
     cum[e + 1] = cum[e] + w;
   }
-  auto cut = [&](int k) -> int64_t {
-    const double target = cum[d->NE] * k / d->nranks;
-    return (int64_t)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
-  };
-  *lo = r == 0 ? 0 : cut(r);
-  *hi = r == d->nranks - 1 ? d->NE : cut(r + 1);
+  cut_range(cum, n, k, lo, hi);
   *wlo = std::max<int64_t>(0, *lo - Dmax);
   *whi = std::min<int64_t>(d->NE, *hi + Dmax);
 }
 
-// input window of a rank: its owned atoms plus every neighbour of them (contiguous hull)
-void rank_window(const qt_sse_desc* d, const int32_t* nbr, int r, int64_t* a_lo, int64_t* a_hi, int64_t* w_lo,
-                 int64_t* w_hi) {
-  qt_sse_desc e = *d;
-  e.rank = r;
-  owned_range(&e, nbr, a_lo, a_hi);
-  *w_lo = *a_lo;
-  *w_hi = *a_hi;
-  for (int64_t a = *a_lo; a < *a_hi; ++a)
+void grid_of(const qt_sse_desc* d, int* Ta, int* TE) {
+  if (d->nranks == 1) {
+    *Ta = *TE = 1;
+  } else if (d->shard == QT_SHARD_ENERGY) {
+    *Ta = 1;
+    *TE = d->nranks;
+  } else if (d->shard == QT_SHARD_2D) {
+    *Ta = d->grid_atoms;
+    *TE = d->nranks / d->grid_atoms;
+  } else {
+    *Ta = d->nranks;
+    *TE = 1;
+  }
+}
+
+// geometry of rank r; `reduce` = the Π partial sums are reduced to sub-slab owners (communicator, TE > 1)
+Geom geom_of(const qt_sse_desc* d, const int32_t* nbr, int r, bool reduce) {
+  Geom g;
+  grid_of(d, &g.Ta, &g.TE);
+  g.ta = r / g.TE;
+  g.te = r % g.TE;
+  atom_slab(d, nbr, 0, d->Na, g.Ta, g.ta, &g.a_lo, &g.a_hi);
+  g.w_lo = g.a_lo;
+  g.w_hi = g.a_hi;
+  for (int64_t a = g.a_lo; a < g.a_hi; ++a)
     for (int64_t s = 0; s < d->Nb; ++s) {
       const int32_t b = nbr[a * d->Nb + s];
       if (b < 0) continue;
-      *w_lo = std::min<int64_t>(*w_lo, b);
-      *w_hi = std::max<int64_t>(*w_hi, b + 1);
+      g.w_lo = std::min<int64_t>(g.w_lo, b);
+      g.w_hi = std::max<int64_t>(g.w_hi, b + 1);
     }
+  energy_slab(d, g.TE, g.te, &g.e_lo, &g.e_hi, &g.ew_lo, &g.ew_hi);
+  if (reduce && g.TE > 1) {
+    atom_slab(d, nbr, g.a_lo, g.a_hi, g.TE, g.te, &g.pa_lo, &g.pa_hi);
+  } else {
+    g.pa_lo = g.a_lo;
+    g.pa_hi = g.a_hi;
+  }
+  return g;
+}
+
+size_t d_block_bytes(const qt_sse_desc& d) { return (size_t)d.Nqz * d.Nw * (d.Nb + 1) * 9 * 16; }   // per atom
+
+// Builds everything host-side for `rank` (reduce: a communicator will exist).
+qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce, size_t ws_budget, Layout* L,
+                       bool strict = true) {
+  L->d = *desc;
+  const qt_sse_desc& d = L->d;
+  L->NN = d.Norb * d.Norb;
+  L->h = d.Nkz / 2;
+  L->Dmax = shift_of(&d, d.Nw - 1);
+  L->Dwin = 2 * L->Dmax + 1;
+  L->DWp = (L->Dwin + 3) & ~3LL;
+  L->NWv = (d.Nw - 1) * d.shift_step + 1;
+  L->NWP = (L->NWv + 7) & ~7LL;
+  L->fp32 = d.precision == QT_PREC_FP32_MIXED;
+  L->g = geom_of(&d, nbr, d.rank, reduce);
+  const Geom& g = L->g;
+  if (strict && g.TE > 1 && d.Norb > 10) return QT_ERR_UNSUPPORTED;   // energy windows: TMA / tcgen05 kernels only
+  L->reduce = reduce && g.TE > 1;
+  L->Nwin = g.w_hi - g.w_lo;
+  L->Nout = g.a_hi - g.a_lo;
+  L->NEw = g.ew_hi - g.ew_lo;
+  L->NEo = g.e_hi - g.e_lo;
+  L->E0 = g.e_lo - g.ew_lo;
+  L->nbr_win.assign(L->Nwin * d.Nb, -1);
+  for (int64_t a = g.w_lo; a < g.w_hi; ++a)
+    for (int64_t s = 0; s < d.Nb; ++s) {
+      int32_t b = nbr[a * d.Nb + s];
+      if (b >= g.w_lo && b < g.w_hi) L->nbr_win[(a - g.w_lo) * d.Nb + s] = (int32_t)(b - g.w_lo);
+    }
+
+  // Σ work list: source-organized. For each source atom b, its reverse pairs (a,s) with a owned; interior
+  // sources (b owned: no halo read in the contraction or the coefficient tables) first, then halo sources.
+  const size_t scap = L->fp32 ? kTcPiPairs : kMaxPairs;   // 126 / 72 GEMM rows
+  auto add_source = [&](int64_t b) {
+    std::vector<SigPair> mine;
+    for (int64_t r = 0; r < d.Nb; ++r) {
+      int32_t a = nbr[b * d.Nb + r];
+      if (a < 0 || a < g.a_lo || a >= g.a_hi) continue;
+      SigPair q;
+      q.a = (int32_t)(a - g.a_lo);
+      q.a_in = (int32_t)(a - g.w_lo);
+      q.s = (int32_t)rev_slot(nbr, d.Nb, a, b);
+      q.r = (int32_t)r;
+      mine.push_back(q);
+    }
+    for (size_t k = 0; k < mine.size(); k += scap) {
+      SigItem it;
+      it.b_in = (int32_t)(b - g.w_lo);
+      it.b = (int32_t)b;
+      it.npair = (int32_t)std::min<size_t>(scap, mine.size() - k);
+      it.pair0 = (int32_t)L->sig_pairs.size();
+      for (int t = 0; t < it.npair; ++t) {
+        L->sig_pairs.push_back(mine[k + t]);
+        L->sig_pair_item.push_back((int32_t)L->sig_items.size());
+      }
+      L->sig_items.push_back(it);
+    }
+  };
+  for (int64_t b = g.a_lo; b < g.a_hi; ++b) add_source(b);
+  L->n_interior_items = (int64_t)L->sig_items.size();
+  for (int64_t b = g.w_lo; b < g.w_hi; ++b)
+    if (b < g.a_lo || b >= g.a_hi) add_source(b);
+
+  // Π groups: one per output owner (sub-slabs of the owned atoms when the partial sums are reduced)
+  if (L->reduce) {
+    for (int j = 0; j < g.TE; ++j) {
+      PiGroup G;
+      atom_slab(&d, nbr, g.a_lo, g.a_hi, g.TE, j, &G.lo, &G.hi);
+      G.root = j;
+      L->groups.push_back(G);
+    }
+  } else {
+    PiGroup G;
+    G.lo = g.a_lo;
+    G.hi = g.a_hi;
+    L->groups.push_back(G);
+  }
+  // Π work list: destination-organized. For each owned atom a, its valid slots in items of <= 8 (14) pairs;
+  // a_out is relative to the atom's group.
+  std::vector<int64_t> group_item0;
+  for (const PiGroup& G : L->groups) {
+    group_item0.push_back((int64_t)L->pi_items.size());
+    for (int64_t a = G.lo; a < G.hi; ++a) {
+      std::vector<PiPair> mine;
+      for (int64_t s = 0; s < d.Nb; ++s) {
+        int32_t b = nbr[a * d.Nb + s];
+        if (b < 0) continue;
+        PiPair q;
+        q.s = (int32_t)s;
+        q.b_in = (int32_t)(b - g.w_lo);
+        q.r = (int32_t)rev_slot(nbr, d.Nb, b, a);
+        q.a_in = (int32_t)(a - g.w_lo);
+        mine.push_back(q);
+      }
+      for (size_t k = 0; k < mine.size(); k += scap) {
+        PiItem it;
+        it.a_out = (int32_t)(a - G.lo);
+        it.a_in = (int32_t)(a - g.w_lo);
+        it.npair = (int32_t)std::min<size_t>(scap, mine.size() - k);
+        it.pair0 = (int32_t)L->pi_pairs.size();
+        for (int t = 0; t < it.npair; ++t) {
+          L->pi_pairs.push_back(mine[k + t]);
+          L->pi_pair_item.push_back((int32_t)L->pi_items.size());
+        }
+        L->pi_items.push_back(it);
+      }
+    }
+  }
+  group_item0.push_back((int64_t)L->pi_items.size());
+  L->npairs = (double)L->pi_pairs.size();
+  count_flops(&d, L->npairs, L->flops, g.e_lo, g.e_hi);
+
+  // workspace (shared by the Σ coefficient tables + Gt scratch and the Π W scratch; calls are serialized)
+  const size_t coef_per_pair = (size_t)9 * d.Nqz * L->DWp * sizeof(double2);
+  L->sig_rows = L->fp32 ? kTcRows : kRows;
+  const size_t gt_per_item = (size_t)d.Nkz * L->NEo * L->sig_rows * ((L->NN + 19) / 20) * 20 *
+                             (L->fp32 ? sizeof(float2) : sizeof(double2));
+  L->NNp = (L->NN + 3) & ~int64_t(3);
+  L->Epad = L->NEw + d.shift0 + 80 + 1;
+  const size_t w_per_item = L->fp32 ? (size_t)4 * kTcPiRows * d.Nkz * (((L->NEo * L->NNp + 31) / 32) * 32) * sizeof(float)
+                                    : gt_per_item;
+  L->NEp = std::max<int64_t>(32, (L->NEw + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
+  L->Kp = (L->Dwin + 3 + 31) & ~int64_t(31);                      // delayed coefficient rows, whole 32-chunks
+  L->sig_tma = d.Norb <= 10;
+  L->ndc = (L->Dwin + 15) / 16;
+  const size_t coef_item_t = L->fp32 ? (size_t)d.Nqz * 16 * kTcRows * L->Kp * sizeof(float)
+                                     : (size_t)d.Nqz * L->ndc * kRows * kCoefKCP * sizeof(double2);
+  const size_t need_min = std::max(coef_per_pair * kMaxPairs, coef_item_t) + w_per_item + 512;
+  const size_t full = std::max((coef_per_pair * kMaxPairs + coef_item_t + w_per_item) * L->sig_items.size() + 512,
+                               w_per_item * L->pi_items.size());
+  size_t budget = std::max(ws_budget, need_min);
+  L->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
+
+  // Π chunks inside each group (each chunk's W scratch fits the workspace)
+  {
+    const int64_t cap = std::max<int64_t>(1, (int64_t)(L->ws_bytes / w_per_item));
+    for (size_t gi = 0; gi < L->groups.size(); ++gi) {
+      PiGroup& G = L->groups[gi];
+      const int64_t i0 = group_item0[gi], i1 = group_item0[gi + 1];
+      G.chunks.push_back(i0);
+      for (int64_t i = i0 + cap; i < i1; i += cap) G.chunks.push_back(i);
+      G.chunks.push_back(i1);
+    }
+  }
+  // Σ chunks. TMA path (Norb <= 10): per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] + its
+  // Gt scratch; cp.async path (Norb 11, 12): per pair coefficient rows. Workspace = [coef | Gt]. A chunk never
+  // mixes interior and halo sources.
+  {
+    const size_t gt_item = L->sig_tma ? gt_per_item : 0;
+    size_t coef_acc = 0, gt_acc = 0, coef_max = 0;
+    SigChunk c;
+    c.i0 = 0;
+    auto close = [&](int64_t i) {
+      c.i1 = i;
+      const bool halo_src = c.i0 >= L->n_interior_items;
+      c.coef_halo = halo_src && g.Ta > 1;
+      c.g_halo = halo_src || g.TE > 1;
+      if (c.i1 > c.i0) L->sig_chunks.push_back(c);
+      c.i0 = i;
+      coef_max = std::max(coef_max, coef_acc);
+      coef_acc = gt_acc = 0;
+    };
+    for (size_t i = 0; i < L->sig_items.size(); ++i) {
+      const size_t cu = L->sig_tma ? coef_item_t : (size_t)L->sig_items[i].npair * coef_per_pair;
+      if ((int64_t)i == L->n_interior_items && gt_acc + coef_acc > 0) close((int64_t)i);
+      if (gt_acc > 0 && coef_acc + cu + gt_acc + gt_item + 256 > L->ws_bytes) close((int64_t)i);
+      coef_acc += cu;
+      gt_acc += gt_item == 0 ? 1 : gt_item;
+    }
+    close((int64_t)L->sig_items.size());
+    L->gt_offset = (coef_max + 255) & ~size_t(255);
+  }
+  if (L->reduce) {
+    int64_t mx = 0;
+    for (const PiGroup& G : L->groups) mx = std::max(mx, G.hi - G.lo);
+    L->part_bytes = (size_t)mx * d_block_bytes(d);
+    for (const PiGroup& G : L->groups)
+      if (G.root != g.te) L->reduce_bytes += 2.0 * (double)(G.hi - G.lo) * d_block_bytes(d);
+  }
+
+  // halo boxes per peer: G≷ = (my window ∩ their owned block), D≷ (Ta > 1) from the peer of my energy row
+  if (d.nranks > 1) {
+    const size_t gb = (size_t)L->NN * 16, db = d_block_bytes(d) / (d.Nqz * d.Nw);   // per (kz,e,atom) / (q,m,atom)
+    for (int r = 0; r < d.nranks; ++r) {
+      if (r == d.rank) continue;
+      const Geom o = geom_of(&d, nbr, r, reduce);
+      HaloPeer hp;
+      hp.rank = r;
+      auto box = [](int64_t lo1, int64_t hi1, int64_t lo2, int64_t hi2, int64_t* lo, int64_t* n) {
+        *lo = std::max(lo1, lo2);
+        *n = std::max<int64_t>(0, std::min(hi1, hi2) - *lo);
+      };
+      int64_t ra0, rna, re0, rne, sa0, sna, se0, sne;
+      box(g.w_lo, g.w_hi, o.a_lo, o.a_hi, &ra0, &rna);
+      box(g.ew_lo, g.ew_hi, o.e_lo, o.e_hi, &re0, &rne);
+      box(g.a_lo, g.a_hi, o.w_lo, o.w_hi, &sa0, &sna);
+      box(g.e_lo, g.e_hi, o.ew_lo, o.ew_hi, &se0, &sne);
+      if (rna && rne) {
+        hp.recv_g = {re0 - g.ew_lo, rne, ra0 - g.w_lo, rna};
+      }
+      if (sna && sne) {
+        hp.send_g = {se0 - g.ew_lo, sne, sa0 - g.w_lo, sna};
+      }
+      if (g.Ta > 1 && o.te == g.te) {
+        if (rna) hp.recv_d = {0, 1, ra0 - g.w_lo, rna};
+        if (sna) hp.send_d = {0, 1, sa0 - g.w_lo, sna};
+      }
+      hp.recv_bytes = 2 * ((size_t)d.Nkz * hp.recv_g.ne * hp.recv_g.na * gb + (size_t)d.Nqz * d.Nw * hp.recv_d.na * db);
+      hp.send_bytes = 2 * ((size_t)d.Nkz * hp.send_g.ne * hp.send_g.na * gb + (size_t)d.Nqz * d.Nw * hp.send_d.na * db);
+      if (!hp.recv_bytes && !hp.send_bytes) continue;
+      // energy-only splits (Ta == 1): the G boxes are Nkz contiguous runs of the window, sent in place
+      hp.direct = g.Ta == 1;
+      if (!hp.direct) {
+        hp.recv_off = L->recv_total;
+        hp.send_off = L->send_total;
+        L->recv_total += hp.recv_bytes;
+        L->send_total += hp.send_bytes;
+      }
+      L->halo_recv += (double)hp.recv_bytes;
+      L->peers.push_back(hp);
+    }
+  }
+  return QT_OK;
+}
+
+// footprint of one rank: caller tensors (window inputs, owned outputs) + the plan's device allocations
+double footprint(const Layout& L) {
+  const qt_sse_desc& d = L.d;
+  const double c16 = 16.0;
+  double caller = 2.0 * d.Nkz * L.NEw * L.Nwin * L.NN * c16 + 2.0 * L.Nwin * (double)d_block_bytes(d) +
+                  (double)L.Nwin * d.Nb * 3 * L.NN * c16 + 2.0 * d.Nkz * L.NEo * L.Nout * L.NN * c16 +
+                  2.0 * (L.g.pa_hi - L.g.pa_lo) * (double)d_block_bytes(d);
+  double plan = (double)L.ws_bytes + (1 << 20) + (double)L.send_total + (double)L.recv_total + 2.0 * L.part_bytes;
+  if (L.fp32)
+    plan += 2.0 * L.gtp_elems() * 4 + (double)L.gpi_elems() * 4;
+  else
+    plan += 2.0 * L.gs_elems() * 8;
+  plan += (double)(L.sig_items.size() * sizeof(SigItem) + L.sig_pairs.size() * (sizeof(SigPair) + 4) +
+                   L.pi_items.size() * sizeof(PiItem) + L.pi_pairs.size() * (sizeof(PiPair) + 4) + L.nbr_win.size() * 4);
+  return caller + plan;
+}
+
+constexpr size_t kAutoWsCap = (size_t)48 << 30;
+
+}  // namespace
+
+struct qt_sse_plan_s {
+  Layout L;
+  // device
+  int device = 0;
+  int32_t* d_nbr_win = nullptr;
+  SigItem* d_sig_items = nullptr;
+  SigPair* d_sig_pairs = nullptr;
+  int32_t* d_sig_pair_item = nullptr;
+  PiItem* d_pi_items = nullptr;
+  PiPair* d_pi_pairs = nullptr;
+  int32_t* d_pi_pair_item = nullptr;
+  double2* ws = nullptr;
+  double* ws_gs = nullptr;      // FP64: Re + Im planes of G^<, G^> [2][Nwin][Nkz][NEw][NN rounded up to even]
+  float* ws_gtp = nullptr;      // FP32 mode: split G planes [2][Nwin][Nkz][4][128][NEp]
+  float* ws_gpi = nullptr;      // FP32 mode: split G^X planes for Π [Nwin][Nkz][4][Epad][NNp] (one X at a time)
+  double2* part[2] = {nullptr, nullptr};   // Π partial sums of one group (TE > 1 with a communicator)
+  // host-execute staging
+  void* h_dev = nullptr;
+  size_t h_dev_bytes = 0;
+  // communication
+  void* comm = nullptr;         // all ranks
+  void* comm_e = nullptr;       // the TE ranks of this atom slab (Π reduction)
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr, ev_part[2] = {nullptr, nullptr}, ev_red[2] = {nullptr, nullptr};
+  bool red_pending[2] = {false, false};
+  char* sendbuf = nullptr;
+  char* recvbuf = nullptr;
+  // call ordering across streams
+  cudaEvent_t ev_done = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
+  // per-kernel timing (qt_sse_timing_*)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  size_t ev_used = 0;
+};
+
+namespace {
+
+qt_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return QT_OK;
+  if (e == cudaErrorMemoryAllocation) return QT_ERR_OUT_OF_MEMORY;
+  return QT_ERR_CUDA;
+}
+// a failed kernel launch: the status, plus (with QT_DEBUG set in the environment) the CUDA error on stderr
+qt_status launch_fail(int kind, cudaError_t e, int line) {
+  static const bool dbg = getenv("QT_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "qt_sse: launch of kernel kind %d failed (qt_sse.cu:%d): %s\n", kind, line, cudaGetErrorString(e));
+  return cuda_status(e);
+}
+#define QT_CUDA(call)                              \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
+#define QT_TRY(call)                  \
+  do {                                \
+    qt_status s_ = (call);            \
+    if (s_ != QT_OK) return s_;       \
+  } while (0)
+cudaEvent_t take_event(qt_sse_plan_s* p) {
+  if (p->ev_used == p->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    p->ev_pool.push_back(e);
+  }
+  return p->ev_pool[p->ev_used++];
+}
+#define QT_LAUNCH(kind, call)                                            \
+  do {                                                                   \
+    g_launches.fetch_add(1);                                             \
+    cudaEvent_t ea_ = nullptr, eb_ = nullptr;                            \
+    if (p->timing) {                                                     \
+      ea_ = take_event(p);                                               \
+      eb_ = take_event(p);                                               \
+      if (ea_ && eb_) cudaEventRecord(ea_, cs);                          \
+    }                                                                    \
+    cudaError_t e_ = (call);                                             \
+    if (e_ != cudaSuccess) return launch_fail(kind, e_, __LINE__);       \
+    if (ea_ && eb_) {                                                    \
+      cudaEventRecord(eb_, cs);                                          \
+      p->recs.push_back({kind, ea_, eb_});                               \
+    }                                                                    \
+  } while (0)
+
+bool aligned16(const void* q) { return q != nullptr && (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+// asynchronous NCCL failures of earlier calls (ncclCommGetAsyncError) -> QT_ERR_NCCL
+qt_status nccl_check(const qt_sse_plan_s* p) {
+  if (p->comm && nccl_async_error(p->comm)) return QT_ERR_NCCL;
+  if (p->comm_e && nccl_async_error(p->comm_e)) return QT_ERR_NCCL;
+  return QT_OK;
+}
+
+// every call: order after the plan's previous call when it ran on another stream (the calls share scratch)
+qt_status call_begin(qt_sse_plan_s* p, cudaStream_t cs) {
+  QT_TRY(nccl_check(p));
+  if (p->has_last && p->last_stream != cs) QT_CUDA(cudaStreamWaitEvent(cs, p->ev_done, 0));
+  return QT_OK;
+}
+qt_status call_end(qt_sse_plan_s* p, cudaStream_t cs) {
+  QT_CUDA(cudaEventRecord(p->ev_done, cs));
+  p->last_stream = cs;
+  p->has_last = true;
+  return QT_OK;
+}
+
+// sum planes (FP64) / split planes (FP32) of the window atoms [a0, a1) of both G^X
+qt_status relayout_sigma(qt_sse_plan_s* p, const void* GL, const void* GG, int64_t a0, int64_t a1, cudaStream_t cs) {
+  const Layout& L = p->L;
+  const qt_sse_desc& d = L.d;
+  if (a1 <= a0) return QT_OK;
+  if (L.fp32) {
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GL, p->ws_gtp, d.Nkz, L.NEw, L.NEp, L.Nwin, (int)L.NN, a0, a1, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GG, p->ws_gtp + L.gtp_elems(), d.Nkz, L.NEw, L.NEp, L.Nwin,
+                                                (int)L.NN, a0, a1, cs));
+  } else {
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_gs, d.Nkz, L.NEw, L.Nwin, L.NN, a0, a1, cs));
+    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_gs + L.gs_elems(), d.Nkz, L.NEw, L.Nwin, L.NN, a0, a1, cs));
+  }
+  return QT_OK;
+}
+
+// Σ^X (Eq. 3) over the Σ chunks; with `halo` set the stream waits for it (and re-lays-out the halo part of
+// G) before the first chunk that reads halo data.
+qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void* GG, const void* DL, const void* DG,
+                    double sre, double sim, void* SL, void* SG, cudaStream_t cs, cudaEvent_t halo, bool* halo_done) {
+  const Layout& L = p->L;
+  const qt_sse_desc& d = L.d;
+  const size_t sig_bytes = (size_t)d.Nkz * L.NEo * L.Nout * L.NN * sizeof(double2);
+  auto wait_halo = [&](bool need) -> qt_status {
+    if (!need || *halo_done) return QT_OK;
+    if (halo) QT_CUDA(cudaStreamWaitEvent(cs, halo, 0));
+    if (L.g.TE > 1 || !halo) {
+      QT_TRY(relayout_sigma(p, GL, GG, 0, L.Nwin, cs));   // energy halo: every atom's window
+    } else {
+      QT_TRY(relayout_sigma(p, GL, GG, 0, L.g.a_lo - L.g.w_lo, cs));
+      QT_TRY(relayout_sigma(p, GL, GG, L.g.a_hi - L.g.w_lo, L.Nwin, cs));
+    }
+    *halo_done = true;
+    return QT_OK;
+  };
+  for (int X = 0; X < 2; ++X) {
+    void* S = X == 0 ? SL : SG;
+    QT_CUDA(cudaMemsetAsync(S, 0, sig_bytes, cs));
+    for (const SigChunk& ch : L.sig_chunks) {
+      const int64_t i0 = ch.i0, i1 = ch.i1;
+      const int64_t pp0 = L.sig_items[i0].pair0;
+      const int64_t pp1 = L.sig_items[i1 - 1].pair0 + L.sig_items[i1 - 1].npair;
+      QT_TRY(wait_halo(ch.coef_halo));
+      CoefArgs ca;
+      ca.DX = (const double2*)(X == 0 ? DL : DG);
+      ca.DY = (const double2*)(X == 0 ? DG : DL);
+      ca.pairs = p->d_sig_pairs + pp0;
+      ca.items = p->d_sig_items;
+      ca.pair_item = p->d_sig_pair_item + pp0;
+      ca.coef = p->ws;
+      ca.npairs = pp1 - pp0;
+      ca.Nw = d.Nw;
+      ca.Nwin = L.Nwin;
+      ca.Nb = d.Nb;
+      ca.Nqz = d.Nqz;
+      ca.DWp = L.DWp;
+      ca.Dmax = (int)L.Dmax;
+      ca.shift0 = d.shift0;
+      ca.step = d.shift_step;
+      ca.tiled = L.sig_tma;
+      ca.item0 = i0;
+      ca.nitems = i1 - i0;
+      ca.ndc = L.ndc;
+      ca.Dwin = L.Dwin;
+      QT_LAUNCH(QT_K_SIGMA_COEF, L.fp32      ? launch_sigma_coef_tc(ca, (int)L.Kp, cs)
+                                 : L.sig_tma ? launch_sigma_coef_tiled(ca, cs)
+                                             : launch_sigma_coef(ca, cs));
+      QT_TRY(wait_halo(ch.g_halo));
+      SigmaArgs sa;
+      sa.G = (const double2*)(X == 0 ? GL : GG);
+      sa.Gsum = p->ws_gs ? p->ws_gs + (X == 0 ? 0 : L.gs_elems()) : nullptr;
+      sa.coef = p->ws;
+      sa.Gt = reinterpret_cast<double2*>(reinterpret_cast<char*>(p->ws) + L.gt_offset);
+      sa.cp0 = pp0;
+      sa.npairs_chunk = pp1 - pp0;
+      sa.dH = (const double2*)dH;
+      sa.items = p->d_sig_items + i0;
+      sa.pairs = p->d_sig_pairs;
+      sa.Sig = (double2*)S;
+      sa.scale = make_double2(sre, sim);
+      sa.Nwin = L.Nwin;
+      sa.Nout = L.Nout;
+      sa.Nb = d.Nb;
+      sa.DWp = L.DWp;
+      sa.NE = (int)L.NEw;
+      sa.E0 = (int)L.E0;
+      sa.NEo = (int)L.NEo;
+      sa.Nkz = (int)d.Nkz;
+      sa.Nqz = (int)d.Nqz;
+      sa.h = (int)L.h;
+      sa.Norb = (int)d.Norb;
+      sa.NN = (int)L.NN;
+      sa.Dmax = (int)L.Dmax;
+      sa.ndc = (int)L.ndc;
+      sa.Dwin = (int)L.Dwin;
+      sa.rows = (int)L.sig_rows;
+      sa.gt_f32 = L.fp32 ? 1 : 0;
+      sa.ntiles = 0;
+      if (L.fp32) {
+        QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : L.gtp_elems()), L.NEp,
+                                              reinterpret_cast<const float*>(p->ws), (int)L.Kp, i1 - i0, cs));
+      } else {
+        QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
+      }
+      QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
+    }
+  }
+  return QT_OK;
+}
+
+// Π^X (Eq. 4): per group, W sandwiches + correlation per chunk, the self slot, and (TE > 1 with a
+// communicator) an ncclReduce of the group's partial sums to its owner on the communication stream, while
+// the compute stream continues with the next group (two partial buffers).
+qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* GG, double sre, double sim, void* PL,
+                 void* PG, cudaStream_t cs) {
+  const Layout& L = p->L;
+  const qt_sse_desc& d = L.d;
+  int nb = 0;   // partial buffer toggle
+  for (int X = 0; X < 2; ++X) {
+    const double2* GX = (const double2*)(X == 0 ? GL : GG);
+    const double2* GY = (const double2*)(X == 0 ? GG : GL);
+    double2* P = (double2*)(X == 0 ? PL : PG);
+    if (L.fp32)
+      QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_pi_tc(GX, p->ws_gpi, d.Nkz, L.NEw, L.Epad, L.Nwin, (int)L.NN, (int)L.NNp, cs));
+    for (const PiGroup& G : L.groups) {
+      const int64_t nga = G.hi - G.lo;
+      double2* target = P;
+      int buf = -1;
+      if (L.reduce) {
+        buf = nb;
+        nb ^= 1;
+        if (p->red_pending[buf]) {   // the reduction that last read this buffer must be done
+          QT_CUDA(cudaStreamWaitEvent(cs, p->ev_red[buf], 0));
+          p->red_pending[buf] = false;
+        }
+        target = p->part[buf];
+      }
+      for (size_t c = 0; c + 1 < G.chunks.size(); ++c) {
+        const int64_t i0 = G.chunks[c], i1 = G.chunks[c + 1];
+        if (i1 <= i0) continue;
+        const int64_t pp0 = L.pi_items[i0].pair0;
+        PiWArgs wa;
+        wa.GY = GY;
+        wa.dH = (const double2*)dH;
+        wa.pairs = p->d_pi_pairs;
+        wa.items = p->d_pi_items;
+        wa.pair_item = p->d_pi_pair_item;
+        wa.W = p->ws;
+        wa.p0 = pp0;
+        wa.i0 = i0;
+        wa.Nwin = L.Nwin;
+        wa.Nb = d.Nb;
+        wa.NE = (int)L.NEw;
+        wa.E0 = (int)L.E0;
+        wa.NEo = (int)L.NEo;
+        wa.Nkz = (int)d.Nkz;
+        wa.Norb = (int)d.Norb;
+        wa.NN = (int)L.NN;
+        wa.nEB = (int)((L.NEw + kEB - 1) / kEB);
+        if (L.fp32) {
+          QT_LAUNCH(QT_K_PI_W, launch_pi_w_tc(wa, reinterpret_cast<float*>(p->ws), (int)L.NNp, i1 - i0, cs));
+        } else {
+          QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, i1 - i0, cs));
+        }
+        PiCArgs ca;
+        ca.GX = GX;
+        ca.W = p->ws;
+        ca.GXsum = p->ws_gs ? p->ws_gs + (X == 0 ? 0 : L.gs_elems()) : nullptr;
+        ca.items = p->d_pi_items;
+        ca.pairs = p->d_pi_pairs;
+        ca.Pi = target;
+        ca.scale = make_double2(sre, sim);
+        ca.i0 = i0;
+        ca.nitems = i1 - i0;
+        ca.Nwin = L.Nwin;
+        ca.Nout = nga;
+        ca.Nb = d.Nb;
+        ca.NE = (int)L.NEw;
+        ca.E0 = (int)L.E0;
+        ca.NEo = (int)L.NEo;
+        ca.Nkz = (int)d.Nkz;
+        ca.Nqz = (int)d.Nqz;
+        ca.h = (int)L.h;
+        ca.NN = (int)L.NN;
+        ca.Nw = (int)d.Nw;
+        ca.NWv = (int)L.NWv;
+        ca.NWP = (int)L.NWP;
+        ca.shift0 = d.shift0;
+        ca.step = d.shift_step;
+        if (L.fp32) {
+          QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract_tc(ca, reinterpret_cast<const float*>(p->ws), p->ws_gpi, L.Epad,
+                                                            (int)L.NNp, i1 - i0, cs));
+        } else {
+          QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
+        }
+      }
+      PiSelfArgs sa;
+      sa.Pi = target;
+      sa.nbr = p->d_nbr_win;
+      sa.Nout = nga;
+      sa.Nb = d.Nb;
+      sa.Nqz = d.Nqz;
+      sa.Nw = d.Nw;
+      sa.a_off = G.lo - L.g.w_lo;
+      QT_LAUNCH(QT_K_PI_SELF, launch_pi_self(sa, cs));
+      if (L.reduce) {   // Π is a sum over energies: the group's owner receives the sum of the TE partials
+        QT_CUDA(cudaEventRecord(p->ev_part[buf], cs));
+        QT_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_part[buf], 0));
+        const size_t n = (size_t)nga * d_block_bytes(d) / sizeof(double);
+        if (nccl_reduce_sum(p->comm_e, reinterpret_cast<const double*>(target), reinterpret_cast<double*>(P), n, G.root,
+                            p->cstream) != 0)
+          return QT_ERR_NCCL;
+        QT_CUDA(cudaEventRecord(p->ev_red[buf], p->cstream));
+        p->red_pending[buf] = true;
+      }
+    }
+  }
+  for (int b = 0; b < 2; ++b)
+    if (p->red_pending[b]) {
+      QT_CUDA(cudaStreamWaitEvent(cs, p->ev_red[b], 0));
+      p->red_pending[b] = false;
+    }
+  return QT_OK;
+}
+
+// halo exchange on `st`: pack (atom splits) -> one grouped send/recv round -> unpack into the window halo
+qt_status exchange(qt_sse_plan_s* p, void* GL, void* GG, void* DL, void* DG, cudaStream_t st) {
+  const Layout& L = p->L;
+  const qt_sse_desc& d = L.d;
+  cudaStream_t cs = st;   // for QT_LAUNCH
+  void* gt[2] = {GL, GG};
+  void* dt[2] = {DL, DG};
+  const int64_t ginner = L.NN * 16, dinner = (int64_t)(d.Nb + 1) * 9 * 16;
+  for (const HaloPeer& h : L.peers) {
+    if (h.direct) continue;
+    size_t off = h.send_off;
+    for (int x = 0; x < 2; ++x) {
+      const HaloBox& b = h.send_g;
+      QT_LAUNCH(QT_K_HALO, launch_pack(gt[x], p->sendbuf + off, d.Nkz, L.NEw, b.e0, b.ne, L.Nwin, b.a0, b.na, ginner, false, cs));
+      off += (size_t)d.Nkz * b.ne * b.na * ginner;
+    }
+    for (int x = 0; x < 2; ++x) {
+      const HaloBox& b = h.send_d;
+      QT_LAUNCH(QT_K_HALO, launch_pack(dt[x], p->sendbuf + off, d.Nqz * d.Nw, 1, 0, b.na ? 1 : 0, L.Nwin, b.a0, b.na, dinner,
+                                       false, cs));
+      off += (size_t)d.Nqz * d.Nw * b.na * dinner;
+    }
+  }
+  const int64_t kzstride = L.NEw * L.Nwin * ginner;   // bytes per kz of the G window
+  if (nccl_exchange(p->comm, L.peers, p->sendbuf, p->recvbuf, gt, d.Nkz, kzstride, L.Nwin * ginner, cs) != 0)
+    return QT_ERR_NCCL;
+  for (const HaloPeer& h : L.peers) {
+    if (h.direct) continue;
+    size_t off = h.recv_off;
+    for (int x = 0; x < 2; ++x) {
+      const HaloBox& b = h.recv_g;
+      QT_LAUNCH(QT_K_HALO, launch_pack(p->recvbuf + off, gt[x], d.Nkz, L.NEw, b.e0, b.ne, L.Nwin, b.a0, b.na, ginner, true, cs));
+      off += (size_t)d.Nkz * b.ne * b.na * ginner;
+    }
+    for (int x = 0; x < 2; ++x) {
+      const HaloBox& b = h.recv_d;
+      QT_LAUNCH(QT_K_HALO, launch_pack(p->recvbuf + off, dt[x], d.Nqz * d.Nw, 1, 0, b.na ? 1 : 0, L.Nwin, b.a0, b.na, dinner,
+                                       true, cs));
+      off += (size_t)d.Nqz * d.Nw * b.na * dinner;
+    }
+  }
+  return QT_OK;
+}
+
+template <typename T>
+qt_status upload(T** dst, const std::vector<T>& v, cudaStream_t st) {
+  if (v.empty()) return QT_OK;
+  QT_CUDA(cudaMalloc(dst, v.size() * sizeof(T)));
+  QT_CUDA(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return QT_OK;
+}
+
+qt_status check_ptrs(std::initializer_list<const void*> ins, std::initializer_list<const void*> outs) {
+  for (const void* q : ins)
+    if (!aligned16(q)) return QT_ERR_INVALID_ARG;
+  for (const void* o : outs) {
+    if (!aligned16(o)) return QT_ERR_INVALID_ARG;
+    for (const void* q : ins)
+      if (q == o) return QT_ERR_INVALID_ARG;
+  }
+  std::vector<const void*> o(outs);
+  for (size_t i = 0; i < o.size(); ++i)
+    for (size_t j = i + 1; j < o.size(); ++j)
+      if (o[i] == o[j]) return QT_ERR_INVALID_ARG;
+  return QT_OK;
 }
 
 }  // namespace
@@ -278,16 +903,37 @@ extern "C" qt_status qt_sse_count_flops(const qt_sse_desc* desc, const int32_t* 
   if (st != QT_OK) return st;
   if (!out) return QT_ERR_INVALID_ARG;
   if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
-  int64_t lo = 0, hi = desc->Na, e_lo = 0, e_hi = desc->NE, wlo, whi;
-  if (desc->shard == QT_SHARD_ENERGY && desc->nranks > 1)
-    energy_range(desc, desc->rank, &e_lo, &e_hi, &wlo, &whi);   // all atoms, this rank's energies
-  else
-    owned_range(desc, nbr, &lo, &hi);
+  const Geom g = geom_of(desc, nbr, desc->rank, false);
   double np = 0;
-  for (int64_t a = lo; a < hi; ++a)
+  for (int64_t a = g.a_lo; a < g.a_hi; ++a)
     for (int64_t s = 0; s < desc->Nb; ++s) np += nbr[a * desc->Nb + s] >= 0;
-  count_flops(desc, np, out, e_lo, e_hi);
+  count_flops(desc, np, out, g.e_lo, g.e_hi);
   return QT_OK;
+}
+
+static void fill_info(const Layout& L, size_t ws_total, qt_sse_info* o) {
+  const Geom& g = L.g;
+  o->a_lo = g.a_lo;
+  o->a_hi = g.a_hi;
+  o->w_lo = g.w_lo;
+  o->w_hi = g.w_hi;
+  o->npairs = (int64_t)L.npairs;
+  o->workspace_bytes = ws_total;
+  o->flops_sigma = L.flops[0] + L.flops[1];
+  o->flops_pi = L.flops[2] + L.flops[3];
+  o->halo_bytes = L.halo_recv;
+  o->e_lo = g.e_lo;
+  o->e_hi = g.e_hi;
+  o->ew_lo = g.ew_lo;
+  o->ew_hi = g.ew_hi;
+  o->pa_lo = g.pa_lo;
+  o->pa_hi = g.pa_hi;
+  o->Ta = g.Ta;
+  o->TE = g.TE;
+  o->ta = g.ta;
+  o->te = g.te;
+  o->reduce_bytes = L.reduce_bytes;
+  o->mem_bytes = footprint(L);
 }
 
 extern "C" qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* nbr, qt_sse_info* o) {
@@ -296,47 +942,22 @@ extern "C" qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* n
   if (st != QT_OK) return st;
   if (!o) return QT_ERR_INVALID_ARG;
   if ((st = validate_nbr(desc, nbr)) != QT_OK) return st;
-  const bool eshard = desc->shard == QT_SHARD_ENERGY && desc->nranks > 1;
-  if (eshard) {
-    o->a_lo = o->w_lo = 0;
-    o->a_hi = o->w_hi = desc->Na;
-    energy_range(desc, desc->rank, &o->e_lo, &o->e_hi, &o->ew_lo, &o->ew_hi);
-  } else {
-    rank_window(desc, nbr, desc->rank, &o->a_lo, &o->a_hi, &o->w_lo, &o->w_hi);
-    o->e_lo = o->ew_lo = 0;
-    o->e_hi = o->ew_hi = desc->NE;
+  Layout* L = new (std::nothrow) Layout();
+  if (!L) return QT_ERR_OUT_OF_MEMORY;
+  // a sharded description is reported as the communicator-backed plan it describes
+  const bool reduce = desc->nranks > 1;
+  st = build_layout(desc, nbr, reduce, desc->workspace_limit ? desc->workspace_limit : kAutoWsCap, L, false);
+  if (st == QT_OK) {
+    size_t gsb = L->fp32 ? 2 * L->gtp_elems() * 4 + L->gpi_elems() * 4 : 2 * L->gs_elems() * 8;
+    fill_info(*L, L->ws_bytes + gsb, o);
   }
-  double np = 0;
-  for (int64_t a = o->a_lo; a < o->a_hi; ++a)
-    for (int64_t s = 0; s < desc->Nb; ++s) np += nbr[a * desc->Nb + s] >= 0;
-  double f[4];
-  count_flops(desc, np, f, o->e_lo, o->e_hi);
-  o->npairs = (int64_t)np;
-  o->workspace_bytes = 0;
-  o->flops_sigma = f[0] + f[1];
-  o->flops_pi = f[2] + f[3];
-  double recv = 0;
-  const double per_atom = 2.0 * desc->Nkz * desc->NE * desc->Norb * desc->Norb * 16 +
-                          2.0 * desc->Nqz * desc->Nw * (desc->Nb + 1) * 9 * 16;
-  const double per_e = 2.0 * desc->Nkz * desc->Na * desc->Norb * desc->Norb * 16;
-  for (int r = 0; eshard && r < desc->nranks; ++r) {
-    if (r == desc->rank) continue;
-    int64_t elo, ehi, wlo, whi;
-    energy_range(desc, r, &elo, &ehi, &wlo, &whi);
-    recv += std::max<int64_t>(0, std::min(o->ew_hi, ehi) - std::max(o->ew_lo, elo)) * per_e;
-  }
-  for (int r = 0; !eshard && r < desc->nranks; ++r) {
-    if (r == desc->rank) continue;
-    int64_t alo, ahi, wlo, whi;
-    rank_window(desc, nbr, r, &alo, &ahi, &wlo, &whi);
-    recv += std::max<int64_t>(0, std::min(o->w_hi, ahi) - std::max(o->w_lo, alo)) * per_atom;
-  }
-  o->halo_bytes = recv;
-  return QT_OK;
+  delete L;
+  return st;
 }
 
 extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   if (!p) return;
+  if (p->has_last) cudaEventSynchronize(p->ev_done);
   cudaFree(p->d_nbr_win);
   cudaFree(p->d_sig_items);
   cudaFree(p->d_sig_pairs);
@@ -345,24 +966,22 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_pi_pairs);
   cudaFree(p->d_pi_pair_item);
   cudaFree(p->ws);
-  cudaFree(p->ws_g);
   cudaFree(p->ws_gs);
   cudaFree(p->ws_gtp);
   cudaFree(p->ws_gpi);
+  cudaFree(p->part[0]);
+  cudaFree(p->part[1]);
   cudaFree(p->sendbuf);
   cudaFree(p->recvbuf);
+  nccl_comm_destroy(p->comm_e);
   nccl_comm_destroy(p->comm);
   cudaFree(p->h_dev);
+  cudaEvent_t evs[] = {p->ev_in, p->ev_halo, p->ev_part[0], p->ev_part[1], p->ev_red[0], p->ev_red[1], p->ev_done};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  if (p->cstream) cudaStreamDestroy(p->cstream);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
-}
-
-template <typename T>
-static qt_status upload(T** dst, const std::vector<T>& v, cudaStream_t st) {
-  if (v.empty()) return QT_OK;
-  QT_CUDA(cudaMalloc(dst, v.size() * sizeof(T)));
-  QT_CUDA(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
-  return QT_OK;
 }
 
 extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, void* stream, qt_sse_plan_t* out) {
@@ -374,285 +993,69 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
   cudaStream_t cs = (cudaStream_t)stream;
   qt_sse_plan_s* p = new (std::nothrow) qt_sse_plan_s();
   if (!p) return QT_ERR_OUT_OF_MEMORY;
-  p->d = *desc;
-  const qt_sse_desc& d = p->d;
-  p->NN = d.Norb * d.Norb;
-  p->h = d.Nkz / 2;
-  p->Dmax = d.shift0 + (d.Nw - 1) * d.shift_step;
-  p->Dwin = 2 * p->Dmax + 1;
-  p->DWp = (p->Dwin + 3) & ~3LL;
-  p->NWP = (d.Nw + 7) & ~7LL;
-  p->nbr.assign(nbr, nbr + d.Na * d.Nb);
-  p->eshard = d.shard == QT_SHARD_ENERGY && d.nranks > 1;
-  if (p->eshard) {
-    // energy sharding: all atoms, an energy window; halo = window energies owned by peers (G only: D and
-    // ∇H do not depend on energy and are replicated)
-    p->a_lo = p->w_lo = 0;
-    p->a_hi = p->w_hi = d.Na;
-    energy_range(&d, d.rank, &p->e_lo, &p->e_hi, &p->ew_lo, &p->ew_hi);
-    const size_t per_e = 2 * (size_t)d.Nkz * d.Na * d.Norb * d.Norb * 16;
-    for (int r = 0; r < d.nranks; ++r) {
-      if (r == d.rank) continue;
-      int64_t elo, ehi, wlo, whi;
-      energy_range(&d, r, &elo, &ehi, &wlo, &whi);
-      HaloPeer h;
-      h.rank = r;
-      const int64_t rl = std::max(p->ew_lo, elo), rh = std::min(p->ew_hi, ehi);
-      const int64_t sl = std::max(p->e_lo, wlo), sh = std::min(p->e_hi, whi);
-      h.recv_lo = rl - p->ew_lo;
-      h.recv_n = std::max<int64_t>(0, rh - rl);
-      h.send_lo = sl - p->ew_lo;
-      h.send_n = std::max<int64_t>(0, sh - sl);
-      h.recv_bytes = h.recv_n * per_e;
-      h.send_bytes = h.send_n * per_e;
-      h.recv_off = p->recv_total;
-      h.send_off = p->send_total;
-      p->recv_total += h.recv_bytes;
-      p->send_total += h.send_bytes;
-      if (h.recv_n || h.send_n) p->peers.push_back(h);
-    }
-  } else {
-    rank_window(&d, nbr, d.rank, &p->a_lo, &p->a_hi, &p->w_lo, &p->w_hi);
-    p->e_lo = p->ew_lo = 0;
-    p->e_hi = p->ew_hi = d.NE;
-  }
-  p->NEw = p->ew_hi - p->ew_lo;
-  p->NEo = p->e_hi - p->e_lo;
-  p->E0 = p->e_lo - p->ew_lo;
-  // halo exchange plan: receive window atoms owned by peers, send owned atoms in the peers' windows
-  if (d.nranks > 1 && !p->eshard) {
-    const size_t per_atom = 2 * (size_t)d.Nkz * d.NE * d.Norb * d.Norb * 16 + 2 * (size_t)d.Nqz * d.Nw * (d.Nb + 1) * 9 * 16;
-    for (int r = 0; r < d.nranks; ++r) {
-      if (r == d.rank) continue;
-      int64_t alo, ahi, wlo, whi;
-      rank_window(&d, nbr, r, &alo, &ahi, &wlo, &whi);
-      HaloPeer h;
-      h.rank = r;
-      const int64_t rl = std::max(p->w_lo, alo), rh = std::min(p->w_hi, ahi);
-      const int64_t sl = std::max(p->a_lo, wlo), sh = std::min(p->a_hi, whi);
-      h.recv_lo = rl - p->w_lo;
-      h.recv_n = std::max<int64_t>(0, rh - rl);
-      h.send_lo = sl - p->w_lo;
-      h.send_n = std::max<int64_t>(0, sh - sl);
-      h.recv_bytes = h.recv_n * per_atom;
-      h.send_bytes = h.send_n * per_atom;
-      h.recv_off = p->recv_total;
-      h.send_off = p->send_total;
-      p->recv_total += h.recv_bytes;
-      p->send_total += h.send_bytes;
-      if (h.recv_n || h.send_n) p->peers.push_back(h);
-    }
-  }
-  p->Nwin = p->w_hi - p->w_lo;
-  p->Nout = p->a_hi - p->a_lo;
-  p->nbr_win.assign(p->Nwin * d.Nb, -1);
-  for (int64_t a = p->w_lo; a < p->w_hi; ++a)
-    for (int64_t s = 0; s < d.Nb; ++s) {
-      int32_t b = nbr[a * d.Nb + s];
-      if (b >= p->w_lo && b < p->w_hi) p->nbr_win[(a - p->w_lo) * d.Nb + s] = (int32_t)(b - p->w_lo);
-    }
-
-  // Σ work list: source-organized. For each source atom b, its reverse pairs (a,s) with a owned.
-  std::vector<SigPair> sp;
-  std::vector<int32_t> sp_item;
-  for (int64_t b = p->w_lo; b < p->w_hi; ++b) {
-    std::vector<SigPair> mine;
-    for (int64_t r = 0; r < d.Nb; ++r) {
-      int32_t a = nbr[b * d.Nb + r];
-      if (a < 0 || a < p->a_lo || a >= p->a_hi) continue;
-      SigPair q;
-      q.a = (int32_t)(a - p->a_lo);
-      q.a_in = (int32_t)(a - p->w_lo);
-      q.s = (int32_t)rev_slot(nbr, d.Nb, a, b);
-      q.r = (int32_t)r;
-      mine.push_back(q);
-    }
-    const size_t scap = d.precision == QT_PREC_FP32_MIXED ? kTcPiPairs : kMaxPairs;   // 126 / 72 GEMM rows
-    for (size_t k = 0; k < mine.size(); k += scap) {
-      SigItem it;
-      it.b_in = (int32_t)(b - p->w_lo);
-      it.b = (int32_t)b;
-      it.npair = (int32_t)std::min<size_t>(scap, mine.size() - k);
-      it.pair0 = (int32_t)sp.size();
-      for (int t = 0; t < it.npair; ++t) {
-        sp.push_back(mine[k + t]);
-        sp_item.push_back((int32_t)p->sig_items.size());
-      }
-      p->sig_items.push_back(it);
-    }
-  }
-  p->n_sig_pairs = (int64_t)sp.size();
-  // Π work list: destination-organized. For each owned atom a, its valid slots in chunks of 8.
-  std::vector<PiPair> pp;
-  std::vector<int32_t> pp_item;
-  for (int64_t a = p->a_lo; a < p->a_hi; ++a) {
-    std::vector<PiPair> mine;
-    for (int64_t s = 0; s < d.Nb; ++s) {
-      int32_t b = nbr[a * d.Nb + s];
-      if (b < 0) continue;
-      PiPair q;
-      q.s = (int32_t)s;
-      q.b_in = (int32_t)(b - p->w_lo);
-      q.r = (int32_t)rev_slot(nbr, d.Nb, b, a);
-      q.a_in = (int32_t)(a - p->w_lo);
-      mine.push_back(q);
-    }
-    const size_t cap = d.precision == QT_PREC_FP32_MIXED ? kTcPiPairs : kMaxPairs;   // 126 / 72 GEMM rows
-    for (size_t k = 0; k < mine.size(); k += cap) {
-      PiItem it;
-      it.a_out = (int32_t)(a - p->a_lo);
-      it.a_in = (int32_t)(a - p->w_lo);
-      it.npair = (int32_t)std::min<size_t>(cap, mine.size() - k);
-      it.pair0 = (int32_t)pp.size();
-      for (int t = 0; t < it.npair; ++t) {
-        pp.push_back(mine[k + t]);
-        pp_item.push_back((int32_t)p->pi_items.size());
-      }
-      p->pi_items.push_back(it);
-    }
-  }
-  p->n_pi_pairs = (int64_t)pp.size();
-  count_flops(&d, (double)p->n_pi_pairs, p->flops, p->e_lo, p->e_hi);
-
-  // workspace (shared by Σ coefficient tables and Π W scratch; the two calls never overlap)
-  const size_t coef_per_pair = (size_t)9 * d.Nqz * p->DWp * sizeof(double2);
-  // Π W scratch per item: complex tiles (FP64 mode) or four fp32 split planes (FP32 mode)
-  p->sig_rows = d.precision == QT_PREC_FP32_MIXED ? kTcRows : kRows;   // Gt rows per (item, kz, E)
-  const size_t gt_per_item = (size_t)d.Nkz * p->NEo * p->sig_rows * ((p->NN + 19) / 20) * 20 *
-                             (d.precision == QT_PREC_FP32_MIXED ? sizeof(float2) : sizeof(double2));
-  p->NNp = (p->NN + 3) & ~int64_t(3);
-  p->Epad = p->NEw + d.shift0 + 80 + 1;
-  const size_t w_per_item = d.precision == QT_PREC_FP32_MIXED
-                                ? (size_t)4 * kTcPiRows * d.Nkz * (((p->NEo * p->NNp + 31) / 32) * 32) * sizeof(float)
-                                : gt_per_item;
-  size_t budget = d.workspace_limit;
+  cudaGetDevice(&p->device);
+  const bool have_comm = desc->nranks > 1 && desc->nccl_unique_id != nullptr;
+  size_t budget = desc->workspace_limit;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-      qt_sse_destroy(p);
+      delete p;
       return QT_ERR_CUDA;
     }
-    budget = std::min<size_t>((size_t)(fr * 0.6), (size_t)48 << 30);
+    budget = std::min<size_t>((size_t)(fr * 0.6), kAutoWsCap);
   }
-  p->fp32 = d.precision == QT_PREC_FP32_MIXED;
-  p->NEp = std::max<int64_t>(32, (p->NEw + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
-  p->Kp = (p->Dwin + 3 + 31) & ~int64_t(31);   // delayed coefficient rows (d + s, s <= 3), whole 32-chunks
-  const size_t coef_item_t = p->fp32 ? (size_t)d.Nqz * 16 * kTcRows * p->Kp * sizeof(float)
-                                     : (size_t)d.Nqz * ((p->Dwin + 15) / 16) * kRows * kCoefKCP * sizeof(double2);
-  const size_t need_min = std::max(coef_per_pair * kMaxPairs, coef_item_t) + w_per_item + 512;
-  if (budget < need_min) budget = need_min;
-  const size_t full = std::max((coef_per_pair * kMaxPairs + coef_item_t + w_per_item) * p->sig_items.size() + 512,
-                               w_per_item * p->pi_items.size());
-  p->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
-  // chunk item ranges so that each chunk's pairs fit the workspace
-  // chunk item ranges so that each chunk's scratch fits the workspace (Σ: per pair; Π: per item)
-  auto make_chunks = [&](auto& items, size_t per_unit, bool per_pair, std::vector<int64_t>& bounds) {
-    const int64_t cap = (int64_t)(p->ws_bytes / per_unit);
-    bounds.clear();
-    bounds.push_back(0);
-    int64_t acc = 0;
-    for (size_t i = 0; i < items.size(); ++i) {
-      const int64_t u = per_pair ? items[i].npair : 1;
-      if (acc + u > cap) {
-        bounds.push_back((int64_t)i);
-        acc = 0;
-      }
-      acc += u;
-    }
-    bounds.push_back((int64_t)items.size());
+  if ((st = build_layout(desc, nbr, have_comm, budget, &p->L)) != QT_OK) {
+    delete p;
+    return st;
+  }
+  Layout& L = p->L;
+  auto fail = [&](qt_status s) {
+    qt_sse_destroy(p);
+    return s;
   };
-  make_chunks(p->pi_items, w_per_item, false, p->pi_chunks);
-  // Σ chunks. TMA path (Norb <= 10): per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] +
-  // its Gt scratch; cp.async path (Norb 11, 12): per pair coefficient rows. Workspace = [coef | Gt].
-  {
-    p->sig_tma = d.Norb <= 10;
-    p->ndc = (p->Dwin + 15) / 16;
-    const size_t coef_item = coef_item_t;
-    const size_t gt_item = p->sig_tma ? gt_per_item : 0;
-    p->sig_chunks.clear();
-    p->sig_chunks.push_back(0);
-    size_t coef_acc = 0, gt_acc = 0, coef_max = 0;
-    for (size_t i = 0; i < p->sig_items.size(); ++i) {
-      const size_t cu = p->sig_tma ? coef_item : (size_t)p->sig_items[i].npair * coef_per_pair;
-      if (gt_acc > 0 && coef_acc + cu + gt_acc + gt_item + 256 > p->ws_bytes) {
-        p->sig_chunks.push_back((int64_t)i);
-        coef_max = std::max(coef_max, coef_acc);
-        coef_acc = 0;
-        gt_acc = 0;
-      }
-      coef_acc += cu;
-      gt_acc += gt_item == 0 ? 1 : gt_item;
-    }
-    coef_max = std::max(coef_max, coef_acc);
-    p->sig_chunks.push_back((int64_t)p->sig_items.size());
-    p->gt_offset = (coef_max + 255) & ~size_t(255);
-  }
-
   qt_status s2;
-  if ((s2 = upload(&p->d_nbr_win, p->nbr_win, cs)) != QT_OK || (s2 = upload(&p->d_sig_items, p->sig_items, cs)) != QT_OK ||
-      (s2 = upload(&p->d_sig_pairs, sp, cs)) != QT_OK || (s2 = upload(&p->d_sig_pair_item, sp_item, cs)) != QT_OK ||
-      (s2 = upload(&p->d_pi_items, p->pi_items, cs)) != QT_OK || (s2 = upload(&p->d_pi_pairs, pp, cs)) != QT_OK ||
-      (s2 = upload(&p->d_pi_pair_item, pp_item, cs)) != QT_OK) {
-    qt_sse_destroy(p);
-    return s2;
-  }
-  p->g_elems = (size_t)d.Nkz * p->NEw * p->Nwin * p->NN;
-  if (cudaMalloc(&p->ws_g, 2 * p->g_elems * sizeof(double2)) != cudaSuccess ||
-      cudaMalloc(&p->ws_gs, 2 * p->gs_elems() * sizeof(double)) != cudaSuccess ||
-      (p->fp32 && cudaMalloc(&p->ws_gtp, 2 * p->gtp_elems() * sizeof(float)) != cudaSuccess) ||
-      (p->fp32 && cudaMalloc(&p->ws_gpi, p->gpi_elems() * sizeof(float)) != cudaSuccess)) {
-    qt_sse_destroy(p);
-    return QT_ERR_OUT_OF_MEMORY;
-  }
+  if ((s2 = upload(&p->d_nbr_win, L.nbr_win, cs)) != QT_OK || (s2 = upload(&p->d_sig_items, L.sig_items, cs)) != QT_OK ||
+      (s2 = upload(&p->d_sig_pairs, L.sig_pairs, cs)) != QT_OK ||
+      (s2 = upload(&p->d_sig_pair_item, L.sig_pair_item, cs)) != QT_OK ||
+      (s2 = upload(&p->d_pi_items, L.pi_items, cs)) != QT_OK || (s2 = upload(&p->d_pi_pairs, L.pi_pairs, cs)) != QT_OK ||
+      (s2 = upload(&p->d_pi_pair_item, L.pi_pair_item, cs)) != QT_OK)
+    return fail(s2);
+  if ((!L.fp32 && cudaMalloc(&p->ws_gs, 2 * L.gs_elems() * sizeof(double)) != cudaSuccess) ||
+      (L.fp32 && cudaMalloc(&p->ws_gtp, 2 * L.gtp_elems() * sizeof(float)) != cudaSuccess) ||
+      (L.fp32 && cudaMalloc(&p->ws_gpi, L.gpi_elems() * sizeof(float)) != cudaSuccess))
+    return fail(QT_ERR_OUT_OF_MEMORY);
   // the odd-NN padding element of each sum-plane row is never written by k_relayout: keep it a finite zero
-  if (cudaMemsetAsync(p->ws_gs, 0, 2 * p->gs_elems() * sizeof(double), cs) != cudaSuccess) {
-    qt_sse_destroy(p);
-    return QT_ERR_CUDA;
-  }
-  if (d.nranks > 1 && d.nccl_unique_id) {
-    if ((p->send_total && cudaMalloc(&p->sendbuf, p->send_total) != cudaSuccess) ||
-        (p->recv_total && cudaMalloc(&p->recvbuf, p->recv_total) != cudaSuccess)) {
-      qt_sse_destroy(p);
-      return QT_ERR_OUT_OF_MEMORY;
-    }
-    if (nccl_comm_init(&p->comm, d.nranks, d.nccl_unique_id, d.rank) != 0) {
-      qt_sse_destroy(p);
-      return QT_ERR_NCCL;
-    }
+  if (p->ws_gs && cudaMemsetAsync(p->ws_gs, 0, 2 * L.gs_elems() * sizeof(double), cs) != cudaSuccess)
+    return fail(QT_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming) != cudaSuccess) return fail(QT_ERR_CUDA);
+  if (have_comm) {
+    if ((L.send_total && cudaMalloc(&p->sendbuf, L.send_total) != cudaSuccess) ||
+        (L.recv_total && cudaMalloc(&p->recvbuf, L.recv_total) != cudaSuccess))
+      return fail(QT_ERR_OUT_OF_MEMORY);
+    if (L.reduce && (cudaMalloc(&p->part[0], L.part_bytes) != cudaSuccess || cudaMalloc(&p->part[1], L.part_bytes) != cudaSuccess))
+      return fail(QT_ERR_OUT_OF_MEMORY);
+    if (cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking) != cudaSuccess) return fail(QT_ERR_CUDA);
+    cudaEvent_t* evs[] = {&p->ev_in, &p->ev_halo, &p->ev_part[0], &p->ev_part[1], &p->ev_red[0], &p->ev_red[1]};
+    for (cudaEvent_t* e : evs)
+      if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(QT_ERR_CUDA);
+    if (nccl_comm_init(&p->comm, desc->nranks, desc->nccl_unique_id, desc->rank) != 0) return fail(QT_ERR_NCCL);
+    if (L.g.TE > 1 && nccl_comm_split(p->comm, L.g.ta, L.g.te, &p->comm_e) != 0) return fail(QT_ERR_NCCL);
   }
   // + slack: the last Π stage of a chunk may read one energy block past the chunk (its results are unused)
-  if (cudaMalloc(&p->ws, p->ws_bytes + (1 << 20)) != cudaSuccess) {
-    qt_sse_destroy(p);
-    return QT_ERR_OUT_OF_MEMORY;
-  }
+  if (cudaMalloc(&p->ws, L.ws_bytes + (1 << 20)) != cudaSuccess) return fail(QT_ERR_OUT_OF_MEMORY);
   // zero once: padding columns of the Π W tiles are never written and must hold finite values
-  if (cudaMemsetAsync(p->ws, 0, p->ws_bytes + (1 << 20), cs) != cudaSuccess) {
-    qt_sse_destroy(p);
-    return QT_ERR_CUDA;
-  }
-  if (cudaStreamSynchronize(cs) != cudaSuccess) {
-    qt_sse_destroy(p);
-    return QT_ERR_CUDA;
-  }
+  if (cudaMemsetAsync(p->ws, 0, L.ws_bytes + (1 << 20), cs) != cudaSuccess) return fail(QT_ERR_CUDA);
+  if (cudaStreamSynchronize(cs) != cudaSuccess) return fail(QT_ERR_CUDA);
   *out = p;
   return QT_OK;
 }
 
 extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
   if (!p || !o) return QT_ERR_INVALID_ARG;
-  o->a_lo = p->a_lo;
-  o->a_hi = p->a_hi;
-  o->w_lo = p->w_lo;
-  o->w_hi = p->w_hi;
-  o->npairs = p->n_pi_pairs;
-  o->workspace_bytes = p->ws_bytes + 2 * p->g_elems * sizeof(double2) + 2 * p->gs_elems() * sizeof(double);
-  o->flops_sigma = p->flops[0] + p->flops[1];
-  o->flops_pi = p->flops[2] + p->flops[3];
-  o->halo_bytes = (double)p->recv_total;
-  o->e_lo = p->e_lo;
-  o->e_hi = p->e_hi;
-  o->ew_lo = p->ew_lo;
-  o->ew_hi = p->ew_hi;
+  const Layout& L = p->L;
+  size_t gsb = L.fp32 ? 2 * L.gtp_elems() * 4 + L.gpi_elems() * 4 : 2 * L.gs_elems() * 8;
+  fill_info(L, L.ws_bytes + gsb + L.send_total + L.recv_total + 2 * L.part_bytes, o);
+  QT_TRY(nccl_check(p));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? QT_OK : cuda_status(e);
 }
@@ -660,191 +1063,55 @@ extern "C" qt_status qt_sse_query(qt_sse_plan_t p, qt_sse_info* o) {
 extern "C" qt_status qt_sse_sigma(qt_sse_plan_t p, const void* dH, const void* GL, const void* GG, const void* DL,
                                   const void* DG, double sre, double sim, void* SL, void* SG, void* stream) {
   if (!p) return QT_ERR_INVALID_ARG;
-  const void* ins[] = {dH, GL, GG, DL, DG};
-  for (const void* q : ins)
-    if (!aligned16(q)) return QT_ERR_INVALID_ARG;
-  if (!aligned16(SL) || !aligned16(SG) || SL == SG) return QT_ERR_INVALID_ARG;
-  for (const void* q : ins)
-    if (q == SL || q == SG) return QT_ERR_INVALID_ARG;
+  QT_TRY(check_ptrs({dH, GL, GG, DL, DG}, {SL, SG}));
   cudaStream_t cs = (cudaStream_t)stream;
-  const qt_sse_desc& d = p->d;
-  const size_t sig_bytes = (size_t)d.Nkz * p->NEo * p->Nout * p->NN * sizeof(double2);
-  if (p->fp32) {
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GL, p->ws_gtp, d.Nkz, p->NEw, p->NEp, p->Nwin, (int)p->NN, cs));
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_tc((const double2*)GG, p->ws_gtp + p->gtp_elems(), d.Nkz, p->NEw, p->NEp, p->Nwin,
-                                                (int)p->NN, cs));
-  } else {
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, p->NEw, p->Nwin, p->NN, cs));
-    QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, p->NEw, p->Nwin, p->NN, cs));
-  }
-  for (int X = 0; X < 2; ++X) {
-    void* S = X == 0 ? SL : SG;
-    QT_CUDA(cudaMemsetAsync(S, 0, sig_bytes, cs));
-    for (size_t c = 0; c + 1 < p->sig_chunks.size(); ++c) {
-      const int64_t i0 = p->sig_chunks[c], i1 = p->sig_chunks[c + 1];
-      if (i1 <= i0) continue;
-      const int64_t pp0 = p->sig_items[i0].pair0;
-      const int64_t pp1 = p->sig_items[i1 - 1].pair0 + p->sig_items[i1 - 1].npair;
-      CoefArgs ca;
-      ca.DX = (const double2*)(X == 0 ? DL : DG);
-      ca.DY = (const double2*)(X == 0 ? DG : DL);
-      ca.pairs = p->d_sig_pairs + pp0;
-      ca.items = p->d_sig_items;
-      ca.pair_item = p->d_sig_pair_item + pp0;
-      ca.coef = p->ws;
-      ca.npairs = pp1 - pp0;
-      ca.Nw = d.Nw;
-      ca.Nwin = p->Nwin;
-      ca.Nb = d.Nb;
-      ca.Nqz = d.Nqz;
-      ca.DWp = p->DWp;
-      ca.Dmax = (int)p->Dmax;
-      ca.shift0 = d.shift0;
-      ca.tiled = p->sig_tma;
-      ca.item0 = i0;
-      ca.nitems = i1 - i0;
-      ca.ndc = p->ndc;
-      ca.Dwin = p->Dwin;
-      QT_LAUNCH(QT_K_SIGMA_COEF, p->fp32      ? launch_sigma_coef_tc(ca, (int)p->Kp, cs)
-                                 : p->sig_tma ? launch_sigma_coef_tiled(ca, cs)
-                                              : launch_sigma_coef(ca, cs));
-      SigmaArgs sa;
-      sa.G = (const double2*)(X == 0 ? GL : GG);
-      sa.Gam = p->ws_g + (X == 0 ? 0 : p->g_elems);
-      sa.Gsum = p->ws_gs + (X == 0 ? 0 : p->gs_elems());
-      sa.coef = p->ws;
-      sa.Gt = reinterpret_cast<double2*>(reinterpret_cast<char*>(p->ws) + p->gt_offset);
-      sa.cp0 = pp0;
-      sa.npairs_chunk = pp1 - pp0;
-      sa.dH = (const double2*)dH;
-      sa.items = p->d_sig_items + i0;
-      sa.pairs = p->d_sig_pairs;
-      sa.Sig = (double2*)S;
-      sa.scale = make_double2(sre, sim);
-      sa.Nwin = p->Nwin;
-      sa.Nout = p->Nout;
-      sa.Nb = d.Nb;
-      sa.DWp = p->DWp;
-      sa.NE = (int)p->NEw;
-      sa.E0 = (int)p->E0;
-      sa.NEo = (int)p->NEo;
-      sa.Nkz = (int)d.Nkz;
-      sa.Nqz = (int)d.Nqz;
-      sa.h = (int)p->h;
-      sa.Norb = (int)d.Norb;
-      sa.NN = (int)p->NN;
-      sa.Dmax = (int)p->Dmax;
-      sa.ndc = (int)p->ndc;
-      sa.Dwin = (int)p->Dwin;
-      sa.rows = (int)p->sig_rows;
-      sa.gt_f32 = p->fp32 ? 1 : 0;
-      if (p->fp32) {
-        QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : p->gtp_elems()), p->NEp,
-                                              reinterpret_cast<const float*>(p->ws), (int)p->Kp, i1 - i0, cs));
-      } else {
-        QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
-      }
-      QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
-    }
-  }
-  return QT_OK;
+  QT_TRY(call_begin(p, cs));
+  QT_TRY(relayout_sigma(p, GL, GG, 0, p->L.Nwin, cs));
+  bool done = true;
+  QT_TRY(run_sigma(p, dH, GL, GG, DL, DG, sre, sim, SL, SG, cs, nullptr, &done));
+  return call_end(p, cs);
 }
 
 extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, const void* GG, double sre,
                                double sim, void* PL, void* PG, void* stream) {
   if (!p) return QT_ERR_INVALID_ARG;
-  const void* ins[] = {dH, GL, GG};
-  for (const void* q : ins)
-    if (!aligned16(q)) return QT_ERR_INVALID_ARG;
-  if (!aligned16(PL) || !aligned16(PG) || PL == PG) return QT_ERR_INVALID_ARG;
-  for (const void* q : ins)
-    if (q == PL || q == PG) return QT_ERR_INVALID_ARG;
+  QT_TRY(check_ptrs({dH, GL, GG}, {PL, PG}));
   cudaStream_t cs = (cudaStream_t)stream;
-  const qt_sse_desc& d = p->d;
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GL, p->ws_g, p->ws_gs, d.Nkz, p->NEw, p->Nwin, p->NN, cs));
-  QT_LAUNCH(QT_K_RELAYOUT, launch_relayout((const double2*)GG, p->ws_g + p->g_elems, p->ws_gs + p->gs_elems(), d.Nkz, p->NEw, p->Nwin, p->NN, cs));
-  for (int X = 0; X < 2; ++X) {
-    const double2* GXam = p->ws_g + (X == 0 ? 0 : p->g_elems);
-    const double2* GY = (const double2*)(X == 0 ? GG : GL);
-    double2* P = (double2*)(X == 0 ? PL : PG);
-    if (p->fp32)
-      QT_LAUNCH(QT_K_RELAYOUT, launch_relayout_pi_tc((const double2*)(X == 0 ? GL : GG), p->ws_gpi, d.Nkz, p->NEw, p->Epad,
-                                                     p->Nwin, (int)p->NN, (int)p->NNp, cs));
-    for (size_t c = 0; c + 1 < p->pi_chunks.size(); ++c) {
-      const int64_t i0 = p->pi_chunks[c], i1 = p->pi_chunks[c + 1];
-      if (i1 <= i0) continue;
-      const int64_t pp0 = p->pi_items[i0].pair0;
-      const int64_t pp1 = p->pi_items[i1 - 1].pair0 + p->pi_items[i1 - 1].npair;
-      PiWArgs wa;
-      wa.GY = GY;
-      wa.GYam = p->ws_g + (X == 0 ? p->g_elems : 0);
-      wa.dH = (const double2*)dH;
-      wa.pairs = p->d_pi_pairs;
-      wa.items = p->d_pi_items;
-      wa.pair_item = p->d_pi_pair_item;
-      wa.W = p->ws;
-      wa.p0 = pp0;
-      wa.i0 = i0;
-      wa.Nwin = p->Nwin;
-      wa.Nb = d.Nb;
-      wa.NE = (int)p->NEw;
-      wa.E0 = (int)p->E0;
-      wa.NEo = (int)p->NEo;
-      wa.Nkz = (int)d.Nkz;
-      wa.Norb = (int)d.Norb;
-      wa.NN = (int)p->NN;
-      wa.nEB = (int)((p->NEw + kEB - 1) / kEB);
-      if (p->fp32) {
-        QT_LAUNCH(QT_K_PI_W, launch_pi_w_tc(wa, reinterpret_cast<float*>(p->ws), (int)p->NNp, i1 - i0, cs));
-      } else {
-        QT_LAUNCH(QT_K_PI_W, launch_pi_w(wa, i1 - i0, cs));
-      }
-      PiCArgs ca;
-      ca.GX = GXam;
-      ca.W = p->ws;
-      ca.GXsum = p->ws_gs + (X == 0 ? 0 : p->gs_elems());
-      ca.items = p->d_pi_items;
-      ca.pairs = p->d_pi_pairs;
-      ca.Pi = P;
-      ca.scale = make_double2(sre, sim);
-      ca.i0 = i0;
-      ca.nitems = i1 - i0;
-      ca.Nwin = p->Nwin;
-      ca.Nout = p->Nout;
-      ca.Nb = d.Nb;
-      ca.NE = (int)p->NEw;
-      ca.E0 = (int)p->E0;
-      ca.NEo = (int)p->NEo;
-      ca.Nkz = (int)d.Nkz;
-      ca.Nqz = (int)d.Nqz;
-      ca.h = (int)p->h;
-      ca.NN = (int)p->NN;
-      ca.Nw = (int)d.Nw;
-      ca.NWP = (int)p->NWP;
-      ca.shift0 = d.shift0;
-      if (p->fp32) {
-        QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract_tc(ca, reinterpret_cast<const float*>(p->ws), p->ws_gpi, p->Epad,
-                                                          (int)p->NNp, i1 - i0, cs));
-      } else {
-        QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
-      }
-    }
-    PiSelfArgs sa;
-    sa.Pi = P;
-    sa.nbr = p->d_nbr_win;
-    sa.Nout = p->Nout;
-    sa.Nb = d.Nb;
-    sa.Nqz = d.Nqz;
-    sa.Nw = d.Nw;
-    sa.a_off = p->a_lo - p->w_lo;
-    QT_LAUNCH(QT_K_PI_SELF, launch_pi_self(sa, cs));
-    if (p->eshard) {   // Π is a sum over energies: add the ranks' partial sums (NCCL over NVLink)
-      if (!p->comm) return QT_ERR_UNSUPPORTED;
-      const size_t n = (size_t)d.Nqz * d.Nw * p->Nout * (d.Nb + 1) * 9 * 2;
-      if (nccl_allreduce_sum(p->comm, reinterpret_cast<double*>(P), n, cs) != 0) return QT_ERR_NCCL;
-    }
+  QT_TRY(call_begin(p, cs));
+  if (!p->L.fp32) QT_TRY(relayout_sigma(p, GL, GG, 0, p->L.Nwin, cs));   // Re+Im planes of G^X_a (Π correlation)
+  QT_TRY(run_pi(p, dH, GL, GG, sre, sim, PL, PG, cs));
+  return call_end(p, cs);
+}
+
+extern "C" qt_status qt_sse_sigma_pi(qt_sse_plan_t p, const void* dH, void* GL, void* GG, void* DL, void* DG,
+                                     double ssre, double ssim, double psre, double psim, void* SL, void* SG, void* PL,
+                                     void* PG, void* stream) {
+  if (!p) return QT_ERR_INVALID_ARG;
+  QT_TRY(check_ptrs({dH, GL, GG, DL, DG}, {SL, SG, PL, PG}));
+  cudaStream_t cs = (cudaStream_t)stream;
+  QT_TRY(call_begin(p, cs));
+  const Layout& L = p->L;
+  cudaEvent_t halo = nullptr;
+  bool halo_done = true;
+  if (p->comm && !L.peers.empty()) {
+    // the exchange runs on the communication stream once the caller's inputs are ready (stream order)
+    QT_CUDA(cudaEventRecord(p->ev_in, cs));
+    QT_CUDA(cudaStreamWaitEvent(p->cstream, p->ev_in, 0));
+    QT_TRY(exchange(p, GL, GG, DL, DG, p->cstream));
+    QT_CUDA(cudaEventRecord(p->ev_halo, p->cstream));
+    halo = p->ev_halo;
+    halo_done = false;
+    if (L.g.TE == 1) QT_TRY(relayout_sigma(p, GL, GG, L.g.a_lo - L.g.w_lo, L.g.a_hi - L.g.w_lo, cs));   // owned atoms
+  } else {
+    QT_TRY(relayout_sigma(p, GL, GG, 0, L.Nwin, cs));
   }
-  return QT_OK;
+  QT_TRY(run_sigma(p, dH, GL, GG, DL, DG, ssre, ssim, SL, SG, cs, halo, &halo_done));
+  if (!halo_done) {   // no Σ chunk read the halo (e.g. no pairs): Π still needs it
+    QT_CUDA(cudaStreamWaitEvent(cs, halo, 0));
+    QT_TRY(relayout_sigma(p, GL, GG, 0, L.Nwin, cs));
+  }
+  QT_TRY(run_pi(p, dH, GL, GG, psre, psim, PL, PG, cs));
+  return call_end(p, cs);
 }
 
 extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const void* GL, const void* GG,
@@ -852,14 +1119,16 @@ extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const 
                                          double psim, void* SL, void* SG, void* PL, void* PG, void* stream) {
   if (!p || !dH || !GL || !GG || !DL || !DG || !SL || !SG || !PL || !PG) return QT_ERR_INVALID_ARG;
   cudaStream_t cs = (cudaStream_t)stream;
-  const qt_sse_desc& d = p->d;
-  const size_t b_dH = (size_t)p->Nwin * d.Nb * 3 * p->NN * 16;
-  const size_t b_G = (size_t)d.Nkz * p->NEw * p->Nwin * p->NN * 16;
-  const size_t b_D = (size_t)d.Nqz * d.Nw * p->Nwin * (d.Nb + 1) * 9 * 16;
-  const size_t b_S = (size_t)d.Nkz * p->NEo * p->Nout * p->NN * 16;
-  const size_t b_P = (size_t)d.Nqz * d.Nw * p->Nout * (d.Nb + 1) * 9 * 16;
+  const Layout& L = p->L;
+  const qt_sse_desc& d = L.d;
+  const size_t b_dH = (size_t)L.Nwin * d.Nb * 3 * L.NN * 16;
+  const size_t b_G = (size_t)d.Nkz * L.NEw * L.Nwin * L.NN * 16;
+  const size_t b_D = (size_t)L.Nwin * d_block_bytes(d);
+  const size_t b_S = (size_t)d.Nkz * L.NEo * L.Nout * L.NN * 16;
+  const size_t b_P = (size_t)(L.g.pa_hi - L.g.pa_lo) * d_block_bytes(d);
   const size_t total = b_dH + 2 * b_G + 2 * b_D + 2 * b_S + 2 * b_P;
   if (p->h_dev_bytes < total) {
+    if (p->has_last) cudaEventSynchronize(p->ev_done);
     cudaFree(p->h_dev);
     p->h_dev = nullptr;
     p->h_dev_bytes = 0;
@@ -874,51 +1143,25 @@ extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const 
   QT_CUDA(cudaMemcpyAsync(dGG, GG, b_G, cudaMemcpyHostToDevice, cs));
   QT_CUDA(cudaMemcpyAsync(dDL, DL, b_D, cudaMemcpyHostToDevice, cs));
   QT_CUDA(cudaMemcpyAsync(dDG, DG, b_D, cudaMemcpyHostToDevice, cs));
-  qt_status st = qt_sse_sigma(p, ddH, dGL, dGG, dDL, dDG, ssre, ssim, dSL, dSG, stream);
-  if (st != QT_OK) return st;
-  st = qt_sse_pi(p, ddH, dGL, dGG, psre, psim, dPL, dPG, stream);
-  if (st != QT_OK) return st;
+  QT_TRY(qt_sse_sigma_pi(p, ddH, dGL, dGG, dDL, dDG, ssre, ssim, psre, psim, dSL, dSG, dPL, dPG, stream));
   QT_CUDA(cudaMemcpyAsync(SL, dSL, b_S, cudaMemcpyDeviceToHost, cs));
   QT_CUDA(cudaMemcpyAsync(SG, dSG, b_S, cudaMemcpyDeviceToHost, cs));
   QT_CUDA(cudaMemcpyAsync(PL, dPL, b_P, cudaMemcpyDeviceToHost, cs));
   QT_CUDA(cudaMemcpyAsync(PG, dPG, b_P, cudaMemcpyDeviceToHost, cs));
   QT_CUDA(cudaStreamSynchronize(cs));
+  QT_TRY(nccl_check(p));
   return QT_OK;
 }
 
 extern "C" qt_status qt_sse_halo_exchange(qt_sse_plan_t p, void* GL, void* GG, void* DL, void* DG, void* stream) {
   if (!p) return QT_ERR_INVALID_ARG;
-  if (p->d.nranks == 1) return QT_OK;
-  if (!p->comm) return QT_ERR_UNSUPPORTED;   // planned without an NCCL unique id
-  void* ts[4] = {GL, GG, DL, DG};
-  for (void* t : ts)
-    if (!aligned16(t)) return QT_ERR_INVALID_ARG;
+  if (p->L.d.nranks == 1) return QT_OK;
+  if (!p->comm) return QT_ERR_UNSUPPORTED;   // loopback plan (no NCCL unique id)
+  QT_TRY(check_ptrs({GL, GG, DL, DG}, {}));
   cudaStream_t cs = (cudaStream_t)stream;
-  const qt_sse_desc& d = p->d;
-  // atom sharding: G≷ [Nkz·NE][atoms][NN] and D≷ [Nqz·Nω][atoms][Nb+1][9] along atoms; energy sharding:
-  // G≷ [Nkz][energies][Na·NN] along energies (D≷ replicated)
-  const int nt = p->eshard ? 2 : 4;
-  const int64_t outer[4] = {p->eshard ? d.Nkz : d.Nkz * d.NE, p->eshard ? d.Nkz : d.Nkz * d.NE, d.Nqz * d.Nw,
-                            d.Nqz * d.Nw};
-  const int64_t inner[4] = {p->eshard ? d.Na * p->NN * 16 : p->NN * 16, p->eshard ? d.Na * p->NN * 16 : p->NN * 16,
-                            (d.Nb + 1) * 9 * 16, (d.Nb + 1) * 9 * 16};
-  const int64_t span = p->eshard ? p->NEw : p->Nwin;
-  for (const HaloPeer& h : p->peers) {
-    size_t off = h.send_off;
-    for (int k = 0; k < nt; ++k) {
-      QT_LAUNCH(QT_K_HALO, launch_pack(ts[k], p->sendbuf + off, outer[k], span, h.send_lo, h.send_n, inner[k], false, cs));
-      off += (size_t)outer[k] * h.send_n * inner[k];
-    }
-  }
-  if (nccl_exchange(p->comm, p->peers, p->sendbuf, p->recvbuf, cs) != 0) return QT_ERR_NCCL;
-  for (const HaloPeer& h : p->peers) {
-    size_t off = h.recv_off;
-    for (int k = 0; k < nt; ++k) {
-      QT_LAUNCH(QT_K_HALO, launch_pack(p->recvbuf + off, ts[k], outer[k], span, h.recv_lo, h.recv_n, inner[k], true, cs));
-      off += (size_t)outer[k] * h.recv_n * inner[k];
-    }
-  }
-  return QT_OK;
+  QT_TRY(call_begin(p, cs));
+  QT_TRY(exchange(p, GL, GG, DL, DG, cs));
+  return call_end(p, cs);
 }
 
 extern "C" qt_status qt_sse_timing_enable(qt_sse_plan_t p, int enable) {

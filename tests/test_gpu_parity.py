@@ -30,14 +30,14 @@ def to_dev(inp):
     return {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
 
 
-def gpu_run(p, inp, ss=1j, ps=-1j):
-    out = qt.run(p, to_dev(inp), ss, ps)
+def gpu_run(p, inp, ss=1j, ps=-1j, **kw):
+    out = qt.run(p, to_dev(inp), ss, ps, **kw)
     torch.cuda.synchronize()
     return {k: v.cpu().numpy() for k, v in out.items()}
 
 
-def check_full(p, inp, ss=1j, ps=-1j, exact=False):
-    g = gpu_run(p, inp, ss, ps)
+def check_full(p, inp, ss=1j, ps=-1j, exact=False, **kw):
+    g = gpu_run(p, inp, ss, ps, **kw)
     SL, SG = oracle.sigma(p, inp, ss)
     PL, PG = oracle.pi(p, inp, ps)
     pairs = ((g["S_less"], SL), (g["S_gtr"], SG), (g["P_less"], PL), (g["P_gtr"], PG))
@@ -78,6 +78,37 @@ def test_parity_tiny_config():
     p = qtgen.problem("tiny")
     check_full(p, inputs(p))
     check_full(p, inputs(p, mode=qtgen.INTEGER), ss=1j, ps=1.0, exact=True)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("prec", [qt.QT_PREC_FP64, qt.QT_PREC_FP32_MIXED])
+def test_parity_multichunk_workspace(fused, prec):
+    """workspace_limit = 1 byte (clamped to one item's scratch): Σ and Π run as many chunks (the chunk offsets
+    cp0 / pp0 / i0 that the BASELINE sizes reach), through the separate and the fused calls."""
+    tol = 1e-12 if prec == qt.QT_PREC_FP64 else 1e-5
+    for p in (qtgen.problem("tiny"), micro(Na=14, Nb=12, Norb=3, NE=12, Nw=3, Nkz=3, fill=0.9, seed=5)):
+        n0 = qt.launch_count()
+        g = gpu_run(p, inputs(p, seed=21), fused=fused, workspace_limit=1, precision=prec)
+        nl = qt.launch_count() - n0
+        assert nl >= 2 * 3 * 3 + 2 * 3 * 2, nl   # >= 3 Σ chunks (3 launches) and 3 Π chunks (2) per X
+        SL, SG = oracle.sigma(p, inputs(p, seed=21), 1j)
+        PL, PG = oracle.pi(p, inputs(p, seed=21), -1j)
+        for got, ref in ((g["S_less"], SL), (g["S_gtr"], SG), (g["P_less"], PL), (g["P_gtr"], PG)):
+            assert rel_fro(got, ref, AX) <= tol
+        inp = inputs(p, mode=qtgen.INTEGER, seed=22)
+        g = gpu_run(p, inp, 1.0, 1j, fused=fused, workspace_limit=1, precision=prec)
+        SL, SG = oracle.sigma(p, inp, 1.0)
+        PL, PG = oracle.pi(p, inp, 1j)
+        for got, ref in ((g["S_less"], SL), (g["S_gtr"], SG), (g["P_less"], PL), (g["P_gtr"], PG)):
+            assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("cfg", range(len(MICROS)))
+def test_parity_fused_call(cfg):
+    """qt_sse_sigma_pi (one re-layout shared by Σ and Π) == the oracle, like the separate calls."""
+    p = micro(**MICROS[cfg])
+    check_full(p, inputs(p, seed=700 + cfg), fused=True)
+    check_full(p, inputs(p, mode=qtgen.INTEGER, seed=800 + cfg), ss=1.0, ps=1j, exact=True, fused=True)
 
 
 @pytest.mark.parametrize("Norb", list(range(1, 13)))
@@ -185,6 +216,14 @@ def test_small_config_sampled_random():
 
 def test_small_config_sampled_integer():
     _sampled_parity(qtgen.problem("small"), qtgen.INTEGER, 96, 96, exact=True)
+
+
+@pytest.mark.slow
+def test_small_config_full_oracle():
+    """BASELINE 'small' nanowire slice, EVERY Σ and Π block against the full oracle (≈16 Tflop of plain-loop
+    oracle work), through the fused call in the bench launch configuration (default workspace)."""
+    p = qtgen.problem("small")
+    check_full(p, qtgen.host_inputs(p, qtgen.RANDOM), fused=True)
 
 
 @pytest.mark.slow

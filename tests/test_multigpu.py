@@ -1,6 +1,6 @@
-"""Multi-GPU (atom sharding + NCCL halo exchange) parity: runs tests/mgpu_worker.py under torchrun on
-2 GPUs (skipped when fewer are visible); the sharded result must equal the unsharded one."""
-import os
+"""Multi-GPU parity over real NCCL (halo exchange inside qt_sse_sigma_pi, Π reduction to sub-slab owners): runs
+tests/mgpu_worker.py under torchrun on 2 (or 4) GPUs, skipped when fewer are visible. The same sharded kernels
+are covered on ONE GPU by tests/test_gpu_loopback.py."""
 import socket
 import subprocess
 import sys
@@ -20,21 +20,31 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("cfg,mode,prec,shard", [("small", "integer", "fp64", "atom"), ("small", "random", "fp64", "atom"),
-                                                 ("prof", "integer", "fp64", "atom"), ("small", "random", "fp32", "atom"),
-                                                 ("prof", "integer", "fp32", "atom"),
-                                                 ("small", "integer", "fp64", "energy"),
-                                                 ("small", "random", "fp64", "energy"),
-                                                 ("prof", "integer", "fp64", "energy"),
-                                                 ("small", "integer", "fp32", "energy"),
-                                                 ("prof", "random", "fp32", "energy")])
-def test_sharded_matches_unsharded(cfg, mode, prec, shard):
-    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
-    if n < 2:
-        pytest.skip("needs 2 GPUs")
+def _run(n, args):
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < n:
+        pytest.skip(f"needs {n} GPUs")
     root = Path(__file__).resolve().parent.parent
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(root / "tests" / "mgpu_worker.py"), cfg, mode, prec, shard]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(root / "tests" / "mgpu_worker.py"), *args]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "mgpu ok" in r.stdout
+
+
+@pytest.mark.parametrize("cfg,mode,prec,shard,call", [
+    ("small", "integer", "fp64", "atom", "fused"), ("small", "random", "fp64", "atom", "separate"),
+    ("prof", "integer", "fp64", "atom", "fused"), ("small", "random", "fp32", "atom", "fused"),
+    ("prof", "integer", "fp32", "atom", "separate"),
+    ("small", "integer", "fp64", "energy", "fused"), ("small", "random", "fp64", "energy", "separate"),
+    ("prof", "integer", "fp64", "energy", "fused"), ("small", "integer", "fp32", "energy", "fused"),
+    ("prof", "random", "fp32", "energy", "fused")])
+def test_sharded_matches_unsharded_2gpu(cfg, mode, prec, shard, call):
+    _run(2, [cfg, mode, prec, shard, "0", call])
+
+
+@pytest.mark.parametrize("cfg,mode,prec", [("small", "integer", "fp64"), ("prof", "random", "fp64"),
+                                           ("small", "integer", "fp32")])
+def test_2d_grid_matches_unsharded_4gpu(cfg, mode, prec):
+    """Ta x TE = 2 x 2: packed atom+energy halo boxes, D halo within the energy row, Π reduced per atom slab."""
+    _run(4, [cfg, mode, prec, "2d", "2", "fused"])

@@ -167,3 +167,104 @@ def test_per_rank_flops_partition_the_total(nranks):
         if shard == qt.QT_SHARD_ENERGY:
             assert [i["e_lo"] for i in infos][0] == 0 and infos[-1]["e_hi"] == p.NE
             assert all(infos[r]["e_hi"] == infos[r + 1]["e_lo"] for r in range(nranks - 1))
+
+
+def _gworker(rank, world, ga, port, result_q):
+    """Ta x TE grid (the paper's 2-D tiling): the oracle on this rank's window (atom window x energy
+    window) reproduces its owned Σ block; Π of the rank is its partial sum over its OWN energies (emulated here by
+    zeroing the G^Y_b energies the rank does not own), and the partials of a slab's TE ranks add up to Π."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1912_10024_b200 as qt
+    p = qtgen.problem("tiny")
+    inp = qtgen.host_inputs(p, qtgen.INTEGER)
+    # loopback geometry (no communicator: Π output = the partial of the whole slab)
+    i = qt.shard_info(p, rank, world, shard=qt.QT_SHARD_2D, grid_atoms=ga)
+    assert (i["Ta"], i["TE"]) == (ga, world // ga) and i["ta"] * i["TE"] + i["te"] == rank
+    w_lo, w_hi, ew_lo, ew_hi = i["w_lo"], i["w_hi"], i["ew_lo"], i["ew_hi"]
+    wp = _window_problem(p, w_lo, w_hi)
+    wp = Problem(wp.nbr, p.Norb, ew_hi - ew_lo, p.Nw, p.Nkz, Nqz=p.Nqz, shift0=p.shift0)
+    win = {"dH": inp["dH"][w_lo:w_hi]}
+    for k in ("G_less", "G_gtr"):
+        win[k] = np.ascontiguousarray(inp[k][:, ew_lo:ew_hi, w_lo:w_hi])
+    for k in ("D_less", "D_gtr"):
+        win[k] = np.ascontiguousarray(inp[k][:, :, w_lo:w_hi])
+    SL, SG = oracle.sigma(wp, win, 1.0)
+    own_a = slice(i["a_lo"] - w_lo, i["a_hi"] - w_lo)
+    own_e = slice(i["e_lo"] - ew_lo, i["e_hi"] - ew_lo)
+    mask = np.zeros(ew_hi - ew_lo, dtype=bool)
+    mask[own_e] = True
+    part = {}
+    for X, (gx, gy) in enumerate((("G_less", "G_gtr"), ("G_gtr", "G_less"))):
+        w2 = dict(win)
+        w2[gy] = np.where(mask[None, :, None, None, None], win[gy], 0)   # G^Y_b(E): own energies only
+        PL, PG = oracle.pi(wp, w2, 1j)
+        part[X] = (PL, PG)[X][:, :, own_a]
+    objs = [None] * world
+    dist.all_gather_object(objs, (i["a_lo"], i["a_hi"], i["e_lo"], i["e_hi"], SL[:, own_e, own_a], SG[:, own_e, own_a],
+                                  part[0], part[1]))
+    if rank == 0:
+        result_q.put(objs)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,ga", [(4, 2), (6, 3)])
+def test_2d_grid_matches_single_process_oracle(world, ga):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gworker, args=(r, world, ga, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    objs = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=600)
+        assert pr.exitcode == 0
+    p = qtgen.problem("tiny")
+    inp = qtgen.host_inputs(p, qtgen.INTEGER)
+    SL, SG = oracle.sigma(p, inp, 1.0)
+    PL, PG = oracle.pi(p, inp, 1j)
+    cov = np.zeros((p.NE, p.Na), dtype=np.int64)
+    PLs, PGs = np.zeros_like(PL), np.zeros_like(PG)
+    for a_lo, a_hi, e_lo, e_hi, sl, sg, pl, pg in objs:
+        assert np.array_equal(sl, SL[:, e_lo:e_hi, a_lo:a_hi]) and np.array_equal(sg, SG[:, e_lo:e_hi, a_lo:a_hi])
+        PLs[:, :, a_lo:a_hi] += pl
+        PGs[:, :, a_lo:a_hi] += pg
+        cov[e_lo:e_hi, a_lo:a_hi] += 1
+    assert (cov == 1).all()
+    assert np.array_equal(PLs, PL) and np.array_equal(PGs, PG)   # integer mode: exact
+
+
+@pytest.mark.parametrize("cfg,shard,nranks,ga", [("tiny", "2d", 4, 2), ("small", "energy", 3, 0),
+                                                 ("small", "2d", 8, 2), ("small", "atom", 5, 0)])
+def test_pi_sub_slabs_tile_the_atoms(cfg, shard, nranks, ga):
+    """With a communicator, the Π outputs [pa_lo, pa_hi) of all ranks tile [0, Na) once; owned blocks tile
+    (energies x atoms) once."""
+    import paper_1912_10024_b200 as qt
+    p = qtgen.problem(cfg)
+    sh = {"atom": qt.QT_SHARD_ATOM, "energy": qt.QT_SHARD_ENERGY, "2d": qt.QT_SHARD_2D}[shard]
+    infos = [qt.shard_info(p, r, nranks, shard=sh, grid_atoms=ga) for r in range(nranks)]
+    pa = np.zeros(p.Na, dtype=np.int64)
+    blk = np.zeros((p.NE, p.Na), dtype=np.int64)
+    for i in infos:
+        pa[i["pa_lo"]:i["pa_hi"]] += 1
+        blk[i["e_lo"]:i["e_hi"], i["a_lo"]:i["a_hi"]] += 1
+        assert i["w_lo"] <= i["a_lo"] <= i["a_hi"] <= i["w_hi"] and i["ew_lo"] <= i["e_lo"] <= i["e_hi"] <= i["ew_hi"]
+    assert (pa == 1).all() and (blk == 1).all()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,shard,nranks,ga", [("cfg4", "energy", 2, 0), ("cfg4", "energy", 4, 0),
+                                                 ("cfg4", "energy", 8, 0), ("cfg4", "atom", 8, 0),
+                                                 ("cfg5", "energy", 8, 0), ("cfg5", "atom", 8, 0),
+                                                 ("cfg5", "2d", 8, 2)])
+def test_north_star_configs_fit_per_rank(cfg, shard, nranks, ga):
+    """BASELINE cfg4 (energy-sharded at 2/4/8 B200) and cfg5 (8 B200) fit in HBM: the per-rank footprint the
+    library reports (caller window tensors + outputs + plan workspace of 8 GiB, halo staging, Π partial
+    buffers, G sum planes) is <= 170 GB of the B200's 180 GB on every rank."""
+    import paper_1912_10024_b200 as qt
+    p = qtgen.problem(cfg)
+    sh = {"atom": qt.QT_SHARD_ATOM, "energy": qt.QT_SHARD_ENERGY, "2d": qt.QT_SHARD_2D}[shard]
+    worst = max(qt.shard_info(p, r, nranks, shard=sh, grid_atoms=ga, workspace_limit=8 << 30)["mem_bytes"]
+                for r in range(nranks))
+    assert worst <= 170e9, f"{cfg} {shard} x{nranks}: {worst / 1e9:.1f} GB per rank"
