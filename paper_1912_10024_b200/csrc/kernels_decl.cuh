@@ -40,6 +40,11 @@ struct SigmaArgs {
   int rows;              // Gt rows per (item, kz, E) block: 72 (items of <= 8 pairs) or 128 (FP32 mode, <= 14)
   int E0, NEo;           // energy sharding: outputs for window energies [E0, E0 + NEo) (NE = the G window)
   int gt_f32;            // Gt scratch holds float2 (FP32 mixed mode: k_sigma_tc -> FP32 sandwich)
+  // QT_FLAG_DETERMINISTIC: destination lists of the chunk — entry = {a_out, first, count, -} into det_pairs
+  // {il (chunk-relative item), t (pair in item)}, pairs in a fixed order; one CTA sums an atom's pairs
+  const int4* det_atoms;
+  const int2* det_pairs;
+  int64_t n_det;
 };
 
 struct PiWArgs {
@@ -82,6 +87,7 @@ cudaError_t launch_sigma_coef_tiled(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
+cudaError_t launch_sigma_sand_det(const SigmaArgs& a, cudaStream_t st);   // QT_FLAG_DETERMINISTIC
 // FP32 mixed-precision Σ contraction (tcgen05 kind::tf32; kernels_sigma_tc.cu). Coefficient planes
 // [item][q][4 planes][kTcRows][Kp] fp32; G planes [Nwin][Nkz][4][kTcRowsA][NEp] fp32.
 constexpr int kTcRows = 128;    // FP32-mode Σ items: <= 14 pairs (126 coefficient rows) = UMMA N

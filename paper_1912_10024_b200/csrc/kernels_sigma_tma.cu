@@ -398,6 +398,123 @@ __global__ void __launch_bounds__(kSandThreads, 512 / kSandThreads) k_sigma_sand
   }
 }
 
+// ---------------------------------------------------------------- deterministic Σ sandwich (QT_FLAG_DETERMINISTIC)
+// Destination-organized: one CTA per (destination atom with pairs in the chunk, kz) runs the sandwich of each of
+// the atom's pairs in a fixed order and adds scale·S into Σ_a with plain loads and stores (each Σ element is
+// updated by the same thread for every pair, and chunks run in a fixed order), so the neighbour sum of Eq. 3
+// has one summation order and Σ is bitwise reproducible — no floating-point atomics.
+template <int NO, class R>
+__global__ void __launch_bounds__(kSandThreads) k_sigma_sand_det(SigmaArgs A) {
+  using C2 = typename Cx<R>::T;
+  constexpr int NN = NO * NO;
+  extern __shared__ __align__(16) double2 sand_raw[];
+  C2* sm = reinterpret_cast<C2*>(sand_raw);
+  C2* Hr = sm;                  // [3][NN]  ∇_jH_{br}
+  C2* Hl = Hr + 3 * NN;         // [3][NN]  ∇_iH_{as}
+  C2* Vs = Hl + 3 * NN;         // [kSandE][3][NN]
+  const int kz = (int)(blockIdx.x % A.Nkz);
+  const int4 ent = A.det_atoms[blockIdx.x / A.Nkz];
+  constexpr int NYG = (NO + kSandY - 1) / kSandY;
+  for (int q = 0; q < ent.z; ++q) {
+    const int2 pi = A.det_pairs[ent.y + q];
+    const SigItem item = A.items[pi.x];
+    const SigPair pr = A.pairs[item.pair0 + pi.y];
+    __syncthreads();   // the previous pair's V and H are no longer read
+    for (int idx = threadIdx.x; idx < 3 * NN; idx += blockDim.x) {
+      Hr[idx] = Cx<R>::from(A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + idx]);
+      Hl[idx] = Cx<R>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + idx]);
+    }
+    const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)pi.x * A.Nkz + kz) * A.NEo * A.rows * NN;
+    for (int e0 = 0; e0 < A.NEo; e0 += kSandE) {
+      __syncthreads();
+      for (int u = threadIdx.x; u < kSandE * 3 * NO; u += blockDim.x) {   // V rows (e, i, x)
+        const int x = u % NO, r1 = u / NO, i = r1 % 3, e = r1 / 3;
+        if (e0 + e >= A.NEo) continue;
+        C2 s[NO];
+#pragma unroll
+        for (int y = 0; y < NO; ++y) s[y] = Cx<R>::zero();
+        const C2* g = gbase + ((int64_t)(e0 + e) * A.rows + pi.y * 9 + i * 3) * NN + x * NO;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          C2 gv[NO];
+#pragma unroll
+          for (int v = 0; v < NO; ++v) gv[v] = g[j * NN + v];
+          const C2* hr = Hr + j * NN;
+#pragma unroll
+          for (int v = 0; v < NO; ++v)
+#pragma unroll
+            for (int y = 0; y < NO; ++y) cfma(s[y], gv[v], hr[v * NO + y]);
+        }
+        C2* vo = Vs + (e * 3 + i) * NN + x * NO;
+#pragma unroll
+        for (int y = 0; y < NO; ++y) vo[y] = s[y];
+      }
+      __syncthreads();
+      for (int u = threadIdx.x; u < kSandE * NO * NYG; u += blockDim.x) {   // S units (e, x, y group)
+        const int yg = u % NYG, r0 = u / NYG, x = r0 % NO, e = r0 / NO;
+        if (e0 + e >= A.NEo) continue;
+        const int y0 = yg * kSandY;
+        C2 s[kSandY];
+#pragma unroll
+        for (int y = 0; y < kSandY; ++y) s[y] = Cx<R>::zero();
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const C2* hl = Hl + i * NN + x * NO;
+          const C2* v = Vs + (e * 3 + i) * NN + y0;
+#pragma unroll
+          for (int k = 0; k < NO; ++k) {
+            const C2 h = hl[k];
+#pragma unroll
+            for (int y = 0; y < kSandY; ++y)
+              if (y0 + y < NO) cfma(s[y], h, v[k * NO + y]);
+          }
+        }
+        double2* out = A.Sig + (((int64_t)kz * A.NEo + e0 + e) * A.Nout + ent.x) * NN + x * NO + y0;
+#pragma unroll
+        for (int y = 0; y < kSandY; ++y) {
+          if (y0 + y < NO) {
+            const double2 rr = cmul(A.scale, Cx<R>::wide(s[y]));
+            double2 o = out[y];
+            o.x += rr.x;
+            o.y += rr.y;
+            out[y] = o;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int NO, class R>
+static cudaError_t launch_sand_det_nr(const SigmaArgs& a, cudaStream_t st) {
+  const int smem = (2 + kSandE) * 3 * NO * NO * (int)sizeof(typename Cx<R>::T);
+  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand_det<NO, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_sigma_sand_det<NO, R><<<(unsigned)(a.n_det * a.Nkz), kSandThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+template <int NO>
+static cudaError_t launch_sand_det_no(const SigmaArgs& a, cudaStream_t st) {
+  return a.gt_f32 ? launch_sand_det_nr<NO, float>(a, st) : launch_sand_det_nr<NO, double>(a, st);
+}
+
+cudaError_t launch_sigma_sand_det(const SigmaArgs& a, cudaStream_t st) {
+  if (a.n_det * a.Nkz == 0) return cudaSuccess;
+  switch (a.Norb) {
+    case 1: return launch_sand_det_no<1>(a, st);
+    case 2: return launch_sand_det_no<2>(a, st);
+    case 3: return launch_sand_det_no<3>(a, st);
+    case 4: return launch_sand_det_no<4>(a, st);
+    case 5: return launch_sand_det_no<5>(a, st);
+    case 6: return launch_sand_det_no<6>(a, st);
+    case 7: return launch_sand_det_no<7>(a, st);
+    case 8: return launch_sand_det_no<8>(a, st);
+    case 9: return launch_sand_det_no<9>(a, st);
+    case 10: return launch_sand_det_no<10>(a, st);
+    default: return cudaErrorInvalidValue;   // Norb 11, 12 (cp.async kernel, atomics): rejected at plan time
+  }
+}
+
 // ---------------------------------------------------------------- host: tensor maps + launch
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

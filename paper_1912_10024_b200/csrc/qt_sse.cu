@@ -40,6 +40,7 @@ struct PiGroup {            // Π output group: atoms [lo, hi) of the owned slab
 
 struct SigChunk {
   int64_t i0 = 0, i1 = 0;
+  int64_t det_off = 0, det_n = 0;   // QT_FLAG_DETERMINISTIC: the chunk's destination-atom entries
   bool coef_halo = false;   // the coefficient tables read D of halo atoms
   bool g_halo = false;      // the contraction reads G entries of the halo
 };
@@ -58,6 +59,9 @@ struct Layout {
   std::vector<PiPair> pi_pairs;
   std::vector<int32_t> pi_pair_item;
   std::vector<SigChunk> sig_chunks;
+  bool det = false;
+  std::vector<int4> det_atoms;   // {a_out, first pair entry, count, 0}
+  std::vector<int2> det_pairs;   // {chunk-relative item, pair in item}
   std::vector<PiGroup> groups;
   int64_t n_interior_items = 0;
   int64_t sig_rows = kRows, ndc = 0, NNp = 0, Epad = 0, NEp = 0, Kp = 0;
@@ -245,6 +249,8 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
   L->g = geom_of(&d, nbr, d.rank, reduce);
   const Geom& g = L->g;
   if (strict && g.TE > 1 && d.Norb > 10) return QT_ERR_UNSUPPORTED;   // energy windows: TMA / tcgen05 kernels only
+  L->det = (d.flags & QT_FLAG_DETERMINISTIC) != 0;
+  if (strict && L->det && d.Norb > 10) return QT_ERR_UNSUPPORTED;     // the Norb 11-12 kernel sums with atomics
   L->reduce = reduce && g.TE > 1;
   L->Nwin = g.w_hi - g.w_lo;
   L->Nout = g.a_hi - g.a_lo;
@@ -400,6 +406,22 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
     close((int64_t)L->sig_items.size());
     L->gt_offset = (coef_max + 255) & ~size_t(255);
   }
+  if (L->det) {   // per chunk: destination atoms (ascending) and their pairs in (item, slot) order
+    for (SigChunk& c : L->sig_chunks) {
+      std::vector<std::vector<int2>> by_atom(L->Nout);
+      for (int64_t i = c.i0; i < c.i1; ++i) {
+        const SigItem& it = L->sig_items[i];
+        for (int t = 0; t < it.npair; ++t) by_atom[L->sig_pairs[it.pair0 + t].a].push_back(make_int2((int)(i - c.i0), t));
+      }
+      c.det_off = (int64_t)L->det_atoms.size();
+      for (int64_t a = 0; a < L->Nout; ++a) {
+        if (by_atom[a].empty()) continue;
+        L->det_atoms.push_back(make_int4((int)a, (int)L->det_pairs.size(), (int)by_atom[a].size(), 0));
+        L->det_pairs.insert(L->det_pairs.end(), by_atom[a].begin(), by_atom[a].end());
+      }
+      c.det_n = (int64_t)L->det_atoms.size() - c.det_off;
+    }
+  }
   if (L->reduce) {
     int64_t mx = 0;
     for (const PiGroup& G : L->groups) mx = std::max(mx, G.hi - G.lo);
@@ -485,6 +507,8 @@ struct qt_sse_plan_s {
   PiItem* d_pi_items = nullptr;
   PiPair* d_pi_pairs = nullptr;
   int32_t* d_pi_pair_item = nullptr;
+  int4* d_det_atoms = nullptr;
+  int2* d_det_pairs = nullptr;
   double2* ws = nullptr;
   double* ws_gs = nullptr;      // FP64: Re + Im planes of G^<, G^> [2][Nwin][Nkz][NEw][NN rounded up to even]
   float* ws_gtp = nullptr;      // FP32 mode: split G planes [2][Nwin][Nkz][4][128][NEp]
@@ -681,13 +705,20 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       sa.rows = (int)L.sig_rows;
       sa.gt_f32 = L.fp32 ? 1 : 0;
       sa.ntiles = 0;
+      sa.det_atoms = p->d_det_atoms ? p->d_det_atoms + ch.det_off : nullptr;
+      sa.det_pairs = p->d_det_pairs;
+      sa.n_det = ch.det_n;
       if (L.fp32) {
         QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : L.gtp_elems()), L.NEp,
                                               reinterpret_cast<const float*>(p->ws), (int)L.Kp, i1 - i0, cs));
       } else {
         QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
       }
-      QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
+      if (L.det) {
+        QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand_det(sa, cs));
+      } else {
+        QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
+      }
     }
   }
   return QT_OK;
@@ -965,6 +996,8 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->d_pi_items);
   cudaFree(p->d_pi_pairs);
   cudaFree(p->d_pi_pair_item);
+  cudaFree(p->d_det_atoms);
+  cudaFree(p->d_det_pairs);
   cudaFree(p->ws);
   cudaFree(p->ws_gs);
   cudaFree(p->ws_gtp);
@@ -1018,7 +1051,8 @@ extern "C" qt_status qt_sse_plan(const qt_sse_desc* desc, const int32_t* nbr, vo
       (s2 = upload(&p->d_sig_pairs, L.sig_pairs, cs)) != QT_OK ||
       (s2 = upload(&p->d_sig_pair_item, L.sig_pair_item, cs)) != QT_OK ||
       (s2 = upload(&p->d_pi_items, L.pi_items, cs)) != QT_OK || (s2 = upload(&p->d_pi_pairs, L.pi_pairs, cs)) != QT_OK ||
-      (s2 = upload(&p->d_pi_pair_item, L.pi_pair_item, cs)) != QT_OK)
+      (s2 = upload(&p->d_pi_pair_item, L.pi_pair_item, cs)) != QT_OK ||
+      (s2 = upload(&p->d_det_atoms, L.det_atoms, cs)) != QT_OK || (s2 = upload(&p->d_det_pairs, L.det_pairs, cs)) != QT_OK)
     return fail(s2);
   if ((!L.fp32 && cudaMalloc(&p->ws_gs, 2 * L.gs_elems() * sizeof(double)) != cudaSuccess) ||
       (L.fp32 && cudaMalloc(&p->ws_gtp, 2 * L.gtp_elems() * sizeof(float)) != cudaSuccess) ||

@@ -106,5 +106,8 @@ CONFIGS = {
     # profiling slice: cfg3's per-atom shape (Nb=34, NE=176, Nω=70, Nkz=3) on 384 atoms
     "prof":  dict(cells=(3, 4, 4), Nb=34, Norb=10, NE=176, Nw=70, Nkz=3),
     "cfg4":  dict(cells=(38, 4, 4), Nb=34, Norb=10, NE=706, Nw=70, Nkz=7),
+    # cfg4 / cfg5 per-atom shapes (longest contraction: K = Nqz·(2Nω+1)) on the 384-atom slice
+    "prof4": dict(cells=(3, 4, 4), Nb=34, Norb=10, NE=706, Nw=70, Nkz=7),
+    "prof5": dict(cells=(3, 4, 4), Nb=34, Norb=10, NE=1000, Nw=70, Nkz=5),
     "cfg5":  dict(cells=(40, 8, 4), Nb=34, Norb=10, NE=1000, Nw=70, Nkz=5),
 }

@@ -119,6 +119,31 @@ def test_fp32_small_config_sampled():
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["prof4", "prof5"])
+def test_fp32_long_contraction_sampled(cfg):
+    """cfg4 / cfg5 per-atom shapes (Nkz = 7 / 5: the longest Σ accumulation, K = Nqz·(2Nω+1) = 987 / 705 products;
+    NE = 706 / 1000): sampled Σ and Π blocks within 1e-5 of the FP64 oracle."""
+    p = qtgen.problem(cfg)
+    inp = qtgen.host_inputs(p, qtgen.RANDOM)
+    t = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
+    out = qt.run(p, t, 1j, -1j, precision=FP32, fused=True)
+    del t
+    rng = np.random.default_rng(17)
+    n = 48
+    sb = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nkz, n), rng.integers(0, p.NE, n),
+                   rng.integers(0, p.Na, n)], 1)
+    got = np.stack([(out["S_less"], out["S_gtr"])[x][k, e, a].cpu().numpy() for x, k, e, a in sb])
+    err_s = rel_fro(got, oracle.sigma_blocks(p, inp, sb, 1j), AX)
+    a_s = rng.integers(0, p.Na, n)
+    pb = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nqz, n), rng.integers(0, p.Nw, n), a_s,
+                   [1 + rng.choice(np.nonzero(p.nbr[x] >= 0)[0]) for x in a_s]], 1)
+    got_p = np.stack([(out["P_less"], out["P_gtr"])[x][q, m, a, s].cpu().numpy() for x, q, m, a, s in pb])
+    err_p = rel_fro(got_p, oracle.pi_blocks(p, inp, pb, -1j), AX)
+    print(f"{cfg} FP32 mode: max per-block rel. Frobenius error Σ {err_s:.2e}, Π {err_p:.2e}")
+    assert err_s <= TOL_FP32 and err_p <= TOL_FP32, (err_s, err_p)
+
+
+@pytest.mark.slow
 def test_fp32_cfg3_sampled():
     """The bench workload (cfg3) in FP32 mode: sampled Σ and Π blocks vs the oracle at 1e-5."""
     p = qtgen.problem("cfg3")

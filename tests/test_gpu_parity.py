@@ -127,6 +127,29 @@ def test_parity_window_sweep(Nw, NE, shift0, Nkz):
     check_full(p, inputs(p, mode=qtgen.INTEGER, seed=Nw), ss=1.0, ps=1.0, exact=True)
 
 
+@pytest.mark.parametrize("step,shift0,Nw,NE", [(2, 1, 4, 20), (3, 2, 5, 30), (2, 3, 7, 12)])
+@pytest.mark.parametrize("prec", [qt.QT_PREC_FP64, qt.QT_PREC_FP32_MIXED])
+def test_parity_shift_step(step, shift0, Nw, NE, prec):
+    """ħω_m/ΔE = shift0 + m·shift_step with shift_step > 1 (reading R6 generalized): the Σ coefficient
+    tables hold zeros between the phonon shifts and the Π correlation computes every shift column and keeps
+    the phonon ones."""
+    p = micro(Na=6, Nb=3, Norb=3, NE=NE, Nw=Nw, Nkz=3, fill=0.8, seed=step + Nw, shift0=shift0)
+    p.shift_step = step
+    tol = 1e-12 if prec == qt.QT_PREC_FP64 else 1e-5
+    inp = inputs(p, seed=31 + step)
+    g = gpu_run(p, inp, precision=prec, fused=True)
+    SL, SG = oracle.sigma(p, inp, 1j)
+    PL, PG = oracle.pi(p, inp, -1j)
+    for got, ref in ((g["S_less"], SL), (g["S_gtr"], SG), (g["P_less"], PL), (g["P_gtr"], PG)):
+        assert rel_fro(got, ref, AX) <= tol
+    inp = inputs(p, mode=qtgen.INTEGER, seed=41 + step)
+    g = gpu_run(p, inp, 1.0, 1j, precision=prec)
+    SL, SG = oracle.sigma(p, inp, 1.0)
+    PL, PG = oracle.pi(p, inp, 1j)
+    for got, ref in ((g["S_less"], SL), (g["S_gtr"], SG), (g["P_less"], PL), (g["P_gtr"], PG)):
+        assert np.array_equal(got, ref)
+
+
 def test_parity_isolated_atoms_and_many_pairs():
     """Atoms with no neighbours (Σ = 0, Π = 0) and atoms with > 8 pairs (several work items)."""
     nbr = qtgen.geometry.random_graph(14, 12, 0.9, 5)
@@ -137,6 +160,41 @@ def test_parity_isolated_atoms_and_many_pairs():
     g = check_full(p, inputs(p, seed=77))
     assert not g["S_less"][:, :, 0].any() and not g["P_gtr"][:, :, 0].any()
     assert (p.nbr >= 0).sum(1).max() > 8
+
+
+@pytest.mark.parametrize("prec", [qt.QT_PREC_FP64, qt.QT_PREC_FP32_MIXED])
+def test_deterministic_flag_bitwise_reproducible(prec):
+    """QT_FLAG_DETERMINISTIC: the Σ neighbour sum runs in one fixed order (no floating-point atomics), so two runs
+    on random inputs agree bit for bit; the result still meets the parity bar (also with many chunks)."""
+    tol = 1e-12 if prec == qt.QT_PREC_FP64 else 1e-5
+    for p, ws in ((qtgen.problem("tiny"), 0), (micro(Na=14, Nb=12, Norb=3, NE=12, Nw=3, Nkz=3, fill=0.9, seed=5), 1)):
+        inp = inputs(p, seed=61)
+        a = gpu_run(p, inp, precision=prec, flags=qt.QT_FLAG_DETERMINISTIC, workspace_limit=ws, fused=True)
+        b = gpu_run(p, inp, precision=prec, flags=qt.QT_FLAG_DETERMINISTIC, workspace_limit=ws, fused=True)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+        SL, SG = oracle.sigma(p, inp, 1j)
+        assert rel_fro(a["S_less"], SL, AX) <= tol and rel_fro(a["S_gtr"], SG, AX) <= tol
+        g = gpu_run(p, inputs(p, mode=qtgen.INTEGER, seed=62), 1.0, 1j, precision=prec,
+                    flags=qt.QT_FLAG_DETERMINISTIC)
+        SL, SG = oracle.sigma(p, inputs(p, mode=qtgen.INTEGER, seed=62), 1.0)
+        assert np.array_equal(g["S_less"], SL) and np.array_equal(g["S_gtr"], SG)
+
+
+@pytest.mark.slow
+def test_deterministic_flag_cfg3_sampled():
+    """The deterministic Σ at full cfg3 size: two runs bitwise equal on sampled blocks, and within 1e-12 of the
+    default (atomic) path."""
+    p = qtgen.problem("cfg3")
+    t = qtgen.dev_inputs(p, qtgen.RANDOM)
+    outs = [qt.run(p, t, 1j, -1j, flags=qt.QT_FLAG_DETERMINISTIC, fused=True) for _ in range(2)]
+    ref = qt.run(p, t, 1j, -1j, fused=True)
+    torch.cuda.synchronize()
+    for k in ("S_less", "S_gtr"):
+        assert torch.equal(outs[0][k], outs[1][k])
+        num = torch.linalg.matrix_norm(outs[0][k] - ref[k])
+        den = torch.linalg.matrix_norm(ref[k])
+        assert float((num[den > 0] / den[den > 0]).max()) <= TOL
 
 
 def test_outputs_overwritten_not_accumulated():

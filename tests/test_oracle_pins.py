@@ -340,3 +340,45 @@ def test_geometry_pair_counts_and_shells():
     d[:, 2] = (d[:, 2] + 6) % 12 - 6
     d2 = sorted((d * d).sum(1).tolist())
     assert d2 == [3] * 4 + [8] * 12 + [11] * 12 + [16] * 6
+
+
+# ------------------------------------------------------------------ R6 with shift_step > 1
+@pytest.mark.parametrize("step,shift0", [(2, 1), (3, 2)])
+def test_shift_step_brute_force_and_impulse(step, shift0):
+    """ħω_m/ΔE = shift0 + m·shift_step: the oracle equals the independent scalar brute force, and a single
+    G impulse at e0 with a single D frequency m0 lands exactly at e0 ± (shift0 + m0·step) (Σ) / at frequency
+    m = (e0 - e1 - shift0) / step (Π)."""
+    p = micro(Na=6, Nb=3, Norb=2, NE=16, Nw=3, Nkz=3, fill=0.9, seed=21, shift0=shift0)
+    p.shift_step = step
+    inp = inputs(p, seed=9)
+    SL, SG = oracle.sigma(p, inp, 0.37j)
+    BL, BG = oracle.brute_sigma(p, inp, 0.37j)
+    assert rel_fro(SL, BL, SIG_AX) < 1e-13 and rel_fro(SG, BG, SIG_AX) < 1e-13
+    PL, PG = oracle.pi(p, inp, 1.0)
+    QL, QG = oracle.brute_pi(p, inp, 1.0)
+    assert rel_fro(PL, QL, PI_AX) < 1e-13 and rel_fro(PG, QG, PI_AX) < 1e-13
+    # Σ impulse: absorption term only (D^> = 0), support at E = e0 + s_m0
+    k0, e0, q0, m0 = 1, 3, 0, 2
+    b0 = int(np.nonzero((p.nbr >= 0).sum(1))[0][0])
+    G = np.zeros_like(inp["G_less"])
+    G[k0, e0, b0] = inp["G_less"][k0, e0, b0]
+    D = np.zeros_like(inp["D_less"])
+    D[q0, m0] = inp["D_less"][q0, m0]
+    SL, SG = oracle.sigma(p, dict(inp, G_less=G, G_gtr=np.zeros_like(G), D_less=D, D_gtr=np.zeros_like(D)), 1.0)
+    h, sm = p.Nkz // 2, shift0 + m0 * step
+    nz = {tuple(x[:2]) for x in np.argwhere(np.abs(SL).sum(axis=(-1, -2)) > 0)}
+    assert nz == {((k0 + q0 - h) % p.Nkz, e0 + sm)}
+    # Π impulse: G^<_a at e0, G^>_b at e1 = e0 - s_m
+    a0 = b0
+    s0 = int(np.nonzero(p.nbr[a0] >= 0)[0][0])
+    b1 = int(p.nbr[a0, s0])
+    m1 = 1
+    e1 = 2
+    e0p = e1 + shift0 + m1 * step
+    GL = np.zeros_like(inp["G_less"])
+    GG = np.zeros_like(inp["G_gtr"])
+    GL[0, e0p, a0] = inp["G_less"][0, e0p, a0]
+    GG[0, e1, b1] = inp["G_gtr"][0, e1, b1]
+    PL, _ = oracle.pi(p, dict(inp, G_less=GL, G_gtr=GG), 1.0)
+    nz = {tuple(x) for x in np.argwhere(np.abs(PL).sum(axis=(-1, -2)) > 0)}
+    assert nz == {(h % p.Nkz, m1, a0, s0 + 1), (h % p.Nkz, m1, a0, 0)}
