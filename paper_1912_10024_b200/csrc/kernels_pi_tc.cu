@@ -50,9 +50,9 @@ __device__ __forceinline__ float tf32_rna_p(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-__device__ __forceinline__ void split3_p(double x, float& hi, float& lo) {
+__device__ __forceinline__ void split3_p(double x, float& hi, float& lo) {   // both terms rounded (unbiased)
   hi = tf32_rna_p((float)x);
-  lo = (float)(x - (double)hi);
+  lo = tf32_rna_p((float)(x - (double)hi));
 }
 
 // G^X (paper layout [Nkz][NE][Nwin][NN], complex128) -> Gp[a][kz][plane][Epad][NNp] fp32 split planes
@@ -184,9 +184,9 @@ __global__ void __launch_bounds__(kTWThreads, 512 / kTWThreads) k_pi_w_tc(PiWArg
       for (int x = 0; x < NO; ++x) {
         const float hr = tf32_rna_p(s[x].x), hi_ = tf32_rna_p(s[x].y);
         o[x * NO] = hr;
-        o[plane + x * NO] = s[x].x - hr;
+        o[plane + x * NO] = tf32_rna_p(s[x].x - hr);
         o[2 * plane + x * NO] = hi_;
-        o[3 * plane + x * NO] = s[x].y - hi_;
+        o[3 * plane + x * NO] = tf32_rna_p(s[x].y - hi_);
       }
     }
     if constexpr (true) {   // zero the xy padding columns of these energies

@@ -10,12 +10,16 @@
 // Precision: every operand is split x ≈ hi + lo with hi = tf32(x), lo = tf32(x − hi) ("3xTF32"), and a real
 // product is hi·hi + hi·lo + lo·hi (relative error ~2^-21); complex products use four real products
 // (Re = ArBr − AiBi via the UMMA negate-A bit, Im = ArBi + AiBr): 12 UMMAs per 8-wide k-step. FP32
-// accumulation over K = Nqz·(2Nω+1) terms in TMEM; the epilogue stores the FP32 Gt scratch and the ∇H
-// sandwich (k_sigma_sand<_, float>) runs in FP32, adding into the FP64 Σ.
+// accumulation in TMEM over SEGMENTS of kTcSegChunks K-chunks (128 shifts; the tensor core's FP32 accumulation
+// error grows with the number of additions into one accumulator: 1.3e-5 per block after K = 987 products at
+// the cfg4 shape with one accumulator per tile), the segments summed by the epilogue in FP32 registers with
+// round-to-nearest adds; the epilogue stores the FP32 Gt scratch and the ∇H sandwich (k_sigma_sand<_, float>)
+// runs in FP32, adding into the FP64 Σ.
 //
-// Warp roles (persistent CTA per SM, 192 threads): warp 0 = TMA producer, warp 1 = UMMA issuer (+ TMEM
-// allocation), warps 2..5 = epilogue (TMEM lane quarter warp%4: rc rows 32·(warp%4) ..). Two TMEM
-// accumulator buffers (Re|Im = 160 columns each) let the epilogue of tile i overlap the MMAs of tile i+1.
+// Warp roles (persistent CTA per SM, 576 threads): warp 0 = TMA producer, warp 1 = UMMA issuer (+ TMEM
+// allocation), warps 2..17 = epilogue (TMEM lane quarter warp%4: rc rows 32·(warp%4) ..; column group
+// (warp-2)/4: 32 of the 128 coefficient rows). Two TMEM accumulator buffers (Re|Im = 256 columns each)
+// alternate between segments, so the epilogue drains one segment while the MMAs fill the next.
 #include "kernels_decl.cuh"
 #include "tc05.cuh"
 #include "tma.cuh"
@@ -37,6 +41,9 @@ constexpr int kTcBPlane = kTcN * kTcKC;          // floats per B plane tile (8 K
 constexpr int kTcStage = 4 * (kTcAPlane + kTcBPlane);
 constexpr uint32_t kTcStageBytes = kTcStage * 4;
 constexpr int kTcBufCols = 256;                  // TMEM columns per accumulator buffer (Re: 0..127, Im: 128..255)
+constexpr int kTcSegChunks = 8;                  // K-chunks per TMEM accumulation segment (128 shifts)
+constexpr int kTcEpiWarps = 16;                  // epilogue warps: 4 TMEM lane quarters x 4 groups of 32 columns
+constexpr int kTcThreads = (2 + kTcEpiWarps) * 32;
 constexpr size_t kTcSmem = (size_t)kTcStages * kTcStageBytes + 1024 + 256;
 static_assert(kTcSmem <= 227 * 1024, "shared memory");
 
@@ -46,10 +53,11 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// x (FP64) -> (hi, lo): hi = tf32(x), lo = fp32(x - hi) (the tensor core reads lo's top 19 bits)
+// x (FP64) -> (hi, lo): hi = tf32(x), lo = tf32(x - hi), both rounded to nearest (a truncated lo would bias
+// every hi·lo product the same way; rounded, the split error ~2^-22 |x| is unbiased)
 __device__ __forceinline__ void split3(double x, float& hi, float& lo) {
   hi = tf32_rna((float)x);
-  lo = (float)(x - (double)hi);
+  lo = tf32_rna((float)(x - (double)hi));
 }
 
 // G (paper layout [Nkz][NE][Nwin][NN], complex128) -> Gtp[a][kz][plane][rc < kTcRowsA][NEp] fp32, planes
@@ -188,7 +196,7 @@ __device__ __forceinline__ TcTile tc_tile(const SigmaArgs& A, int64_t t) {
   return T;
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
     k_sigma_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SigmaArgs A) {
   extern __shared__ uint8_t smem_raw[];
   float* stages = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], kTcEpiWarps);
     }
     fence_barrier_init();
   }
@@ -243,26 +251,30 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- UMMA issuer (one thread)
+    // ---------------- UMMA issuer (one thread): each segment of kTcSegChunks chunks into the next buffer
     if (lane == 0) {
       const uint32_t id_pos = umma_idesc_tf32(kTcM, kTcN, false, false);
       const uint32_t id_neg = umma_idesc_tf32(kTcM, kTcN, true, false);
-      uint32_t g = 0, tc = 0;
-      for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++tc) {
+      uint32_t g = 0, sc = 0;
+      for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
         const TcTile T = tc_tile(A, t);
-        const uint32_t buf = tc & 1;
-        if (tc >= 2) mbar_wait(&tempty[buf], ((tc / 2) - 1) & 1);
-        tc_fence_after();
-        const uint32_t dre = tm + buf * kTcBufCols, dim = dre + kTcN;
-        bool acc = false;
-        for (int q = 0; q < A.Nqz; ++q) {
-          for (int c = 0; c < T.nchunk; ++c, ++g) {
+        const int nck = A.Nqz * T.nchunk;
+        const int nseg = (nck + kTcSegChunks - 1) / kTcSegChunks;
+        for (int sg = 0; sg < nseg; ++sg, ++sc) {
+          const uint32_t buf = sc & 1;
+          if (sc >= 2) mbar_wait(&tempty[buf], ((sc / 2) - 1) & 1);
+          tc_fence_after();
+          const uint32_t dre = tm + buf * kTcBufCols, dim = dre + kTcN;
+          bool acc = false;
+          const int cend = min(nck, (sg + 1) * kTcSegChunks);
+          for (int ci = sg * kTcSegChunks; ci < cend; ++ci, ++g) {
+            const int c = ci % T.nchunk;
             const uint32_t slot = g % kTcStages;
             mbar_wait(&full[slot], (g / kTcStages) & 1);
             tc_fence_after();
             const float* sa = stages + slot * kTcStage;
             const float* sb = sa + 4 * kTcAPlane;
-            // k-steps of 8 shifts j with 32(c0+c) + j in [dlo + sh, dhi + sh)
+            // k-steps of 8 shifts j with 16(c0+c) + j in [dlo + sh, dhi + sh)
             const int kc = (T.c0 + c) * kTcKC;
             const int k_lo = max(0, T.dlo + T.sh - kc) / 8, k_hi = min(kTcKC, T.dhi + T.sh - kc + 7) / 8;
             for (int kk = k_lo; kk < k_hi; ++kk) {
@@ -292,37 +304,52 @@ __global__ void __launch_bounds__(192, 1)
             }
             umma_commit(&empty[slot]);   // frees the stage when these MMAs complete
           }
+          umma_commit(&tfull[buf]);      // segment ready for the epilogue
         }
-        umma_commit(&tfull[buf]);        // accumulator buffer ready for the epilogue
       }
     }
   } else {
-    // ---------------- epilogue: TMEM (FP32) -> Gt scratch (FP64), rc = TMEM lane
+    // ---------------- epilogue: segments (FP32, TMEM) summed in registers, then the FP32 Gt scratch
     const int quarter = warp & 3;
+    const int cg = (warp - 2) >> 2;             // coefficient rows n in [cg·32, cg·32 + 32)
     const int rc = quarter * 32 + lane;
-    uint32_t tc = 0;
-    for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++tc) {
+    uint32_t sc = 0;
+    for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
       const TcTile T = tc_tile(A, t);
-      const uint32_t buf = tc & 1;
-      mbar_wait(&tfull[buf], (tc / 2) & 1);
-      tc_fence_after();
-      const uint32_t taddr = tm + ((uint32_t)(quarter * 32) << 16) + buf * kTcBufCols;
-      const int rows = 9 * T.item.npair;
-      float2* out =
-          reinterpret_cast<float2*>(A.Gt) + (((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0) * A.rows * A.NN + rc;
-      for (int n0 = 0; n0 < rows; n0 += 16) {
-        float re[16], im[16];
-        tmem_ld16(taddr + n0, re);
-        tmem_ld16(taddr + kTcN + n0, im);
-        if (rc < A.NN) {
+      const int nck = A.Nqz * T.nchunk;
+      const int nseg = (nck + kTcSegChunks - 1) / kTcSegChunks;
+      float re[32], im[32];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n0 + i < rows) out[(int64_t)(n0 + i) * A.NN] = make_float2(re[i], im[i]);
+      for (int i = 0; i < 32; ++i) re[i] = im[i] = 0.f;
+      for (int sg = 0; sg < nseg; ++sg, ++sc) {
+        const uint32_t buf = sc & 1;
+        mbar_wait(&tfull[buf], (sc / 2) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tm + ((uint32_t)(quarter * 32) << 16) + buf * kTcBufCols + cg * 32;
+        float v[16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld16(taddr + 16 * h, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) re[16 * h + i] += v[i];
+          tmem_ld16(taddr + kTcN + 16 * h, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) im[16 * h + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);   // buffer free: the registers hold this segment
+      }
+      const int rows = 9 * T.item.npair;
+      if (rc < A.NN) {
+        float2* out = reinterpret_cast<float2*>(A.Gt) +
+                      (((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0) * A.rows * A.NN + rc;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int n = cg * 32 + i;
+          if (n < rows) out[(int64_t)n * A.NN] = make_float2(re[i], im[i]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
   __syncwarp();   // reconverge the single-lane roles before the CTA barrier
@@ -384,7 +411,7 @@ cudaError_t launch_sigma_tc(const SigmaArgs& a, const float* Gtp, int64_t NEp, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(b.ntiles, nsm);
-  k_sigma_tc<<<(unsigned)grid, 192, kTcSmem, st>>>(tmA, tmB, b);
+  k_sigma_tc<<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(tmA, tmB, b);
   return cudaGetLastError();
 }
 

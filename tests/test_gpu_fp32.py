@@ -1,8 +1,8 @@
 """GPU parity of the FP32 mixed-precision mode (QT_PREC_FP32_MIXED) through the C ABI.
 
 In this mode the Σ D-contraction and the Π correlation run on the tcgen05 tensor cores (kind::tf32, every
-operand split into two tf32 terms, FP32 accumulation in TMEM, Π re-accumulated in FP64 every 4,096 products);
-the ∇H sandwiches stay FP64. Bar (north_star): within 1e-5 relative Frobenius error per block of the FP64
+operand split into two round-to-nearest tf32 terms, FP32 accumulation in TMEM over segments of 128 products:
+Σ segments summed in FP32 registers, Π segments in FP64); the ∇H sandwiches run in FP32. Bar (north_star): within 1e-5 relative Frobenius error per block of the FP64
 oracle. In integer mode every operand is exact as hi + lo and every partial sum is an integer below 2^24, so
 both outputs are bit-exact as well.
 """
@@ -81,7 +81,9 @@ def test_fp32_norb1_conditioning():
     inp = inputs(p, seed=1)
     g = _run(p, inp, 1j, -1j)
     SL, SG = oracle.sigma(p, inp, 1j)
-    assert rel_fro(g["S_less"], SL, AX) <= 1e-3 and rel_fro(g["S_gtr"], SG, AX) <= 1e-3
+    err = max(rel_fro(g["S_less"], SL, AX), rel_fro(g["S_gtr"], SG, AX))
+    print(f"Norb=1 FP32 mode: worst per-block rel. Frobenius error {err:.2e}")
+    assert err <= 1e-3
     rel_tensor = np.linalg.norm(g["S_less"] - SL) / np.linalg.norm(SL)
     assert rel_tensor <= TOL_FP32
     check(p, inputs(p, mode=qtgen.INTEGER, seed=1), ss=1.0, ps=1j, exact=True)
