@@ -30,8 +30,10 @@ struct SigmaArgs {
   const double* Gsum;    // Re + Im of G^X, atom-major [Nwin][Nkz][NE][NN rounded up to even] (k_relayout)
   const double2* coef;   // coefficient table of the current chunk: pair index p - cp0
   const double2* dH;
-  const SigItem* items;
+  const SigItem* items;  // the chunk's items (items[0] = global item item0)
   const SigPair* pairs;
+  const int32_t* pair_item;   // pair (global index) -> item (global index)
+  int64_t item0;
   double2* Sig;
   double2* Gt;           // Gt scratch of the chunk [item][kz][E][72][NN] (TMA path)
   double2 scale;
@@ -40,6 +42,7 @@ struct SigmaArgs {
   int rows;              // Gt rows per (item, kz, E) block: 72 (items of <= 8 pairs) or 128 (FP32 mode, <= 14)
   int E0, NEo;           // energy sharding: outputs for window energies [E0, E0 + NEo) (NE = the G window)
   int gt_f32;            // Gt scratch holds float2 (FP32 mixed mode: k_sigma_tc -> FP32 sandwich)
+  int gt_ld;             // Gt scratch row stride in elements: Norb² rounded up to a 16-byte multiple
   // QT_FLAG_DETERMINISTIC: destination lists of the chunk — entry = {a_out, first, count, -} into det_pairs
   // {il (chunk-relative item), t (pair in item)}, pairs in a fixed order; one CTA sums an atom's pairs
   const int4* det_atoms;

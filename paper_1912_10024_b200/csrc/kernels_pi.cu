@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   using C = PiCfg;
   using T = PiTma<NFM>;
   extern __shared__ uint8_t smem_raw[];
-  double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double2* smem = reinterpret_cast<double2*>(smem_raw + ((-smem_u32(smem_raw)) & 127u));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * T::STAGE);
   uint64_t* empty = full + C::STAGES;
 

@@ -248,7 +248,7 @@ struct PiTcArgs {
 __global__ void __launch_bounds__(kPThreads, 1)
     k_pi_contract_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, PiTcArgs A) {
   extern __shared__ uint8_t smem_raw[];
-  float* stages = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stages = reinterpret_cast<float*>(smem_raw + ((-smem_u32(smem_raw)) & 1023u));
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + kPStages * kPStage);
   uint64_t* empty = full + kPStages;
   uint64_t* tfull = empty + kPStages;

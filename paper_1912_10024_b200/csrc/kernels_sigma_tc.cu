@@ -199,7 +199,7 @@ __device__ __forceinline__ TcTile tc_tile(const SigmaArgs& A, int64_t t) {
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_sigma_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SigmaArgs A) {
   extern __shared__ uint8_t smem_raw[];
-  float* stages = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stages = reinterpret_cast<float*>(smem_raw + ((-smem_u32(smem_raw)) & 1023u));
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + kTcStages * kTcStage);
   uint64_t* empty = full + kTcStages;
   uint64_t* tfull = empty + kTcStages;
@@ -343,11 +343,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int rows = 9 * T.item.npair;
       if (rc < A.NN) {
         float2* out = reinterpret_cast<float2*>(A.Gt) +
-                      (((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0) * A.rows * A.NN + rc;
+                      (((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0) * A.rows * A.gt_ld + rc;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int n = cg * 32 + i;
-          if (n < rows) out[(int64_t)n * A.NN] = make_float2(re[i], im[i]);
+          if (n < rows) out[(int64_t)n * A.gt_ld] = make_float2(re[i], im[i]);
         }
       }
     }

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
             const __grid_constant__ CUtensorMap tmGm, const __grid_constant__ CUtensorMap tmSm, SigmaArgs A) {
   using C = SigTmaCfg<NF>;
   extern __shared__ uint8_t smem_raw[];
-  double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double2* smem = reinterpret_cast<double2*>(smem_raw + ((-smem_u32(smem_raw)) & 127u));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE);
   uint64_t* empty = full + C::STAGES;
 
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       if (++c == T.nchunk) c = 0;
     }
     if (active && row < 9 * T.item.npair) {
-      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0 + e) * A.rows + row) * A.NN;
+      double2* out = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0 + e) * A.rows + row) * A.gt_ld;
 #pragma unroll
       for (int f = 0; f < C::TMAXW; ++f) {
         if (f < nfw) {
@@ -294,105 +294,128 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 }
 
 // ---------------------------------------------------------------- Σ sandwich + neighbour sum
-// Σ_a(kz,E) += scale · Σ_i ∇_iH_{a s} (Σ_j Gt^{ij} ∇_jH_{b r}) for every pair of the chunk's items (R8).
-// One CTA per (item, kz, group of 4 of the item's pairs), looping over energy pairs. ∇H blocks stay in
-// shared memory. Compile-time Norb: a V-thread owns a row (e, t, i, x) of V^i = Σ_j Gt^{ij}∇_jH_{br}
-// (Gt row loaded into registers, ∇H broadcast from shared memory, Norb accumulators); an S-thread owns
-// a row (e, t, x) of S = Σ_i ∇_iH_{as} V^i and adds scale·S into Σ_a with RED.F64.
-#ifndef QT_SAND_P
-#define QT_SAND_P 2
+// Σ_a(kz,E) += scale · Σ_{i,j} ∇_iH_{as} Gt^{ij} ∇_jH_{br} for every pair of the chunk (Eq. 3 outer products, R8),
+// associated as S = Σ_j U^j ∇_jH_{br} with U^j = Σ_i ∇_iH_{as} Gt^{ij} (12·Norb³ complex MACs per (pair, kz, E)).
+// CTA = (pair, kz): one producer warp streams the pair's 9 Gt rows of each energy from the scratch into a ring of
+// shared-memory slots (9 bulk copies per energy, padded row stride: conflict-free broadcasts; mbarrier
+// full/empty per slot; the ring is deeper than the consumer warps, so the next energies are in flight while
+// every warp computes); each consumer warp owns whole energies: lane (j, x) = (lane / Norb, lane % Norb) forms
+// row x of U^j (Norb² · 3 MACs) and of S_j = U^j ∇_jH_{br} (Norb² MACs) in registers, the three S_j rows are
+// summed with two shuffles and the j = 0 lanes add scale·S into Σ_a with RED.F64 (other CTAs hold the atom's
+// other pairs). No block-wide barrier after the ∇H load, no intermediate in shared memory.
+#ifndef QT_SAND_W
+#define QT_SAND_W 12
 #endif
-#ifndef QT_SAND_T
-#define QT_SAND_T 128
+#ifndef QT_SAND_S
+#define QT_SAND_S 14
 #endif
-constexpr int kSandPairs = QT_SAND_P;   // pairs per CTA
-constexpr int kSandThreads = QT_SAND_T;
-constexpr int kSandE = 2;       // energies per iteration
-constexpr int kSandY = 5;       // S columns per thread
+constexpr int kSandWarps = QT_SAND_W;   // consumer warps per CTA (energies e ≡ w mod kSandWarps)
+constexpr int kSandSlots = QT_SAND_S;   // Gt ring shared by the warps: kSandSlots - kSandWarps energies prefetched
 
 template <int NO, class R>
-__global__ void __launch_bounds__(kSandThreads, 512 / kSandThreads) k_sigma_sand(SigmaArgs A) {
+struct SandCfg {
   using C2 = typename Cx<R>::T;
-  constexpr int NN = NO * NO;
-  extern __shared__ __align__(16) double2 sand_raw[];
-  C2* sand_sm = reinterpret_cast<C2*>(sand_raw);
-  C2* Hr = sand_sm;                         // [kSandPairs][3][NN]
-  C2* Hl = Hr + kSandPairs * 3 * NN;             // [kSandPairs][3][NN]
-  C2* Vs = Hl + kSandPairs * 3 * NN;             // [kSandE][kSandPairs][3][NN]
-  const int ngrp = (A.rows / 9 + kSandPairs - 1) / kSandPairs;   // pair groups per item (2 or 4)
-  const int half = blockIdx.x % ngrp;
-  const int64_t r = blockIdx.x / ngrp;
-  const int kz = (int)(r % A.Nkz);
-  const int il = (int)(r / A.Nkz);
+  static constexpr int NN = NO * NO;
+  static constexpr int NNE = (int)(((size_t)NN * sizeof(C2) + 15) / 16 * 16 / sizeof(C2));   // row, 16-byte multiple
+  static constexpr int NNP = NNE + 16 / (int)sizeof(C2);   // padded slot row: j = 0,1,2 rows on distinct banks
+  static constexpr uint32_t ROWB = (uint32_t)(NNE * sizeof(C2));   // bytes copied per row (the scratch's gt_ld)
+  static constexpr int SLOT = 9 * NNP;         // C2 per slot (rows (i,j) of one energy)
+  static constexpr int HSZ = 3 * NNP;          // C2 per ∇H triple
+  static constexpr size_t SMEM = ((size_t)kSandSlots * SLOT + 2 * HSZ) * sizeof(C2) + 2 * kSandSlots * 8;
+  static_assert(3 * NO <= 32, "lanes (j, x)");
+};
+
+template <int NO, class R>
+__global__ void __launch_bounds__((kSandWarps + 1) * 32) k_sigma_sand(SigmaArgs A) {
+  using Cf = SandCfg<NO, R>;
+  using C2 = typename Cf::C2;
+  constexpr int NN = Cf::NN, NNP = Cf::NNP;
+  extern __shared__ __align__(128) double2 sand_raw[];
+  C2* ring = reinterpret_cast<C2*>(sand_raw);   // pointer casts only: the loads stay LDS (no generic addressing)
+  C2* Hl = ring + kSandSlots * Cf::SLOT;   // [3][NNP]  ∇_iH_{as}
+  C2* Hr = Hl + Cf::HSZ;                   // [3][NNP]  ∇_jH_{br}
+  uint64_t* full = reinterpret_cast<uint64_t*>(Hr + Cf::HSZ);
+  uint64_t* empty = full + kSandSlots;
+  const int kz = (int)(blockIdx.x % A.Nkz);
+  const int64_t pg = A.cp0 + blockIdx.x / A.Nkz;   // pair (global index)
+  const int il = A.pair_item[pg] - (int)A.item0;    // chunk-relative item
   const SigItem item = A.items[il];
-  const int t0 = half * kSandPairs;
-  const int P = min(kSandPairs, item.npair - t0);
-  if (P <= 0) return;
-  for (int idx = threadIdx.x; idx < P * 3 * NN; idx += blockDim.x) {
-    const int t = idx / (3 * NN), rem = idx - t * 3 * NN;
-    const SigPair pr = A.pairs[item.pair0 + t0 + t];
-    Hr[idx] = Cx<R>::from(A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + rem]);
-    Hl[idx] = Cx<R>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + rem]);
-  }
-  const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)il * A.Nkz + kz) * A.NEo * A.rows * NN;
-  const int nv = kSandE * P * 3 * NO;   // V rows (e, t, i, x)
-  const int ns = kSandE * P * NO;       // S rows (e, t, x)
-  for (int e0 = 0; e0 < A.NEo; e0 += kSandE) {   // output energies (Gt and Σ are indexed from E0)
-    __syncthreads();
-    for (int u = threadIdx.x; u < nv; u += blockDim.x) {
-      const int x = u % NO, r1 = u / NO, i = r1 % 3, r2 = r1 / 3, t = r2 % P, e = r2 / P;
-      if (e0 + e >= A.NEo) continue;
-      C2 s[NO];
-#pragma unroll
-      for (int y = 0; y < NO; ++y) s[y] = Cx<R>::zero();
-      const C2* g = gbase + ((int64_t)(e0 + e) * A.rows + (t0 + t) * 9 + i * 3) * NN + x * NO;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        C2 gv[NO];
-#pragma unroll
-        for (int v = 0; v < NO; ++v) gv[v] = __ldg(g + j * NN + v);
-        const C2* hr = Hr + (t * 3 + j) * NN;
-#pragma unroll
-        for (int v = 0; v < NO; ++v)
-#pragma unroll
-          for (int y = 0; y < NO; ++y) cfma(s[y], gv[v], hr[v * NO + y]);
-      }
-      C2* vo = Vs + ((e * kSandPairs + t) * 3 + i) * NN + x * NO;
-#pragma unroll
-      for (int y = 0; y < NO; ++y) vo[y] = s[y];
+  const SigPair pr = A.pairs[pg];
+  const int t = (int)(pg - item.pair0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSandSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
-    __syncthreads();
-    // S-threads own (e, t, x, column group of kSandY): NYG = ceil(NO / kSandY) groups per row
-    constexpr int NYG = (NO + kSandY - 1) / kSandY;
-    for (int u = threadIdx.x; u < ns * NYG; u += blockDim.x) {
-      const int yg = u % NYG, r0 = u / NYG, x = r0 % NO, r1 = r0 / NO, t = r1 % P, e = r1 / P;
-      if (e0 + e >= A.NEo) continue;
-      const int y0 = yg * kSandY;
-      C2 s[kSandY];
-#pragma unroll
-      for (int y = 0; y < kSandY; ++y) s[y] = Cx<R>::zero();
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const C2* hl = Hl + (t * 3 + i) * NN + x * NO;
-        const C2* v = Vs + ((e * kSandPairs + t) * 3 + i) * NN + y0;
-#pragma unroll
-        for (int k = 0; k < NO; ++k) {
-          const C2 h = hl[k];
-#pragma unroll
-          for (int y = 0; y < kSandY; ++y)
-            if (y0 + y < NO) cfma(s[y], h, v[k * NO + y]);
-        }
+    fence_barrier_init();
+  }
+  for (int idx = threadIdx.x; idx < 3 * NN; idx += blockDim.x) {
+    const int i = idx / NN, rc = idx - i * NN;
+    Hl[i * NNP + rc] = Cx<R>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + idx]);
+    Hr[i * NNP + rc] = Cx<R>::from(A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + idx]);
+  }
+  __syncthreads();
+  const int ld = A.gt_ld;   // Gt row stride: 16-byte multiple (bulk copies)
+  const C2* gsrc = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)il * A.Nkz + kz) * A.NEo * A.rows * ld + t * 9 * ld;
+  if (warp == kSandWarps) {
+    // ---------------- producer: energy e -> slot e % kSandSlots
+    if (lane == 0) {
+      for (int e = 0; e < A.NEo; ++e) {
+        const int slot = e % kSandSlots;
+        if (e >= kSandSlots) mbar_wait(&empty[slot], ((e / kSandSlots) - 1) & 1);
+        mbar_arrive_expect_tx(&full[slot], 9 * Cf::ROWB);
+        const C2* src = gsrc + (int64_t)e * A.rows * ld;
+        for (int r = 0; r < 9; ++r)
+          bulk_load(ring + slot * Cf::SLOT + r * NNP, src + r * ld, Cf::ROWB, &full[slot]);
       }
-      const int a_out = A.pairs[item.pair0 + t0 + t].a;
-      double* out =
-          reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NEo + e0 + e) * A.Nout + a_out) * NN + x * NO + y0);
+    }
+    return;
+  }
+  // ---------------- consumers
+  const int j = min(lane / NO, 2), x = lane % NO;
+  const bool act = lane < 3 * NO;
+  const C2* hr = Hr + j * NNP;
+  for (int e = warp; e < A.NEo; e += kSandWarps) {
+    const int slot = e % kSandSlots;
+    mbar_wait(&full[slot], (e / kSandSlots) & 1);
+    const C2* g = ring + slot * Cf::SLOT;
+    C2 u[NO];
 #pragma unroll
-      for (int y = 0; y < kSandY; ++y) {
-        if (y0 + y < NO) {
-          const double2 rr = cmul(A.scale, Cx<R>::wide(s[y]));
-          atomicAdd(out + 2 * y, rr.x);
-          atomicAdd(out + 2 * y + 1, rr.y);
-        }
+    for (int v = 0; v < NO; ++v) u[v] = Cx<R>::zero();
+#pragma unroll 1
+    for (int i = 0; i < 3; ++i) {   // (i, k) loops rolled: keeps the kernel inside the instruction cache
+      const C2* gr = g + (i * 3 + j) * NNP;
+      const C2* hl = Hl + i * NNP + x * NO;
+#pragma unroll 2
+      for (int k = 0; k < NO; ++k) {
+        const C2 h = hl[k];
+#pragma unroll
+        for (int v = 0; v < NO; ++v) cfma(u[v], h, gr[k * NO + v]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);   // the slot's rows are in registers now
+    C2 sv[NO];
+#pragma unroll
+    for (int y = 0; y < NO; ++y) sv[y] = Cx<R>::zero();
+#pragma unroll
+    for (int v = 0; v < NO; ++v)
+#pragma unroll
+      for (int y = 0; y < NO; ++y) cfma(sv[y], u[v], hr[v * NO + y]);
+    // S = S_0 + S_1 + S_2: lanes (1, x) and (2, x) -> lane (0, x)
+#pragma unroll
+    for (int y = 0; y < NO; ++y) {
+      double2 w = Cx<R>::wide(sv[y]);
+      if (!act) w = make_double2(0.0, 0.0);
+      const double ax = __shfl_down_sync(0xffffffffu, w.x, NO), ay = __shfl_down_sync(0xffffffffu, w.y, NO);
+      const double bx = __shfl_down_sync(0xffffffffu, w.x, 2 * NO), by = __shfl_down_sync(0xffffffffu, w.y, 2 * NO);
+      if (lane < NO) {
+        const double2 tot = make_double2((w.x + ax) + bx, (w.y + ay) + by);
+        const double2 rr = cmul(A.scale, tot);
+        double* out = reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NEo + e) * A.Nout + pr.a) * NN + x * NO + y);
+        atomicAdd(out, rr.x);
+        atomicAdd(out + 1, rr.y);
       }
     }
   }
@@ -403,12 +426,16 @@ __global__ void __launch_bounds__(kSandThreads, 512 / kSandThreads) k_sigma_sand
 // the atom's pairs in a fixed order and adds scale·S into Σ_a with plain loads and stores (each Σ element is
 // updated by the same thread for every pair, and chunks run in a fixed order), so the neighbour sum of Eq. 3
 // has one summation order and Σ is bitwise reproducible — no floating-point atomics.
+constexpr int kSandThreads = 128;
+constexpr int kSandE = 2;   // energies per iteration
+constexpr int kSandY = 5;   // S columns per thread
+
 template <int NO, class R>
 __global__ void __launch_bounds__(kSandThreads) k_sigma_sand_det(SigmaArgs A) {
   using C2 = typename Cx<R>::T;
   constexpr int NN = NO * NO;
-  extern __shared__ __align__(16) double2 sand_raw[];
-  C2* sm = reinterpret_cast<C2*>(sand_raw);
+  extern __shared__ __align__(16) double2 det_raw[];
+  C2* sm = reinterpret_cast<C2*>(det_raw);
   C2* Hr = sm;                  // [3][NN]  ∇_jH_{br}
   C2* Hl = Hr + 3 * NN;         // [3][NN]  ∇_iH_{as}
   C2* Vs = Hl + 3 * NN;         // [kSandE][3][NN]
@@ -424,7 +451,7 @@ __global__ void __launch_bounds__(kSandThreads) k_sigma_sand_det(SigmaArgs A) {
       Hr[idx] = Cx<R>::from(A.dH[((int64_t)item.b_in * A.Nb + pr.r) * 3 * NN + idx]);
       Hl[idx] = Cx<R>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + idx]);
     }
-    const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)pi.x * A.Nkz + kz) * A.NEo * A.rows * NN;
+    const C2* gbase = reinterpret_cast<const C2*>(A.Gt) + ((int64_t)pi.x * A.Nkz + kz) * A.NEo * A.rows * A.gt_ld;
     for (int e0 = 0; e0 < A.NEo; e0 += kSandE) {
       __syncthreads();
       for (int u = threadIdx.x; u < kSandE * 3 * NO; u += blockDim.x) {   // V rows (e, i, x)
@@ -433,12 +460,12 @@ __global__ void __launch_bounds__(kSandThreads) k_sigma_sand_det(SigmaArgs A) {
         C2 s[NO];
 #pragma unroll
         for (int y = 0; y < NO; ++y) s[y] = Cx<R>::zero();
-        const C2* g = gbase + ((int64_t)(e0 + e) * A.rows + pi.y * 9 + i * 3) * NN + x * NO;
+        const C2* g = gbase + ((int64_t)(e0 + e) * A.rows + pi.y * 9 + i * 3) * A.gt_ld + x * NO;
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           C2 gv[NO];
 #pragma unroll
-          for (int v = 0; v < NO; ++v) gv[v] = g[j * NN + v];
+          for (int v = 0; v < NO; ++v) gv[v] = g[j * A.gt_ld + v];
           const C2* hr = Hr + j * NN;
 #pragma unroll
           for (int v = 0; v < NO; ++v)
@@ -578,12 +605,11 @@ static cudaError_t launch_sigma_tma_nf(const SigmaArgs& a, int64_t nitems, cudaS
 }
 
 template <int NO, class R>
-static cudaError_t launch_sand_nr(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
-  const int smem = (2 + kSandE) * kSandPairs * 3 * NO * NO * (int)sizeof(typename Cx<R>::T);
-  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+static cudaError_t launch_sand_nr(const SigmaArgs& a, int64_t /*nitems*/, cudaStream_t st) {
+  using Cf = SandCfg<NO, R>;
+  cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
   if (e != cudaSuccess) return e;
-  const int ngrp = (a.rows / 9 + kSandPairs - 1) / kSandPairs;
-  k_sigma_sand<NO, R><<<(unsigned)(nitems * a.Nkz * ngrp), kSandThreads, smem, st>>>(a);
+  k_sigma_sand<NO, R><<<(unsigned)(a.npairs_chunk * a.Nkz), (kSandWarps + 1) * 32, Cf::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 // FP64 Gt scratch (72-row items) or, in the FP32 mixed mode (128-row items), FP32 Gt and an FP32 sandwich

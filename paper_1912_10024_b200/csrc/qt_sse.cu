@@ -685,6 +685,8 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       sa.dH = (const double2*)dH;
       sa.items = p->d_sig_items + i0;
       sa.pairs = p->d_sig_pairs;
+      sa.pair_item = p->d_sig_pair_item;
+      sa.item0 = i0;
       sa.Sig = (double2*)S;
       sa.scale = make_double2(sre, sim);
       sa.Nwin = L.Nwin;
@@ -704,6 +706,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       sa.Dwin = (int)L.Dwin;
       sa.rows = (int)L.sig_rows;
       sa.gt_f32 = L.fp32 ? 1 : 0;
+      sa.gt_ld = L.fp32 ? (int)((L.NN + 1) & ~int64_t(1)) : (int)L.NN;
       sa.ntiles = 0;
       sa.det_atoms = p->d_det_atoms ? p->d_det_atoms + ch.det_off : nullptr;
       sa.det_pairs = p->d_det_pairs;
