@@ -19,10 +19,11 @@ QT_OK, QT_ERR_INVALID_ARG, QT_ERR_UNSUPPORTED, QT_ERR_OUT_OF_MEMORY, QT_ERR_CUDA
 QT_SHARD_NONE, QT_SHARD_ENERGY, QT_SHARD_ATOM, QT_SHARD_2D = range(4)
 QT_FLAG_DETERMINISTIC = 1
 QT_PREC_FP64, QT_PREC_FP32_MIXED = 0, 1
-EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_sigma_pi", "qt_sse_execute_host", "qt_sse_query",
+EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "qt_sse_query",
             "qt_sse_halo_exchange", "qt_sse_destroy", "qt_sse_status_string", "qt_sse_count_flops",
             "qt_sse_launch_count", "qt_sse_timing_enable", "qt_sse_timing_read", "qt_sse_nccl_unique_id",
-            "qt_sse_shard_info"]
+            "qt_sse_shard_info", "qt_sse_sigma_pi"]
+EXPORTED_RGF = ["qt_rgf_plan", "qt_rgf_solve", "qt_rgf_check_info", "qt_rgf_count_flops", "qt_rgf_destroy"]
 KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout", "k_halo_pack",
                 "k_sigma_sand"]
 
@@ -44,6 +45,10 @@ class Info(ctypes.Structure):
                 ("pa_lo", ctypes.c_int64), ("pa_hi", ctypes.c_int64), ("Ta", ctypes.c_int32), ("TE", ctypes.c_int32),
                 ("ta", ctypes.c_int32), ("te", ctypes.c_int32), ("reduce_bytes", ctypes.c_double),
                 ("mem_bytes", ctypes.c_double)]
+
+
+class RgfDesc(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_int64), ("bnum", ctypes.c_int64), ("bs", ctypes.c_int64)]
 
 
 class QTError(RuntimeError):
@@ -74,6 +79,14 @@ def _load():
     lib.qt_sse_shard_info.argtypes = [ctypes.POINTER(Desc), P, ctypes.POINTER(Info)]
     lib.qt_sse_timing_enable.argtypes = [P, I]
     lib.qt_sse_timing_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    lib.qt_rgf_plan.argtypes = [ctypes.POINTER(RgfDesc), P, ctypes.POINTER(P)]
+    lib.qt_rgf_solve.argtypes = [P, P, P, P, P, P, P, P, P, P]
+    lib.qt_rgf_check_info.argtypes = [P, P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.qt_rgf_count_flops.argtypes = [ctypes.POINTER(RgfDesc), ctypes.POINTER(ctypes.c_double)]
+    lib.qt_rgf_destroy.argtypes = [P]
+    lib.qt_rgf_destroy.restype = None
+    for f in ("qt_rgf_plan", "qt_rgf_solve", "qt_rgf_check_info", "qt_rgf_count_flops"):
+        getattr(lib, f).restype = I
     for f in ("qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_sigma_pi", "qt_sse_execute_host", "qt_sse_query",
               "qt_sse_halo_exchange", "qt_sse_count_flops", "qt_sse_timing_enable", "qt_sse_timing_read",
               "qt_sse_nccl_unique_id", "qt_sse_shard_info"):
@@ -248,4 +261,65 @@ def run(p, t: dict, sig_scale=1j, pi_scale=-1j, plan: Plan | None = None, precis
     if own:
         torch.cuda.synchronize()
         plan.close()
+    return out
+
+
+# ---------------------------------------------------------------- RGF (include/qt_rgf.h)
+def rgf_count_flops(P: int, bnum: int, bs: int) -> dict:
+    """Flops of one RGF solve: the executed dense count and the paper's model 8·(26·bnum − 25)·bs³ per point."""
+    d = RgfDesc(P, bnum, bs)
+    out = (ctypes.c_double * 2)()
+    _check(_get_lib().qt_rgf_count_flops(ctypes.byref(d), out), "qt_rgf_count_flops")
+    return dict(executed=out[0], paper_model=out[1])
+
+
+class Rgf:
+    """Owns a qt_rgf_plan_t: diagonal blocks of G^R, G^<, G^> of a batch of block-tridiagonal systems (Eq. 1)."""
+
+    def __init__(self, P: int, bnum: int, bs: int, stream=None):
+        self.desc = RgfDesc(P, bnum, bs)
+        h = ctypes.c_void_p()
+        _check(_get_lib().qt_rgf_plan(ctypes.byref(self.desc), _stream(stream), ctypes.byref(h)), "qt_rgf_plan")
+        self.h = h
+
+    def solve(self, Ad, Au, Al, Sl, Sg, GR, GL, GG, stream=None):
+        _check(_get_lib().qt_rgf_solve(self.h, _ptr(Ad), _ptr(Au) if Au.numel() else None,
+                                       _ptr(Al) if Al.numel() else None, _ptr(Sl), _ptr(Sg), _ptr(GR), _ptr(GL),
+                                       _ptr(GG), _stream(stream)), "qt_rgf_solve")
+
+    def check(self, stream=None):
+        """(point, block) of the first singular pivot block of the last solve, or None."""
+        p, b = ctypes.c_int64(-1), ctypes.c_int64(-1)
+        rc = _get_lib().qt_rgf_check_info(self.h, _stream(stream), ctypes.byref(p), ctypes.byref(b))
+        if rc == QT_OK:
+            return None
+        if rc == QT_ERR_INVALID_ARG:
+            return int(p.value), int(b.value)
+        _check(rc, "qt_rgf_check_info")
+
+    def close(self):
+        if self.h:
+            _get_lib().qt_rgf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def rgf_run(t: dict, plan: Rgf | None = None):
+    """G^R, G^<, G^> diagonal blocks for device inputs t (dict of complex128 CUDA tensors, qtgen.rgf layout)."""
+    import torch
+    P, nb, bs = t["Ad"].shape[0], t["Ad"].shape[1], t["Ad"].shape[2]
+    own = plan is None
+    plan = Rgf(P, nb, bs) if own else plan
+    out = {k: torch.empty_like(t["Ad"]) for k in ("GR", "GL", "GG")}
+    plan.solve(t["Ad"], t["Au"], t["Al"], t["Sl"], t["Sg"], out["GR"], out["GL"], out["GG"])
+    bad = plan.check()
+    if own:
+        plan.close()
+    if bad is not None:
+        raise QTError(f"qt_rgf_solve: singular pivot block {bad[1]} at point {bad[0]}")
     return out

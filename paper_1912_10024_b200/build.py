@@ -1,6 +1,6 @@
 """Build every native artefact in-tree (no JIT cache; the .so files travel to the GPU box).
 
-  paper_1912_10024_b200/libqtsse.so   product: C-ABI + sm_100a kernels (nvcc)
+  paper_1912_10024_b200/libqtsse.so   product: C-ABI (qt_sse.h, qt_rgf.h) + sm_100a kernels (nvcc)
   qtgen/libqtgen_host.so              input generator, host side (gcc, OpenMP)
   qtgen/libqtgen_dev.so               input generator, device side (nvcc, sm_100a)
   oracle/liboracle.so                 CPU oracle + brute force (gcc; test infrastructure)
@@ -31,15 +31,28 @@ def _nccl_dir() -> Path:
 
 NCCL_DIR = _nccl_dir()
 
+
+def _cublas_dir() -> Path:
+    """cuBLAS of the torch wheel (nvidia-cublas), so one libcublas.so.12 lives in the process with torch's."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.cublas")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.cublas (torch's cuBLAS wheel) not found")
+    return Path(list(spec.submodule_search_locations)[0])
+
+
+CUBLAS_DIR = _cublas_dir()
+
 TARGETS = {
     "libqtsse": dict(
         out=PKG / "libqtsse.so",
         srcs=sorted((PKG / "csrc").glob("*.cu")),
-        deps=sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "qt_sse.h"],
+        deps=sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "qt_sse.h", ROOT / "include" / "qt_rgf.h"],
         cmd=lambda srcs, out: [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
                                "-Xcompiler", "-fPIC,-O2", "-shared", f"-I{ROOT / 'include'}",
                                f"-I{NCCL_DIR / 'include'}", *map(str, srcs), "-o", str(out), "-lcudart",
-                               f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{NCCL_DIR / 'lib'}"],
+                               f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{NCCL_DIR / 'lib'}",
+                               f"-L{CUBLAS_DIR / 'lib'}", "-l:libcublas.so.12", f"-Xlinker=-rpath,{CUBLAS_DIR / 'lib'}"],
     ),
     "qtgen_dev": dict(
         out=ROOT / "qtgen" / "libqtgen_dev.so",

@@ -24,6 +24,15 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(qt.lib, name), name
 
 
+def test_library_exports_every_rgf_symbol():
+    import paper_1912_10024_b200 as qt
+    header = (ROOT / "include" / "qt_rgf.h").read_text()
+    declared = set(re.findall(r"^(?:qt_status|void)\s+(qt_rgf_\w+)\s*\(", header, re.M))
+    assert declared == set(qt.EXPORTED_RGF)
+    for name in declared:
+        assert hasattr(qt.lib, name), name
+
+
 def test_generator_libraries_export_declared_symbols():
     header = (ROOT / "include" / "qt_gen.h").read_text()
     declared = set(re.findall(r"^(?:void|int)\s+(qtgen_\w+)\s*\(", header, re.M))
