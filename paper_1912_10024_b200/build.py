@@ -43,6 +43,17 @@ def _cublas_dir() -> Path:
 
 CUBLAS_DIR = _cublas_dir()
 
+
+def _wheel_dir(mod: str) -> Path:
+    import importlib.util
+    spec = importlib.util.find_spec(mod)
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError(f"{mod} (torch's CUDA library wheel) not found")
+    return Path(list(spec.submodule_search_locations)[0])
+
+
+CUSOLVER_DIR = _wheel_dir("nvidia.cusolver")
+
 TARGETS = {
     "libqtsse": dict(
         out=PKG / "libqtsse.so",
@@ -52,7 +63,9 @@ TARGETS = {
                                "-Xcompiler", "-fPIC,-O2", "-shared", f"-I{ROOT / 'include'}",
                                f"-I{NCCL_DIR / 'include'}", *map(str, srcs), "-o", str(out), "-lcudart",
                                f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{NCCL_DIR / 'lib'}",
-                               f"-L{CUBLAS_DIR / 'lib'}", "-l:libcublas.so.12", f"-Xlinker=-rpath,{CUBLAS_DIR / 'lib'}"],
+                               f"-L{CUBLAS_DIR / 'lib'}", "-l:libcublas.so.12", f"-Xlinker=-rpath,{CUBLAS_DIR / 'lib'}",
+                               f"-L{CUSOLVER_DIR / 'lib'}", "-l:libcusolver.so.11",
+                               f"-Xlinker=-rpath,{CUSOLVER_DIR / 'lib'}"],
     ),
     "qtgen_dev": dict(
         out=ROOT / "qtgen" / "libqtgen_dev.so",

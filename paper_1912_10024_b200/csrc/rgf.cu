@@ -3,14 +3,18 @@
 // (E, kz) points ("operating on all atoms for a specific energy-momentum pair").
 //
 // B200 mapping: every block step is a handful of dense bs x bs complex products, identical for all P points, so
-// each is ONE strided-batched ZGEMM over the points (cuBLAS: a plain library GEMM on the FP64 tensor pipe), the
-// block inversions are batched LU + inverse (cublasZgetrfBatched / getriBatched), and the only hand-written
-// kernel is the anti-Hermitian update G^≷ += Y − Y† of the backward pass (tiled transpose in shared memory).
+// each is ONE strided-batched ZGEMM over the points (cuBLAS: a plain library GEMM on the FP64 tensor pipe, 34 TF
+// measured at bs = 640); the block inversions are blocked LU + triangular solves against the identity
+// (cuSOLVER getrf + getrs, whose trailing updates are GEMMs), one per point, fanned out over kRgfLanes streams so
+// the points' factorizations run concurrently (cuBLAS' batched getrf/getri is built for small matrices: 9 of 10 s
+// at bs = 640); the only hand-written kernels are the anti-Hermitian update G^≷ += Y − Y† of the backward pass
+// (tiled transpose in shared memory), the identity fill and a batched add.
 // The left-connected g^R, g^<, g^> live in the OUTPUT tensors (the backward pass overwrites block n after its
 // last read), so the plan's scratch is seven bs x bs temporaries per point. Row-major blocks are handed to the
 // column-major cuBLAS as their transposes: row-major C = op(A)·op(B) is column-major C^T = op(B)^T·op(A)^T,
 // with op = N for X and op = C (conjugate transpose) for X†.
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -65,6 +69,17 @@ __global__ void k_add(double2* __restrict__ out, int64_t out_stride, const doubl
   }
 }
 
+// out[p] = I (P blocks of bs x bs at stride `stride`)
+__global__ void k_set_identity(double2* __restrict__ out, int64_t stride, int bs, int64_t P) {
+  const int64_t n = (int64_t)bs * bs, total = n * P;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx / n, e = idx - p * n;
+    out[p * stride + e] = make_double2((e / bs) == (e % bs) ? 1.0 : 0.0, 0.0);
+  }
+}
+
+constexpr int kRgfLanes = 16;   // concurrent per-point factorizations
+
 }  // namespace
 
 struct qt_rgf_plan_s {
@@ -72,11 +87,18 @@ struct qt_rgf_plan_s {
   cublasHandle_t h = nullptr;
   double2* tmp = nullptr;          // 7 temporaries [7][P][bs][bs]
   int* piv = nullptr;              // [P][bs]
-  int* info = nullptr;             // [bnum][P] getrf info, [P] getri info
+  int* info = nullptr;             // [bnum][P] getrf info, [P] getrs info
   double2** ptrM = nullptr;        // [P] -> temporary M
   double2** ptrG = nullptr;        // [bnum][P] -> block n of the G^R output (set per solve)
   std::vector<double2*> hptrG;
   const void* last_GR = nullptr;
+  // per-point factorizations (cuSOLVER), fanned out over lanes
+  int lanes = 0;
+  cudaStream_t ls[kRgfLanes] = {};
+  cusolverDnHandle_t sh[kRgfLanes] = {};
+  double2* lwork = nullptr;        // [lanes][lwork_elems]
+  int lwork_elems = 0;
+  cudaEvent_t ev_fork = nullptr, ev_join[kRgfLanes] = {};
 };
 
 namespace {
@@ -116,10 +138,11 @@ qt_status copy(qt_rgf_plan_s* q, double2* dst, int64_t sd, const double2* src, i
 extern "C" qt_status qt_rgf_count_flops(const qt_rgf_desc* d, double out[2]) {
   if (!d || !out || d->P <= 0 || d->bnum <= 0 || d->bs <= 0) return QT_ERR_INVALID_ARG;
   const double n3 = (double)d->bs * d->bs * d->bs, nb = (double)d->bnum;
-  // forward: block 0: 4 GEMMs + 1 inversion; blocks 1..: 10 GEMMs + 1 inversion; backward: 10 GEMMs + 1 add-GEMM
-  // per block 0..bnum-2 (Z = XT·g^R_n included); an LU (≈ n³/3 complex MACs... counted as getrf 1/3 + getri 2/3 = n³)
+  // forward: block 0: 4 GEMMs + 1 inversion; blocks 1..: 10 GEMMs + 1 inversion; backward: 11 GEMMs per block
+  // 0..bnum-2 (Z = XT·g^R_n included); an inversion = LU (n³/3 complex MACs) + two triangular solves with n
+  // right-hand sides (n³)
   const double gemms = 4.0 + 10.0 * (nb - 1.0) + 11.0 * (nb - 1.0);
-  const double inv = nb * 1.0;
+  const double inv = nb * (4.0 / 3.0);
   out[0] = d->P * (gemms + inv) * n3 * 8.0;
   out[1] = d->P * 8.0 * (26.0 * nb - 25.0) * n3;
   return QT_OK;
@@ -127,6 +150,14 @@ extern "C" qt_status qt_rgf_count_flops(const qt_rgf_desc* d, double out[2]) {
 
 extern "C" void qt_rgf_destroy(qt_rgf_plan_t q) {
   if (!q) return;
+  for (int l = 0; l < q->lanes; ++l) {
+    if (q->ls[l]) cudaStreamSynchronize(q->ls[l]);
+    if (q->sh[l]) cusolverDnDestroy(q->sh[l]);
+    if (q->ls[l]) cudaStreamDestroy(q->ls[l]);
+    if (q->ev_join[l]) cudaEventDestroy(q->ev_join[l]);
+  }
+  if (q->ev_fork) cudaEventDestroy(q->ev_fork);
+  cudaFree(q->lwork);
   if (q->h) cublasDestroy(q->h);
   cudaFree(q->tmp);
   cudaFree(q->piv);
@@ -157,6 +188,19 @@ extern "C" qt_status qt_rgf_plan(const qt_rgf_desc* d, void* stream, qt_rgf_plan
   if ((s = cu(cudaMemsetAsync(q->info, 0, (d->bnum + 1) * d->P * sizeof(int), (cudaStream_t)stream))) != QT_OK) return fail(s);
   if ((s = cu(cudaMalloc(&q->ptrM, d->P * sizeof(double2*)))) != QT_OK) return fail(s);
   if ((s = cu(cudaMalloc(&q->ptrG, d->bnum * d->P * sizeof(double2*)))) != QT_OK) return fail(s);
+  q->lanes = (int)std::min<int64_t>(d->P, kRgfLanes);
+  if ((s = cu(cudaEventCreateWithFlags(&q->ev_fork, cudaEventDisableTiming))) != QT_OK) return fail(s);
+  for (int l = 0; l < q->lanes; ++l) {
+    if ((s = cu(cudaStreamCreateWithFlags(&q->ls[l], cudaStreamNonBlocking))) != QT_OK) return fail(s);
+    if ((s = cu(cudaEventCreateWithFlags(&q->ev_join[l], cudaEventDisableTiming))) != QT_OK) return fail(s);
+    if (cusolverDnCreate(&q->sh[l]) != CUSOLVER_STATUS_SUCCESS) return fail(QT_ERR_CUDA);
+    if (cusolverDnSetStream(q->sh[l], q->ls[l]) != CUSOLVER_STATUS_SUCCESS) return fail(QT_ERR_CUDA);
+  }
+  if (cusolverDnZgetrf_bufferSize(q->sh[0], (int)d->bs, (int)d->bs, reinterpret_cast<cuDoubleComplex*>(q->tmp),
+                                  (int)d->bs, &q->lwork_elems) != CUSOLVER_STATUS_SUCCESS)
+    return fail(QT_ERR_CUDA);
+  if ((s = cu(cudaMalloc(&q->lwork, (size_t)q->lanes * std::max(q->lwork_elems, 1) * sizeof(double2)))) != QT_OK)
+    return fail(s);
   std::vector<double2*> pm(d->P);
   for (int64_t p = 0; p < d->P; ++p) pm[p] = q->tmp + p * blk;   // temporary 0 = M
   if ((s = cu(cudaMemcpyAsync(q->ptrM, pm.data(), d->P * sizeof(double2*), cudaMemcpyHostToDevice, (cudaStream_t)stream))) != QT_OK)
@@ -206,11 +250,30 @@ extern "C" qt_status qt_rgf_solve(qt_rgf_plan_t q, const void* Ad_, const void* 
       RG_TRY(gemm(q, Al + (n - 1) * blk, sO, false, GR + (n - 1) * blk, sD, false, T[1], blk, 1.0, 0.0));
       RG_TRY(gemm(q, T[1], blk, false, Au + (n - 1) * blk, sO, false, M, blk, -1.0, 1.0));
     }
-    // g^R_n = M^{-1}: batched LU in place, inverse into block n of GR
-    RG_TRY(cb(cublasZgetrfBatched(q->h, n_i, reinterpret_cast<cuDoubleComplex**>(q->ptrM), n_i, q->piv, q->info + n * P,
-                                  (int)P)));
-    RG_TRY(cb(cublasZgetriBatched(q->h, n_i, reinterpret_cast<const cuDoubleComplex* const*>(q->ptrM), n_i, q->piv,
-                                  reinterpret_cast<cuDoubleComplex**>(q->ptrG + n * P), n_i, q->info + nb * P, (int)P)));
+    // g^R_n = M^{-1}: per point, LU of M_p (in place) and a solve against the identity written into block n of GR
+    {
+      const int64_t tot = P * blk;
+      k_set_identity<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(GR + n * blk, sD, n_i, P);
+      RG_TRY(cu(cudaGetLastError()));
+      RG_TRY(cu(cudaEventRecord(q->ev_fork, st)));
+      for (int l = 0; l < q->lanes; ++l) RG_TRY(cu(cudaStreamWaitEvent(q->ls[l], q->ev_fork, 0)));
+      for (int64_t p = 0; p < P; ++p) {
+        const int l = (int)(p % q->lanes);
+        cuDoubleComplex* Mp = reinterpret_cast<cuDoubleComplex*>(M + p * blk);
+        int* piv = q->piv + p * bs;
+        if (cusolverDnZgetrf(q->sh[l], n_i, n_i, Mp, n_i, reinterpret_cast<cuDoubleComplex*>(q->lwork) + (size_t)l * q->lwork_elems,
+                             piv, q->info + n * P + p) != CUSOLVER_STATUS_SUCCESS)
+          return QT_ERR_CUDA;
+        if (cusolverDnZgetrs(q->sh[l], CUBLAS_OP_N, n_i, n_i, Mp, n_i, piv,
+                             reinterpret_cast<cuDoubleComplex*>(GR + p * sD + n * blk), n_i,
+                             q->info + nb * P + p) != CUSOLVER_STATUS_SUCCESS)
+          return QT_ERR_CUDA;
+      }
+      for (int l = 0; l < q->lanes; ++l) {
+        RG_TRY(cu(cudaEventRecord(q->ev_join[l], q->ls[l])));
+        RG_TRY(cu(cudaStreamWaitEvent(st, q->ev_join[l], 0)));
+      }
+    }
     const double2* S[2] = {Sl, Sg};
     double2* G[2] = {GL, GG};
     for (int x = 0; x < 2; ++x) {
