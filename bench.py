@@ -281,7 +281,11 @@ def main():
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 = QT_PREC_FP32_MIXED (reported separately: contractions on tcgen05 tf32x3)")
     ap.add_argument("--separate", action="store_true", help="qt_sse_sigma + qt_sse_pi instead of the fused call")
+    ap.add_argument("--workload", default="sse", choices=["sse", "rgf"],
+                    help="rgf = the GF-phase RGF solver (SURVEY §8(f) NEXT(4)); reported separately, 1 GPU")
     args = ap.parse_args()
+    if args.workload == "rgf":
+        return run_rgf(args)
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
         sys.exit(_relaunch(args))
@@ -532,6 +536,65 @@ def main():
     plan.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_rgf(args):
+    """RGF line (NEXT(4)): diagonal blocks of G^R, G^<, G^> for a batch of block-tridiagonal systems (Eq. 1) on
+    one GPU. Metric: executed Tflop/s of the dense work (complex GEMMs + inversions, 8 flops per complex MAC),
+    with the paper's RGF model flops beside it; roofline against the sustained FP64 peak."""
+    out_stream = _claim_stdout()
+    import torch
+    import paper_1912_10024_b200 as qt
+    from qtgen import rgf as grgf
+    name = args.config if args.config.startswith("rgf") else "rgf_finfet"
+    p = grgf.problem(name)
+    torch.cuda.set_device(0)
+    t = grgf.dev_inputs(p)
+    out = {k: torch.empty_like(t["Ad"]) for k in ("GR", "GL", "GG")}
+    plan = qt.Rgf(p.P, p.bnum, p.bs)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.solve(t["Ad"], t["Au"], t["Al"], t["Sl"], t["Sg"], out["GR"], out["GL"], out["GG"], stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert plan.check() is None, "singular pivot block"
+    clocks = Clocks(0)
+    clocks.start()
+    n0 = qt.launch_count()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for k in range(args.steps):
+        step()
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    ms = evs[0].elapsed_time(evs[-1]) / args.steps
+    f = qt.rgf_count_flops(p.P, p.bnum, p.bs)
+    med, ci = median_ci(per)
+    peak, peak_src, _ = fp64_peak()
+    value = f["executed"] / (ms * 1e-3) / 1e12
+    in_bytes = sum(v.numel() * 16 for v in t.values())
+    line = {"metric": "RGF (GF phase, NEXT(4)) FP64 Tflop/s of the dense block work", "impl": "ours",
+            "value": round(value, 3), "unit": "Tflop/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "none", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded block-tridiagonal A = E - H - Σ^R, anti-Hermitian Σ^≷)",
+            "config": {"workload": f"{name}: {p.P} points x {p.bnum} blocks of {p.bs} (N = {p.N})",
+                       "flops_per_step": f["executed"], "paper_model_flops_per_step": f["paper_model"],
+                       "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (in_bytes / 1e9)},
+            "step_ms": {"median": round(med, 3), "ci95": [round(ci[0], 3), round(ci[1], 3)], "n": args.steps},
+            "paper_model_tflops": round(f["paper_model"] / (ms * 1e-3) / 1e12, 3),
+            "roofline": {"bound": "tensor", "kernel": "the whole solve (cuBLAS ZGEMM on DMMA + cuSOLVER getrf/getrs)",
+                         "achieved": round(value, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+                         "frac": round(value / peak, 4), "traffic": None, "peak_source": peak_src},
+            "gpu_launches": int(qt.launch_count() - n0), "clocks": clk,
+            "note": "library GEMMs / factorizations (cuBLAS ZGEMM, cuSOLVER getrf + getrs) plus the repo's own "
+                    "kernels (identity fill, anti-Hermitian update, add); gpu_launches counts the repo's own"}
+    print(json.dumps(line), file=out_stream, flush=True)
+    plan.close()
 
 
 def oracle_paper_flops(p):

@@ -152,25 +152,30 @@ struct PiTma {
 // result is Re = T1 - T2, Im = T3 - T1 - T2 (formed once, in the epilogue). The B-side Re+Im (one per
 // fragment) comes precomputed from shared memory; the A-side one (one per k-step, shared by all the
 // warp's fragments) is one DADD per 3·N DMMAs, cheaper than storing and streaming a W sum plane.
+// Fragment f of the warp is column fragment f0 + f·stride: `fs` = stride·8·XC elements between them.
 template <int N>
-__device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const double2* gb, const double* sb) {
+__device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const double2* gb, const double* sb, int fs) {
 #pragma unroll
   for (int f = 0; f < N; ++f) {
-    const double2 b = gb[f * 16 * PiCfg::XC];
-    cmma3s(acc[f], a.x, a.y, as, b.x, b.y, sb[f * 16 * PiCfg::XC]);
+    const double2 b = gb[f * fs];
+    cmma3s(acc[f], a.x, a.y, as, b.x, b.y, sb[f * fs]);
   }
 }
 
-// DMMA work of one stage (EC energies) for one warp. rem = NE - E0 - shift0: energy E0+el has
-// in-window columns m < rem - el; column fragments without any are skipped.
-template <int NFW>
+// DMMA work of one stage (EC energies) for one warp owning nfa column fragments f0, f0 + stride, ..
+// (nfa <= NFW). rem = NE - E0 - shift0: energy E0+el has in-window columns m < rem - el; column fragments
+// without any are skipped.
+template <int NFW, int STRIDE = 0>   // STRIDE > 0: compile-time fragment stride (immediate smem offsets)
 __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double2* gs,
-                                         const double* gss, int rem, int f0) {
+                                         const double* gss, int rem, int f0, int stride_rt, int nfa) {
   static_assert(NFW > 0, "empty fragment range");
   using C = PiCfg;
+  const int stride = STRIDE > 0 ? STRIDE : stride_rt;
+  const int fs = stride * 8 * C::XC;
 #pragma unroll
   for (int el = 0; el < C::EC; ++el) {
-    const int nfe = min(NFW, (((rem - el + 7) >> 3) - f0 + 1) >> 1);   // fragments f0 + 2f with columns < rem
+    const int ncol = (rem - el + 7) >> 3;                        // column fragments with columns < rem - el
+    const int nfe = min(nfa, max(0, (ncol - f0 + stride - 1) / stride));
     const double2* w = ws + el * kRows * C::XC;
     const double2* g = gs + el * C::XC;
     const double* gsm = gss + el * C::XC;
@@ -178,7 +183,7 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
 #pragma unroll
       for (int k4 = 0; k4 < C::XC; k4 += 4) {
         const double2 a = w[k4];
-        pi_kstep<NFW>(acc, a, a.x + a.y, g + k4, gsm + k4);
+        pi_kstep<NFW>(acc, a, a.x + a.y, g + k4, gsm + k4, fs);
       }
     } else if (nfe > 0) {
 #pragma unroll
@@ -188,8 +193,8 @@ __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const do
 #pragma unroll
         for (int f = 0; f < NFW; ++f) {
           if (f < nfe) {
-            const double2 b = g[k4 + f * 16 * C::XC];
-            cmma3s(acc[f], a.x, a.y, as, b.x, b.y, gsm[k4 + f * 16 * C::XC]);
+            const double2 b = g[k4 + f * fs];
+            cmma3s(acc[f], a.x, a.y, as, b.x, b.y, gsm[k4 + f * fs]);
           }
         }
       }
@@ -228,16 +233,29 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   }
   __syncthreads();
 
-  // Warp w issues on sub-partition w % 4 (0, 1: five consumer warps; 2, 3: four). Roles (m-fragment mi,
-  // lower/upper column fragments) are placed so the 5-fragment (lower) warps fill sub-partitions 2, 3 and
-  // the 4-fragment ones 0, 1: DMMA work per sub-partition 21/20/20/20 for NFM = 9 (was 23/22/18/18).
+  // Roles: warp -> (row fragment mi of the item's F = ceil(9P/8) active ones, column fragments f0, f0 + Wp,
+  // ..). Full items (F = 9): Wp = 2 warps per row fragment, placed by a role table so the 5-fragment (lower)
+  // warps fill sub-partitions 2, 3 and the 4-fragment ones 0, 1 (warp w issues on sub-partition w % 4):
+  // DMMA work per sub-partition 21/20/20/20 for NFM = 9. Small items (the remainder of an atom's pairs,
+  // e.g. 2 of 34: F = 3) spread the column fragments over Wp = 18 / F warps per row fragment instead of
+  // leaving 18 - 2F warps idle: the tile takes ceil(NFM/Wp) fragment-times instead of ceil(NFM/2).
+  // Column fragments are interleaved (stride Wp), so the out-of-window cut at large E (R7) removes work
+  // from every warp alike.
   constexpr int kPiRole[18] = {8, 10, 0, 1, 9, 12, 2, 3, 11, 14, 4, 5, 13, 16, 6, 7, 15, 17};
-  const int role = warp < C::NCONS ? kPiRole[warp] : 0;
-  const int mi = role % 9;
-  const bool upper = role >= 9;
-  // column fragments are interleaved: lower warps own 0, 2, 4, .., upper warps 1, 3, 5, .. (so the
-  // out-of-window cut at large E (R7) removes work from both halves alike)
-  const int f0 = upper ? 1 : 0;
+  const int Fr = (9 * P + 7) / 8;
+  const int Wp = Fr >= 9 ? 2 : C::NCONS / Fr;
+  int mi = 0, f0 = 0;
+  if (warp < C::NCONS) {
+    if (Fr >= 9) {
+      const int role = kPiRole[warp];
+      mi = role % 9;
+      f0 = role >= 9 ? 1 : 0;
+    } else {
+      mi = warp / Wp;
+      f0 = warp - mi * Wp;
+    }
+  }
+  const int nfa = f0 < NFM ? (NFM - f0 + Wp - 1) / Wp : 0;   // column fragments of this warp (<= NF0)
   C3Acc acc[T::NF0];
 #pragma unroll
   for (int f = 0; f < T::NF0; ++f) acc[f] = C3Acc{};
@@ -268,7 +286,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
       }
     }
   } else {
-    const bool active = mi * 8 < 9 * P;
+    const bool active = warp < C::NCONS && mi < Fr && nfa > 0;
     int ec = 0;
     for (int st = 0; st < nst; ++st) {
       const int slot = st % C::STAGES;
@@ -281,10 +299,19 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const double2* gs = st0 + C::W_STAGE + boff;
         const double* gss = reinterpret_cast<const double*>(st0 + C::W_STAGE + T::G_STAGE) + boff;
         const int rem = A.NE - A.E0 - ec * C::EC - A.shift0;
-        if (upper) {
-          if constexpr (T::NF1 > 0) pi_stage<T::NF1>(acc, ws, gs, gss, rem, f0);
+        // compile-time fragment counts for the common cases (full-speed unrolled path), guarded otherwise
+        if (Wp == 2 && nfa == T::NF0) {
+          pi_stage<T::NF0, 2>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+        } else if (Wp == 2 && nfa == T::NF0 - 1) {
+          if constexpr (T::NF0 > 1) pi_stage<(T::NF0 > 1 ? T::NF0 - 1 : 1), 2>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+        } else if (nfa == 1) {
+          pi_stage<1>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+        } else if (nfa == 2) {
+          if constexpr (T::NF0 >= 2) pi_stage<2>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+        } else if (nfa == 3) {
+          if constexpr (T::NF0 >= 3) pi_stage<3>(acc, ws, gs, gss, rem, f0, Wp, nfa);
         } else {
-          pi_stage<T::NF0>(acc, ws, gs, gss, rem, f0);
+          pi_stage<T::NF0>(acc, ws, gs, gss, rem, f0, Wp, nfa);
         }
       }
       __syncwarp();
@@ -294,14 +321,13 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
     if (active) {
       const int row = mi * 8 + (lane >> 2);
       const int t = row / 9, ij = row - 9 * t;
-      const int nfw = upper ? T::NF1 : T::NF0;
       if (t < P) {
         const int slot = A.pairs[item.pair0 + t].s + 1;
         const int64_t base = (int64_t)item.a_out * (A.Nb + 1) * 9 + slot * 9 + ij;
 #pragma unroll
         for (int f = 0; f < T::NF0; ++f) {
-          if (f < nfw) {
-            const int c0 = (f0 + 2 * f) * 8 + 2 * (lane & 3);   // shift columns c0, c0 + 1 (shift0 + c)
+          if (f < nfa) {
+            const int c0 = (f0 + Wp * f) * 8 + 2 * (lane & 3);   // shift columns c0, c0 + 1 (shift0 + c)
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int c = c0 + k, m = c / A.step;

@@ -18,6 +18,9 @@
 using namespace qt;
 
 static std::atomic<uint64_t> g_launches{0};
+namespace qt {
+void count_launches(uint64_t n) { g_launches.fetch_add(n); }   // the RGF solver's own kernels (rgf.cu)
+}
 
 namespace {
 

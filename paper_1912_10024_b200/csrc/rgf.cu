@@ -23,6 +23,10 @@
 
 #include "qt_rgf.h"
 
+namespace qt {
+void count_launches(uint64_t n);   // qt_sse_launch_count accounting (qt_sse.cu)
+}
+
 namespace {
 
 struct Z {
@@ -255,6 +259,7 @@ extern "C" qt_status qt_rgf_solve(qt_rgf_plan_t q, const void* Ad_, const void* 
       const int64_t tot = P * blk;
       k_set_identity<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(GR + n * blk, sD, n_i, P);
       RG_TRY(cu(cudaGetLastError()));
+      qt::count_launches(1);
       RG_TRY(cu(cudaEventRecord(q->ev_fork, st)));
       for (int l = 0; l < q->lanes; ++l) RG_TRY(cu(cudaStreamWaitEvent(q->ls[l], q->ev_fork, 0)));
       for (int64_t p = 0; p < P; ++p) {
@@ -304,12 +309,14 @@ extern "C" qt_status qt_rgf_solve(qt_rgf_plan_t q, const void* Ad_, const void* 
       RG_TRY(gemm(q, W, blk, false, X, blk, true, G + n * blk, sD, 1.0, 1.0));                  // g^x_n += W X†
       k_add_antiherm<<<tg, tb, 0, st>>>(G + n * blk, sD, Y, (int)bs);                            // += Y − Y†
       RG_TRY(cu(cudaGetLastError()));
+      qt::count_launches(1);
     }
     RG_TRY(gemm(q, XT, blk, false, GR + n * blk, sD, false, Zt, blk, 1.0, 0.0));                // Z = XT g^R_n
     const int64_t tot = P * blk;
     const int grid = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
     k_add<<<grid, 256, 0, st>>>(GR + n * blk, sD, Zt, blk, P);                                   // G^R_n = g^R_n + Z
     RG_TRY(cu(cudaGetLastError()));
+    qt::count_launches(1);
   }
   return QT_OK;
 }
