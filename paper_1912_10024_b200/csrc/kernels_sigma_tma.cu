@@ -118,11 +118,12 @@ struct SigTmaCfg {
 // One stage of DMMA work for a consumer warp with NFW n-fragments (Gauss 3M complex product: three
 // real DMMAs per complex 8x8x4 step, see C3Acc).
 template <int NFW, int NPS, int KC>
-__device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const double* ss, const double2* cs, int kc) {
+__device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const double* ss, const double2* cs, int klo,
+                                            int khi) {
   static_assert(NFW > 0, "empty fragment range");
 #pragma unroll
   for (int k4 = 0; k4 < KC; k4 += 4) {
-    if (k4 < kc) {
+    if (k4 >= klo && k4 < khi) {   // k-steps whose 4 shifts all lie outside the tile's energy window are skipped
       const double2 a = cs[k4];
 #if QT_SIG_CSUM
       const double as = reinterpret_cast<const double*>(cs - (threadIdx.x & 3))[32 + k4 + (threadIdx.x & 3)];
@@ -140,6 +141,7 @@ __device__ __forceinline__ void sigma_stage(C3Acc* acc, const double2* gs, const
 struct SigTile {
   SigItem item;
   int E, kz, ch, il, dc_lo, nchunk, nst, F, ept;
+  int lo, hi;   // shifts d (window index) with E + e + d - Dmax in [0, NE) for some energy e < ept of the tile
   bool skip;
 };
 
@@ -161,8 +163,10 @@ __device__ __forceinline__ SigTile sig_tile(const SigmaArgs& A, int64_t t) {
   T.skip = ((T.E - A.E0) % T.ept) != 0;
   // K range: shifts d = 16*dc + k - Dmax with E+e+d in [0,NE) for some e < ept (R7), in whole 16-shift
   // chunks (rows outside the window are zero-filled by TMA; shifts beyond the table are zero coefficients).
-  T.dc_lo = max(0, A.Dmax - (T.E + T.ept - 1)) / KC;
-  const int dc_hi = (min(A.Dwin, A.Dmax - T.E + A.NE) + KC - 1) / KC;
+  T.lo = max(0, A.Dmax - (T.E + T.ept - 1));
+  T.hi = min(A.Dwin, A.Dmax - T.E + A.NE);
+  T.dc_lo = T.lo / KC;
+  const int dc_hi = (T.hi + KC - 1) / KC;
   T.nchunk = dc_hi - T.dc_lo;
   T.nst = T.skip ? 0 : A.Nqz * T.nchunk;
   return T;
@@ -262,17 +266,19 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
       const uint32_t slot = g % C::STAGES;
       mbar_wait(&full[slot], (g / C::STAGES) & 1);
       if (active) {
-        const int kc = C::KC;
+        // k-step range of this chunk: shifts 16·dc + k in [lo, hi), in whole DMMA k-steps of 4
+        const int d0 = (T.dc_lo + c) * C::KC;
+        const int klo = max(0, T.lo - d0) & ~3, khi = min(C::KC, T.hi - d0);
         const int boff = ((lane & 3) + e) * C::NPS + (lane >> 2) + f0 * 8;
         const double2* gs = smem + slot * C::STAGE + boff;
         const double* ss = reinterpret_cast<const double*>(smem + slot * C::STAGE + soff) + boff;
         const double2* cs = smem + slot * C::STAGE + coff + row * C::KCP + (lane & 3);
         if (nfw == C::TMAXW) {
-          sigma_stage<C::TMAXW, C::NPS, C::KC>(acc, gs, ss, cs, kc);
+          sigma_stage<C::TMAXW, C::NPS, C::KC>(acc, gs, ss, cs, klo, khi);
         } else if (nfw == C::TMAXW - 1) {
-          if constexpr (C::TMAXW > 1) sigma_stage<C::TMAXW - 1, C::NPS, C::KC>(acc, gs, ss, cs, kc);
+          if constexpr (C::TMAXW > 1) sigma_stage<C::TMAXW - 1, C::NPS, C::KC>(acc, gs, ss, cs, klo, khi);
         } else {
-          if constexpr (C::TMAXW > 2) sigma_stage<C::TMAXW - 2, C::NPS, C::KC>(acc, gs, ss, cs, kc);
+          if constexpr (C::TMAXW > 2) sigma_stage<C::TMAXW - 2, C::NPS, C::KC>(acc, gs, ss, cs, klo, khi);
         }
       }
       __syncwarp();
