@@ -58,6 +58,7 @@ struct PiWArgs {
   const int32_t* pair_item;   // pair -> item
   double2* W;                 // [item - i0][Nkz][xy chunk][NE][72 rows (t,ij)][20]
   int64_t p0, i0, Nwin, Nb;
+  int64_t npairs;             // pairs of the chunk [p0, p0 + npairs) (k_pi_w2: one CTA per (pair, kz))
   int NE, Nkz, Norb, NN, nEB;
   int E0, NEo;                // energies of this rank's Π sum: window energies [E0, E0 + NEo)
 };

@@ -122,6 +122,85 @@ __global__ void __launch_bounds__(kWThreads, 512 / kWThreads) k_pi_w(PiWArgs A) 
   }
 }
 
+// W sandwich, warp-per-energy form (Norb <= 10): CTA = (pair, kz), warp w owns energies e ≡ w (mod kW2Warps).
+// Phase 1, lane (i, q): row q of T_i = G^Y_b(E) ∇_iH_{br} (G_b row from global;
+// ∇_iH_{br} broadcast from shared memory) into the warp's T buffer. Phase 2, lane (j, y): row y of
+// ∇_jH_{as} held in registers, W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x] for i, x (T broadcast), stored
+// straight to the W scratch. Only __syncwarp between the phases; 12·Norb³ complex MACs per (pair, kz, E).
+constexpr int kW2Warps = 4;
+
+template <int NO>
+__global__ void __launch_bounds__(kW2Warps * 32) k_pi_w2(PiWArgs A) {
+  constexpr int NN = NO * NO, NNP = NN + 2;
+  constexpr int XC = 20, NXC = (NN + XC - 1) / XC;
+  static_assert(3 * NO <= 32, "lanes (i, q) / (j, y)");
+  extern __shared__ __align__(16) double2 w2_sm[];
+  double2* Hr = w2_sm;                          // [3][NNP]  ∇_iH_{br}
+  double2* Tw = Hr + 3 * NNP;                   // [kW2Warps][3][NNP]
+  const int kz = (int)(blockIdx.x % A.Nkz);
+  const int64_t pg = A.p0 + blockIdx.x / A.Nkz;                 // pair (global index)
+  const int64_t item = A.pair_item[pg];
+  const PiItem it = A.items[item];
+  const PiPair pr = A.pairs[pg];
+  const int t = (int)(pg - it.pair0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int idx = threadIdx.x; idx < 3 * NN; idx += blockDim.x) {
+    const int i = idx / NN, rc = idx - i * NN;
+    Hr[i * NNP + rc] = A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + idx];
+  }
+  const bool act = lane < 3 * NO;
+  const int hi = min(lane / NO, 2), lo = lane % NO;   // phase 1: (i, q); phase 2: (j, y)
+  double2 hl[NO];                                      // row y of ∇_jH_{as}
+#pragma unroll
+  for (int k = 0; k < NO; ++k) hl[k] = A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + hi * NN + lo * NO + k];
+  __syncthreads();
+  double2* T = Tw + warp * 3 * NNP;
+  const double2* hr = Hr + hi * NNP;
+  double2* Wb = A.W + ((item - A.i0) * A.Nkz + kz) * (int64_t)NXC * A.NEo * kRows * XC;
+  // row q = lo of G^Y_b(kz, E0 + e) (latency covered by the other warps: up to 8 CTAs of 4 warps per SM)
+  const double2* gsrc = A.GY + (((int64_t)kz * A.NE + A.E0) * A.Nwin + pr.b_in) * NN + lo * NO;
+  const int64_t gstep = (int64_t)A.Nwin * NN;   // one energy
+  for (int e = warp; e < A.NEo; e += kW2Warps) {
+    double2 g[NO];
+#pragma unroll
+    for (int p = 0; p < NO; ++p) g[p] = __ldg(gsrc + e * gstep + p);
+    // phase 1: T_i[q][x] = Σ_p G_b[q][p] ∇_iH_{br}[p][x]
+    double2 tr[NO];
+#pragma unroll
+    for (int x = 0; x < NO; ++x) tr[x] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int p = 0; p < NO; ++p)
+#pragma unroll
+      for (int x = 0; x < NO; ++x) cfma(tr[x], g[p], hr[p * NO + x]);
+    if (act) {
+#pragma unroll
+      for (int x = 0; x < NO; ++x) T[hi * NNP + lo * NO + x] = tr[x];
+    }
+    __syncwarp();
+    // phase 2: W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x]; row (t, i, j), column xy = x·Norb + y
+#pragma unroll 1
+    for (int i = 0; i < 3; ++i) {
+      double2 w[NO];
+#pragma unroll
+      for (int x = 0; x < NO; ++x) w[x] = make_double2(0.0, 0.0);
+      const double2* ti = T + i * NNP;
+#pragma unroll
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int x = 0; x < NO; ++x) cfma(w[x], hl[q], ti[q * NO + x]);
+      if (act) {
+        const int row = t * 9 + i * 3 + hi;
+#pragma unroll
+        for (int x = 0; x < NO; ++x) {
+          const int xy = x * NO + lo, xc = xy / XC, c = xy - xc * XC;
+          Wb[(((int64_t)xc * A.NEo + e) * kRows + row) * XC + c] = w[x];
+        }
+      }
+    }
+    __syncwarp();   // T is rewritten by the next energy
+  }
+}
+
 // ---------------------------------------------------------------- Π correlation: TMA / mbarrier pipeline
 // Stage = (kz, E0..E0+EC-1, xy0..xy0+XC-1): the W tile [EC][72][XC] (one contiguous 1-D bulk copy) and the G_a window
 // rows E0+s_0 .. E0+EC-1+s_{NWP-1} (4-D TMA box; rows >= NE zero-filled: reading R7). Warp 18 produces;
@@ -428,8 +507,32 @@ static cudaError_t launch_pi_w_no(const PiWArgs& a, int64_t nitems, cudaStream_t
   return cudaGetLastError();
 }
 
+template <int NO>
+static cudaError_t launch_pi_w2_no(const PiWArgs& a, cudaStream_t st) {
+  const int smem = (1 + kW2Warps) * 3 * (NO * NO + 2) * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_pi_w2<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_pi_w2<NO><<<(unsigned)(a.npairs * a.Nkz), kW2Warps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pi_w(const PiWArgs& a, int64_t nitems_chunk, cudaStream_t st) {
   if (nitems_chunk * a.Nkz == 0) return cudaSuccess;
+#ifndef QT_PIW_OLD
+  switch (a.Norb) {   // warp-per-energy form
+    case 1: return launch_pi_w2_no<1>(a, st);
+    case 2: return launch_pi_w2_no<2>(a, st);
+    case 3: return launch_pi_w2_no<3>(a, st);
+    case 4: return launch_pi_w2_no<4>(a, st);
+    case 5: return launch_pi_w2_no<5>(a, st);
+    case 6: return launch_pi_w2_no<6>(a, st);
+    case 7: return launch_pi_w2_no<7>(a, st);
+    case 8: return launch_pi_w2_no<8>(a, st);
+    case 9: return launch_pi_w2_no<9>(a, st);
+    case 10: return launch_pi_w2_no<10>(a, st);
+    default: break;
+  }
+#endif
   switch (a.Norb) {
     case 1: return launch_pi_w_no<1>(a, nitems_chunk, st);
     case 2: return launch_pi_w_no<2>(a, nitems_chunk, st);

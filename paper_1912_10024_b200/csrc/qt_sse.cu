@@ -770,6 +770,7 @@ qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* G
         wa.W = p->ws;
         wa.p0 = pp0;
         wa.i0 = i0;
+        wa.npairs = L.pi_items[i1 - 1].pair0 + L.pi_items[i1 - 1].npair - pp0;
         wa.Nwin = L.Nwin;
         wa.Nb = d.Nb;
         wa.NE = (int)L.NEw;
