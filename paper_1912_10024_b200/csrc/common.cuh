@@ -96,7 +96,7 @@ __host__ __device__ inline int64_t imod(int64_t x, int64_t n) {
 }
 
 // ---- work lists (built on the host in qt_sse_plan) ----
-// Σ is source-organized: one item = a source atom b and up to 8 of the pairs (a,s) with nbr[a][s] == b.
+// Σ is source-organized: one item = a source atom b and up to 8 (FP32 mode: 14) of the pairs (a,s) with nbr[a][s] == b.
 struct SigPair {
   int32_t a;      // destination atom (local output index space: a - a_lo)
   int32_t s;      // slot of b in nbr[a]
@@ -105,11 +105,11 @@ struct SigPair {
 };
 struct SigItem {
   int32_t b_in;   // source atom in the input window
-  int32_t npair;  // 1..8
+  int32_t npair;  // 1..8 (FP32 mode: 1..14)
   int32_t pair0;  // index into the SigPair list
   int32_t b;      // source atom (global)
 };
-// Π is destination-organized: one item = a destination atom a and up to 8 of its valid slots.
+// Π is destination-organized: one item = a destination atom a and up to 8 (FP32 mode: 14) of its valid slots.
 struct PiPair {
   int32_t s, b_in, r, a_in;
 };

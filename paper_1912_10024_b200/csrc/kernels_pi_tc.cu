@@ -5,7 +5,7 @@
 // W_t^{ij}(kz,E)[xy] · G_a(kz+qz−h, E+s_m)[xy], as the UMMA
 //   D[row][m] = Σ_k A[row][k] · B[m][k],  row = (t, ij) of ≤ 14 pairs of destination atom a (M = 128 TMEM
 //   lanes), m = frequency (N = 80), k = (kz, E, xy) flattened with the xy row padded to NNp = 4⌈Norb²/4⌉.
-// A = the split planes of W (written K-major by k_pi_w_tc from the FP64 sandwich). B = G_a: row m starts
+// A = the split planes of W (written K-major by k_pi_w_tc, an FP32 sandwich on FP32-rounded inputs). B = G_a: row m starts
 // s_m energies later in the same flattened (E, xy) sequence, i.e. B is a TMA view with row stride NNp over a
 // copy of G_a padded with zero energies past NE (R7), so every K-chunk of 32 is one box per plane.
 // Precision: the tensor core's FP32 accumulation loses ~1 ulp per addition (its error grows linearly with the
@@ -27,7 +27,7 @@ namespace qt {
 
 #define UMMA_DESC(p) (kPKC == 16 ? umma_desc_k64(p) : umma_desc_k128(p))
 constexpr int kPM = 128;                 // UMMA M: rows (t, ij), 9·14 = 126 used
-constexpr int kPN = 80;                  // UMMA N: frequencies m (Nω <= 80 in this mode)
+constexpr int kPN = 80;                  // UMMA N: shift columns ((Nω−1)·shift_step + 1 <= 80 in this mode)
 #ifndef QT_PI_KC
 #define QT_PI_KC 32
 #endif

@@ -92,10 +92,12 @@ struct qt_rgf_plan_s {
   double2* tmp = nullptr;          // 7 temporaries [7][P][bs][bs]
   int* piv = nullptr;              // [P][bs]
   int* info = nullptr;             // [bnum][P] getrf info, [P] getrs info
-  double2** ptrM = nullptr;        // [P] -> temporary M
-  double2** ptrG = nullptr;        // [bnum][P] -> block n of the G^R output (set per solve)
-  std::vector<double2*> hptrG;
-  const void* last_GR = nullptr;
+  // point groups: independent halves of the batch, each on its own stream + cuBLAS handle, so one group's
+  // GEMMs overlap the other group's factorizations
+  int ngroups = 1;
+  cudaStream_t gs[2] = {};
+  cublasHandle_t gh[2] = {};
+  cudaEvent_t ev_start = nullptr, ev_gdone[2] = {};
   // per-point factorizations (cuSOLVER), fanned out over lanes
   int lanes = 0;
   cudaStream_t ls[kRgfLanes] = {};
@@ -119,22 +121,29 @@ qt_status cb(cublasStatus_t s) {
     if (s_ != QT_OK) return s_;   \
   } while (0)
 
-// row-major C[p] = alpha·opA(A[p])·opB(B[p]) + beta·C[p] for p < P; conjA / conjB select X† (conjugate transpose)
-qt_status gemm(qt_rgf_plan_s* q, const double2* A, int64_t sA, bool cA, const double2* B, int64_t sB, bool cB, double2* C,
-               int64_t sC, double ar, double br) {
+struct Grp {   // a contiguous range of points [p0, p0 + np) solved on its own stream
+  int64_t p0, np;
+  cublasHandle_t h;
+  cudaStream_t s;
+  int l0, nl;   // its factorization lanes
+};
+
+// row-major C[p] = alpha·opA(A[p])·opB(B[p]) + beta·C[p] for the group's points; cA / cB select X† (conjugate transpose)
+qt_status gemm(qt_rgf_plan_s* q, const Grp& g, const double2* A, int64_t sA, bool cA, const double2* B, int64_t sB, bool cB,
+               double2* C, int64_t sC, double ar, double br) {
   const int n = (int)q->d.bs;
   const cuDoubleComplex al = make_cuDoubleComplex(ar, 0.0), be = make_cuDoubleComplex(br, 0.0);
-  return cb(cublasZgemmStridedBatched(q->h, cB ? CUBLAS_OP_C : CUBLAS_OP_N, cA ? CUBLAS_OP_C : CUBLAS_OP_N, n, n, n, &al,
+  return cb(cublasZgemmStridedBatched(g.h, cB ? CUBLAS_OP_C : CUBLAS_OP_N, cA ? CUBLAS_OP_C : CUBLAS_OP_N, n, n, n, &al,
                                       reinterpret_cast<const cuDoubleComplex*>(B), n, sB,
                                       reinterpret_cast<const cuDoubleComplex*>(A), n, sA, &be,
-                                      reinterpret_cast<cuDoubleComplex*>(C), n, sC, (int)q->d.P));
+                                      reinterpret_cast<cuDoubleComplex*>(C), n, sC, (int)g.np));
 }
 
-// dst[p] = src[p] for p < P (strided blocks of bs² complex)
-qt_status copy(qt_rgf_plan_s* q, double2* dst, int64_t sd, const double2* src, int64_t ss, cudaStream_t st) {
+// dst[p] = src[p] for the group's points (strided blocks of bs² complex)
+qt_status copy(qt_rgf_plan_s* q, const Grp& g, double2* dst, int64_t sd, const double2* src, int64_t ss) {
   const size_t w = (size_t)q->d.bs * q->d.bs * sizeof(double2);
-  return cu(cudaMemcpy2DAsync(dst, sd * sizeof(double2), src, ss * sizeof(double2), w, (size_t)q->d.P,
-                              cudaMemcpyDeviceToDevice, st));
+  return cu(cudaMemcpy2DAsync(dst, sd * sizeof(double2), src, ss * sizeof(double2), w, (size_t)g.np,
+                              cudaMemcpyDeviceToDevice, g.s));
 }
 
 }  // namespace
@@ -161,13 +170,18 @@ extern "C" void qt_rgf_destroy(qt_rgf_plan_t q) {
     if (q->ev_join[l]) cudaEventDestroy(q->ev_join[l]);
   }
   if (q->ev_fork) cudaEventDestroy(q->ev_fork);
+  for (int g = 0; g < 2; ++g) {
+    if (q->gs[g]) cudaStreamSynchronize(q->gs[g]);
+    if (q->gh[g]) cublasDestroy(q->gh[g]);
+    if (q->gs[g]) cudaStreamDestroy(q->gs[g]);
+    if (q->ev_gdone[g]) cudaEventDestroy(q->ev_gdone[g]);
+  }
+  if (q->ev_start) cudaEventDestroy(q->ev_start);
   cudaFree(q->lwork);
   if (q->h) cublasDestroy(q->h);
   cudaFree(q->tmp);
   cudaFree(q->piv);
   cudaFree(q->info);
-  cudaFree(q->ptrM);
-  cudaFree(q->ptrG);
   delete q;
 }
 
@@ -190,8 +204,14 @@ extern "C" qt_status qt_rgf_plan(const qt_rgf_desc* d, void* stream, qt_rgf_plan
   if ((s = cu(cudaMalloc(&q->piv, d->P * d->bs * sizeof(int)))) != QT_OK) return fail(s);
   if ((s = cu(cudaMalloc(&q->info, (d->bnum + 1) * d->P * sizeof(int)))) != QT_OK) return fail(s);
   if ((s = cu(cudaMemsetAsync(q->info, 0, (d->bnum + 1) * d->P * sizeof(int), (cudaStream_t)stream))) != QT_OK) return fail(s);
-  if ((s = cu(cudaMalloc(&q->ptrM, d->P * sizeof(double2*)))) != QT_OK) return fail(s);
-  if ((s = cu(cudaMalloc(&q->ptrG, d->bnum * d->P * sizeof(double2*)))) != QT_OK) return fail(s);
+  q->ngroups = d->P >= 2 ? 2 : 1;
+  if ((s = cu(cudaEventCreateWithFlags(&q->ev_start, cudaEventDisableTiming))) != QT_OK) return fail(s);
+  for (int g = 0; g < q->ngroups; ++g) {
+    if ((s = cu(cudaStreamCreateWithFlags(&q->gs[g], cudaStreamNonBlocking))) != QT_OK) return fail(s);
+    if ((s = cu(cudaEventCreateWithFlags(&q->ev_gdone[g], cudaEventDisableTiming))) != QT_OK) return fail(s);
+    if ((s = cb(cublasCreate(&q->gh[g]))) != QT_OK) return fail(s);
+    if ((s = cb(cublasSetStream(q->gh[g], q->gs[g]))) != QT_OK) return fail(s);
+  }
   q->lanes = (int)std::min<int64_t>(d->P, kRgfLanes);
   if ((s = cu(cudaEventCreateWithFlags(&q->ev_fork, cudaEventDisableTiming))) != QT_OK) return fail(s);
   for (int l = 0; l < q->lanes; ++l) {
@@ -205,14 +225,101 @@ extern "C" qt_status qt_rgf_plan(const qt_rgf_desc* d, void* stream, qt_rgf_plan
     return fail(QT_ERR_CUDA);
   if ((s = cu(cudaMalloc(&q->lwork, (size_t)q->lanes * std::max(q->lwork_elems, 1) * sizeof(double2)))) != QT_OK)
     return fail(s);
-  std::vector<double2*> pm(d->P);
-  for (int64_t p = 0; p < d->P; ++p) pm[p] = q->tmp + p * blk;   // temporary 0 = M
-  if ((s = cu(cudaMemcpyAsync(q->ptrM, pm.data(), d->P * sizeof(double2*), cudaMemcpyHostToDevice, (cudaStream_t)stream))) != QT_OK)
-    return fail(s);
   if ((s = cu(cudaStreamSynchronize((cudaStream_t)stream))) != QT_OK) return fail(s);
   *out = q;
   return QT_OK;
 }
+
+namespace {
+
+// The whole RGF pass for the points of one group, stream-ordered on g.s. Pointers are the group's first point.
+qt_status solve_group(qt_rgf_plan_s* q, const Grp& g, const double2* Ad, const double2* Au, const double2* Al,
+                      const double2* Sl, const double2* Sg, double2* GR, double2* GL, double2* GG) {
+  const int64_t P = q->d.P, nb = q->d.bnum, bs = q->d.bs, blk = bs * bs, np = g.np;
+  const int64_t sD = nb * blk, sO = (nb - 1) * blk;   // point strides of [P][bnum] and [P][bnum-1] tensors
+  const cudaStream_t st = g.s;
+  double2* T[7];
+  for (int k = 0; k < 7; ++k) T[k] = q->tmp + (k * P + g.p0) * blk;   // the group's slice of each temporary
+  const int n_i = (int)bs;
+  // ---------------- forward pass: left-connected g^R_n (into GR), g^<_n (GL), g^>_n (GG)
+  for (int64_t n = 0; n < nb; ++n) {
+    double2* M = T[0];
+    RG_TRY(copy(q, g, M, blk, Ad + n * blk, sD));
+    if (n > 0) {
+      // T1 = A_{n,n-1} g^R_{n-1};  M = A_nn − T1 A_{n-1,n}
+      RG_TRY(gemm(q, g, Al + (n - 1) * blk, sO, false, GR + (n - 1) * blk, sD, false, T[1], blk, 1.0, 0.0));
+      RG_TRY(gemm(q, g, T[1], blk, false, Au + (n - 1) * blk, sO, false, M, blk, -1.0, 1.0));
+    }
+    // g^R_n = M^{-1}: per point, LU of M_p (in place) and a solve against the identity written into block n of GR,
+    // fanned out over the group's lanes
+    {
+      const int64_t tot = np * blk;
+      k_set_identity<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(GR + n * blk, sD, n_i, np);
+      RG_TRY(cu(cudaGetLastError()));
+      qt::count_launches(1);
+      cudaEvent_t fork = g.l0 == 0 ? q->ev_fork : q->ev_gdone[1];   // any free event of this group
+      RG_TRY(cu(cudaEventRecord(fork, st)));
+      for (int l = g.l0; l < g.l0 + g.nl; ++l) RG_TRY(cu(cudaStreamWaitEvent(q->ls[l], fork, 0)));
+      for (int64_t p = 0; p < np; ++p) {
+        const int l = g.l0 + (int)(p % g.nl);
+        cuDoubleComplex* Mp = reinterpret_cast<cuDoubleComplex*>(M + p * blk);
+        int* piv = q->piv + (g.p0 + p) * bs;
+        if (cusolverDnZgetrf(q->sh[l], n_i, n_i, Mp, n_i, reinterpret_cast<cuDoubleComplex*>(q->lwork) + (size_t)l * q->lwork_elems,
+                             piv, q->info + n * P + g.p0 + p) != CUSOLVER_STATUS_SUCCESS)
+          return QT_ERR_CUDA;
+        if (cusolverDnZgetrs(q->sh[l], CUBLAS_OP_N, n_i, n_i, Mp, n_i, piv,
+                             reinterpret_cast<cuDoubleComplex*>(GR + p * sD + n * blk), n_i,
+                             q->info + nb * P + g.p0 + p) != CUSOLVER_STATUS_SUCCESS)
+          return QT_ERR_CUDA;
+      }
+      for (int l = g.l0; l < g.l0 + g.nl; ++l) {
+        RG_TRY(cu(cudaEventRecord(q->ev_join[l], q->ls[l])));
+        RG_TRY(cu(cudaStreamWaitEvent(st, q->ev_join[l], 0)));
+      }
+    }
+    const double2* S[2] = {Sl, Sg};
+    double2* G[2] = {GL, GG};
+    for (int x = 0; x < 2; ++x) {
+      double2* Sx = T[2];
+      RG_TRY(copy(q, g, Sx, blk, S[x] + n * blk, sD));
+      if (n > 0) {
+        // Sx = Σ^x_n + A_{n,n-1} g^x_{n-1} A_{n,n-1}†
+        RG_TRY(gemm(q, g, Al + (n - 1) * blk, sO, false, G[x] + (n - 1) * blk, sD, false, T[3], blk, 1.0, 0.0));
+        RG_TRY(gemm(q, g, T[3], blk, false, Al + (n - 1) * blk, sO, true, Sx, blk, 1.0, 1.0));
+      }
+      // g^x_n = g^R_n Sx g^R_n†
+      RG_TRY(gemm(q, g, GR + n * blk, sD, false, Sx, blk, false, T[3], blk, 1.0, 0.0));
+      RG_TRY(gemm(q, g, T[3], blk, false, GR + n * blk, sD, true, G[x] + n * blk, sD, 1.0, 0.0));
+    }
+  }
+  // ---------------- backward pass: G_{nb-1} = g_{nb-1}; block n <- block n+1
+  const dim3 tb(32, 8), tg((unsigned)((bs + 31) / 32), (unsigned)((bs + 31) / 32), (unsigned)np);
+  for (int64_t n = nb - 2; n >= 0; --n) {
+    double2 *X = T[1], *Tt = T[2], *XT = T[3], *Zt = T[4], *Y = T[5], *W = T[6];
+    RG_TRY(gemm(q, g, GR + n * blk, sD, false, Au + n * blk, sO, false, X, blk, 1.0, 0.0));        // X = g^R_n A_{n,n+1}
+    RG_TRY(gemm(q, g, GR + (n + 1) * blk, sD, false, Al + n * blk, sO, false, Tt, blk, 1.0, 0.0)); // G^R_{n+1} A_{n+1,n}
+    RG_TRY(gemm(q, g, X, blk, false, Tt, blk, false, XT, blk, 1.0, 0.0));                          // XT
+    double2* Gx[2] = {GL, GG};
+    for (int x = 0; x < 2; ++x) {
+      double2* G = Gx[x];
+      RG_TRY(gemm(q, g, XT, blk, false, G + n * blk, sD, false, Y, blk, 1.0, 0.0));                // Y = XT g^x_n
+      RG_TRY(gemm(q, g, X, blk, false, G + (n + 1) * blk, sD, false, W, blk, 1.0, 0.0));           // W = X G^x_{n+1}
+      RG_TRY(gemm(q, g, W, blk, false, X, blk, true, G + n * blk, sD, 1.0, 1.0));                  // g^x_n += W X†
+      k_add_antiherm<<<tg, tb, 0, st>>>(G + n * blk, sD, Y, (int)bs);                               // += Y − Y†
+      RG_TRY(cu(cudaGetLastError()));
+      qt::count_launches(1);
+    }
+    RG_TRY(gemm(q, g, XT, blk, false, GR + n * blk, sD, false, Zt, blk, 1.0, 0.0));                // Z = XT g^R_n
+    const int64_t tot = np * blk;
+    const int grid = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+    k_add<<<grid, 256, 0, st>>>(GR + n * blk, sD, Zt, blk, np);                                     // G^R_n = g^R_n + Z
+    RG_TRY(cu(cudaGetLastError()));
+    qt::count_launches(1);
+  }
+  return QT_OK;
+}
+
+}  // namespace
 
 extern "C" qt_status qt_rgf_solve(qt_rgf_plan_t q, const void* Ad_, const void* Au_, const void* Al_, const void* Sl_,
                                   const void* Sg_, void* GR_, void* GL_, void* GG_, void* stream) {
@@ -223,100 +330,28 @@ extern "C" qt_status qt_rgf_solve(qt_rgf_plan_t q, const void* Ad_, const void* 
   if (q->d.bnum > 1 && (!Au_ || !Al_)) return QT_ERR_INVALID_ARG;
   if (GR_ == GL_ || GR_ == GG_ || GL_ == GG_) return QT_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  RG_TRY(cb(cublasSetStream(q->h, st)));
-  const int64_t P = q->d.P, nb = q->d.bnum, bs = q->d.bs, blk = bs * bs;
-  const double2* Ad = (const double2*)Ad_;
-  const double2* Au = (const double2*)Au_;
-  const double2* Al = (const double2*)Al_;
-  const double2* Sl = (const double2*)Sl_;
-  const double2* Sg = (const double2*)Sg_;
-  double2* GR = (double2*)GR_;
-  double2* GL = (double2*)GL_;
-  double2* GG = (double2*)GG_;
-  const int64_t sD = nb * blk, sO = (nb - 1) * blk;   // point strides of [P][bnum] and [P][bnum-1] tensors
-  double2* T[7];
-  for (int k = 0; k < 7; ++k) T[k] = q->tmp + k * P * blk;   // T[0] = M (pointer array ptrM)
-  // pointer array of the G^R output blocks (inverse destinations), rebuilt when the output moves
-  if (q->last_GR != GR_) {
-    q->hptrG.resize(nb * P);
-    for (int64_t n = 0; n < nb; ++n)
-      for (int64_t p = 0; p < P; ++p) q->hptrG[n * P + p] = GR + p * sD + n * blk;
-    RG_TRY(cu(cudaMemcpyAsync(q->ptrG, q->hptrG.data(), nb * P * sizeof(double2*), cudaMemcpyHostToDevice, st)));
-    q->last_GR = GR_;
+  const int64_t P = q->d.P, nb = q->d.bnum, blk = q->d.bs * q->d.bs;
+  const int64_t sD = nb * blk, sO = (nb - 1) * blk;
+  // fork: the groups start after the caller's stream has produced the inputs; join before returning
+  RG_TRY(cu(cudaEventRecord(q->ev_start, st)));
+  const int G = q->ngroups;
+  for (int gi = 0; gi < G; ++gi) {
+    Grp g;
+    g.p0 = P * gi / G;
+    g.np = P * (gi + 1) / G - g.p0;
+    g.h = q->gh[gi];
+    g.s = q->gs[gi];
+    g.nl = std::max(1, q->lanes / G);
+    g.l0 = std::min(gi * g.nl, q->lanes - g.nl);
+    RG_TRY(cu(cudaStreamWaitEvent(g.s, q->ev_start, 0)));
+    RG_TRY(solve_group(q, g, (const double2*)Ad_ + g.p0 * sD, Au_ ? (const double2*)Au_ + g.p0 * sO : nullptr,
+                       Al_ ? (const double2*)Al_ + g.p0 * sO : nullptr, (const double2*)Sl_ + g.p0 * sD,
+                       (const double2*)Sg_ + g.p0 * sD, (double2*)GR_ + g.p0 * sD, (double2*)GL_ + g.p0 * sD,
+                       (double2*)GG_ + g.p0 * sD));
   }
-  const int n_i = (int)bs;
-  // ---------------- forward pass: left-connected g^R_n (into GR), g^<_n (GL), g^>_n (GG)
-  for (int64_t n = 0; n < nb; ++n) {
-    double2* M = T[0];
-    RG_TRY(copy(q, M, blk, Ad + n * blk, sD, st));
-    if (n > 0) {
-      // T1 = A_{n,n-1} g^R_{n-1};  M = A_nn − T1 A_{n-1,n}
-      RG_TRY(gemm(q, Al + (n - 1) * blk, sO, false, GR + (n - 1) * blk, sD, false, T[1], blk, 1.0, 0.0));
-      RG_TRY(gemm(q, T[1], blk, false, Au + (n - 1) * blk, sO, false, M, blk, -1.0, 1.0));
-    }
-    // g^R_n = M^{-1}: per point, LU of M_p (in place) and a solve against the identity written into block n of GR
-    {
-      const int64_t tot = P * blk;
-      k_set_identity<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(GR + n * blk, sD, n_i, P);
-      RG_TRY(cu(cudaGetLastError()));
-      qt::count_launches(1);
-      RG_TRY(cu(cudaEventRecord(q->ev_fork, st)));
-      for (int l = 0; l < q->lanes; ++l) RG_TRY(cu(cudaStreamWaitEvent(q->ls[l], q->ev_fork, 0)));
-      for (int64_t p = 0; p < P; ++p) {
-        const int l = (int)(p % q->lanes);
-        cuDoubleComplex* Mp = reinterpret_cast<cuDoubleComplex*>(M + p * blk);
-        int* piv = q->piv + p * bs;
-        if (cusolverDnZgetrf(q->sh[l], n_i, n_i, Mp, n_i, reinterpret_cast<cuDoubleComplex*>(q->lwork) + (size_t)l * q->lwork_elems,
-                             piv, q->info + n * P + p) != CUSOLVER_STATUS_SUCCESS)
-          return QT_ERR_CUDA;
-        if (cusolverDnZgetrs(q->sh[l], CUBLAS_OP_N, n_i, n_i, Mp, n_i, piv,
-                             reinterpret_cast<cuDoubleComplex*>(GR + p * sD + n * blk), n_i,
-                             q->info + nb * P + p) != CUSOLVER_STATUS_SUCCESS)
-          return QT_ERR_CUDA;
-      }
-      for (int l = 0; l < q->lanes; ++l) {
-        RG_TRY(cu(cudaEventRecord(q->ev_join[l], q->ls[l])));
-        RG_TRY(cu(cudaStreamWaitEvent(st, q->ev_join[l], 0)));
-      }
-    }
-    const double2* S[2] = {Sl, Sg};
-    double2* G[2] = {GL, GG};
-    for (int x = 0; x < 2; ++x) {
-      double2* Sx = T[2];
-      RG_TRY(copy(q, Sx, blk, S[x] + n * blk, sD, st));
-      if (n > 0) {
-        // Sx = Σ^x_n + A_{n,n-1} g^x_{n-1} A_{n,n-1}†
-        RG_TRY(gemm(q, Al + (n - 1) * blk, sO, false, G[x] + (n - 1) * blk, sD, false, T[3], blk, 1.0, 0.0));
-        RG_TRY(gemm(q, T[3], blk, false, Al + (n - 1) * blk, sO, true, Sx, blk, 1.0, 1.0));
-      }
-      // g^x_n = g^R_n Sx g^R_n†
-      RG_TRY(gemm(q, GR + n * blk, sD, false, Sx, blk, false, T[3], blk, 1.0, 0.0));
-      RG_TRY(gemm(q, T[3], blk, false, GR + n * blk, sD, true, G[x] + n * blk, sD, 1.0, 0.0));
-    }
-  }
-  // ---------------- backward pass: G_{nb-1} = g_{nb-1}; block n <- block n+1
-  const dim3 tb(32, 8), tg((unsigned)((bs + 31) / 32), (unsigned)((bs + 31) / 32), (unsigned)P);
-  for (int64_t n = nb - 2; n >= 0; --n) {
-    double2 *X = T[1], *Tt = T[2], *XT = T[3], *Zt = T[4], *Y = T[5], *W = T[6];
-    RG_TRY(gemm(q, GR + n * blk, sD, false, Au + n * blk, sO, false, X, blk, 1.0, 0.0));        // X = g^R_n A_{n,n+1}
-    RG_TRY(gemm(q, GR + (n + 1) * blk, sD, false, Al + n * blk, sO, false, Tt, blk, 1.0, 0.0)); // G^R_{n+1} A_{n+1,n}
-    RG_TRY(gemm(q, X, blk, false, Tt, blk, false, XT, blk, 1.0, 0.0));                          // XT
-    const double2* Gx[2] = {GL, GG};
-    for (int x = 0; x < 2; ++x) {
-      double2* G = const_cast<double2*>(Gx[x]);
-      RG_TRY(gemm(q, XT, blk, false, G + n * blk, sD, false, Y, blk, 1.0, 0.0));                // Y = XT g^x_n
-      RG_TRY(gemm(q, X, blk, false, G + (n + 1) * blk, sD, false, W, blk, 1.0, 0.0));           // W = X G^x_{n+1}
-      RG_TRY(gemm(q, W, blk, false, X, blk, true, G + n * blk, sD, 1.0, 1.0));                  // g^x_n += W X†
-      k_add_antiherm<<<tg, tb, 0, st>>>(G + n * blk, sD, Y, (int)bs);                            // += Y − Y†
-      RG_TRY(cu(cudaGetLastError()));
-      qt::count_launches(1);
-    }
-    RG_TRY(gemm(q, XT, blk, false, GR + n * blk, sD, false, Zt, blk, 1.0, 0.0));                // Z = XT g^R_n
-    const int64_t tot = P * blk;
-    const int grid = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
-    k_add<<<grid, 256, 0, st>>>(GR + n * blk, sD, Zt, blk, P);                                   // G^R_n = g^R_n + Z
-    RG_TRY(cu(cudaGetLastError()));
-    qt::count_launches(1);
+  for (int gi = 0; gi < G; ++gi) {
+    RG_TRY(cu(cudaEventRecord(q->ev_gdone[gi], q->gs[gi])));
+    RG_TRY(cu(cudaStreamWaitEvent(st, q->ev_gdone[gi], 0)));
   }
   return QT_OK;
 }
