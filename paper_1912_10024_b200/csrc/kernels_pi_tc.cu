@@ -216,125 +216,8 @@ static cudaError_t launch_pi_w_tc_no(const PiWArgs& a, float* Wp, int NNp, int64
   return cudaGetLastError();
 }
 
-// Warp-per-energy form of k_pi_w_tc (same arithmetic and output; cf. k_pi_w2 in kernels_pi.cu): CTA = (pair, kz),
-// warp w owns energies e ≡ w (mod kTW2Warps); phase 1 lane (i, q): row q of T_i = G_b ∇_iH_{br} (FP32) into the
-// warp's T buffer; phase 2 lane (j, y): W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x], stored as the four split
-// planes. The xy padding columns of each energy and the K tail of the pair's rows are zeroed here too.
-constexpr int kTW2Warps = 4;
-
-template <int NO>
-__global__ void __launch_bounds__(kTW2Warps * 32) k_pi_w2_tc(PiWArgs A, float* __restrict__ Wp, int NNp) {
-  constexpr int NN = NO * NO, NNP = NN + 2;
-  static_assert(3 * NO <= 32, "lanes (i, q) / (j, y)");
-  extern __shared__ __align__(16) float2 w2t_sm[];
-  float2* Hr = w2t_sm;                           // [3][NNP]  ∇_iH_{br}
-  float2* Tw = Hr + 3 * NNP;                     // [kTW2Warps][3][NNP]
-  const int kz = (int)(blockIdx.x % A.Nkz);
-  const int64_t pg = A.p0 + blockIdx.x / A.Nkz;
-  const int64_t item = A.pair_item[pg];
-  const PiItem it = A.items[item];
-  const PiPair pr = A.pairs[pg];
-  const int t = (int)(pg - it.pair0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int idx = threadIdx.x; idx < 3 * NN; idx += blockDim.x) {
-    const int i = idx / NN, rc = idx - i * NN;
-    Hr[i * NNP + rc] = Cx<float>::from(A.dH[((int64_t)pr.b_in * A.Nb + pr.r) * 3 * NN + idx]);
-  }
-  const bool act = lane < 3 * NO;
-  const int hi = min(lane / NO, 2), lo = lane % NO;
-  float2 hl[NO];
-#pragma unroll
-  for (int k = 0; k < NO; ++k)
-    hl[k] = Cx<float>::from(A.dH[((int64_t)pr.a_in * A.Nb + pr.s) * 3 * NN + hi * NN + lo * NO + k]);
-  __syncthreads();
-  const int KwB = ((A.NEo * NNp + kPKC - 1) / kPKC) * kPKC;
-  const int64_t K = (int64_t)A.Nkz * KwB;
-  const int64_t plane = (int64_t)kTcPiRows * K;
-  float* Wi = Wp + (item - A.i0) * 4 * plane;
-  float2* T = Tw + warp * 3 * NNP;
-  const float2* hr = Hr + hi * NNP;
-  const double2* gsrc = A.GY + (((int64_t)kz * A.NE + A.E0) * A.Nwin + pr.b_in) * NN + lo * NO;
-  const int64_t gstep = (int64_t)A.Nwin * NN;
-  for (int e = warp; e < A.NEo; e += kTW2Warps) {
-    float2 g[NO];
-#pragma unroll
-    for (int p = 0; p < NO; ++p) g[p] = Cx<float>::from(__ldg(gsrc + e * gstep + p));
-    float2 tr[NO];
-#pragma unroll
-    for (int x = 0; x < NO; ++x) tr[x] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int p = 0; p < NO; ++p)
-#pragma unroll
-      for (int x = 0; x < NO; ++x) cfma(tr[x], g[p], hr[p * NO + x]);
-    if (act) {
-#pragma unroll
-      for (int x = 0; x < NO; ++x) T[hi * NNP + lo * NO + x] = tr[x];
-    }
-    __syncwarp();
-#pragma unroll 1
-    for (int i = 0; i < 3; ++i) {
-      float2 w[NO];
-#pragma unroll
-      for (int x = 0; x < NO; ++x) w[x] = make_float2(0.f, 0.f);
-      const float2* ti = T + i * NNP;
-#pragma unroll
-      for (int q = 0; q < NO; ++q)
-#pragma unroll
-        for (int x = 0; x < NO; ++x) cfma(w[x], hl[q], ti[q * NO + x]);
-      if (act) {
-        float* o = Wi + (int64_t)(t * 9 + i * 3 + hi) * K + (int64_t)kz * KwB + (int64_t)e * NNp + lo;
-#pragma unroll
-        for (int x = 0; x < NO; ++x) {
-          const float hr_ = tf32_rna_p(w[x].x), hi_ = tf32_rna_p(w[x].y);
-          o[x * NO] = hr_;
-          o[plane + x * NO] = tf32_rna_p(w[x].x - hr_);
-          o[2 * plane + x * NO] = hi_;
-          o[3 * plane + x * NO] = tf32_rna_p(w[x].y - hi_);
-        }
-      }
-    }
-    // zero the xy padding columns NN..NNp of this energy's 9 rows (4 planes)
-    const int npad = NNp - NN;
-    for (int u = lane; u < 9 * 4 * npad; u += 32) {
-      const int c = u % npad, r1 = u / npad, pl = r1 % 4, ij = r1 / 4;
-      Wi[pl * plane + (int64_t)(t * 9 + ij) * K + (int64_t)kz * KwB + (int64_t)e * NNp + NN + c] = 0.0f;
-    }
-    __syncwarp();
-  }
-  // zero the K tail of the pair's rows for this kz (positions NEo·NNp .. KwB of the kz block)
-  const int tail = KwB - A.NEo * NNp;
-  for (int u = threadIdx.x; u < 9 * 4 * tail; u += blockDim.x) {
-    const int c = u % tail, r1 = u / tail, pl = r1 % 4, ij = r1 / 4;
-    Wi[pl * plane + (int64_t)(t * 9 + ij) * K + (int64_t)kz * KwB + A.NEo * NNp + c] = 0.0f;
-  }
-}
-
-template <int NO>
-static cudaError_t launch_pi_w2_tc_no(const PiWArgs& a, float* Wp, int NNp, cudaStream_t st) {
-  const int smem = (1 + kTW2Warps) * 3 * (NO * NO + 2) * 8;
-  cudaError_t e = cudaFuncSetAttribute(k_pi_w2_tc<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  k_pi_w2_tc<NO><<<(unsigned)(a.npairs * a.Nkz), kTW2Warps * 32, smem, st>>>(a, Wp, NNp);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_pi_w_tc(const PiWArgs& a, float* Wp, int NNp, int64_t nitems, cudaStream_t st) {
   if (nitems * a.Nkz == 0) return cudaSuccess;
-#ifndef QT_PIW_OLD
-  switch (a.Norb) {
-    case 1: return launch_pi_w2_tc_no<1>(a, Wp, NNp, st);
-    case 2: return launch_pi_w2_tc_no<2>(a, Wp, NNp, st);
-    case 3: return launch_pi_w2_tc_no<3>(a, Wp, NNp, st);
-    case 4: return launch_pi_w2_tc_no<4>(a, Wp, NNp, st);
-    case 5: return launch_pi_w2_tc_no<5>(a, Wp, NNp, st);
-    case 6: return launch_pi_w2_tc_no<6>(a, Wp, NNp, st);
-    case 7: return launch_pi_w2_tc_no<7>(a, Wp, NNp, st);
-    case 8: return launch_pi_w2_tc_no<8>(a, Wp, NNp, st);
-    case 9: return launch_pi_w2_tc_no<9>(a, Wp, NNp, st);
-    case 10: return launch_pi_w2_tc_no<10>(a, Wp, NNp, st);
-    default: break;
-  }
-#endif
   switch (a.Norb) {
     case 1: return launch_pi_w_tc_no<1>(a, Wp, NNp, nitems, st);
     case 2: return launch_pi_w_tc_no<2>(a, Wp, NNp, nitems, st);
