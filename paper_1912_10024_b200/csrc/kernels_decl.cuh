@@ -1,4 +1,5 @@
-// kernels_decl.cuh — launcher declarations (definitions in kernels_sigma.cu / kernels_pi.cu).
+// kernels_decl.cuh — launcher declarations (definitions in kernels_sigma_tma.cu, kernels_sigma_tc.cu, kernels_pi.cu,
+// kernels_pi_tc.cu).
 #pragma once
 #include "common.cuh"
 
@@ -86,10 +87,8 @@ struct PiSelfArgs {
 
 constexpr int kEB = 4;
 
-cudaError_t launch_sigma_coef(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma_coef_tiled(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
-cudaError_t launch_sigma_cp(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_sand_det(const SigmaArgs& a, cudaStream_t st);   // QT_FLAG_DETERMINISTIC
 // FP32 mixed-precision Σ contraction (tcgen05 kind::tf32; kernels_sigma_tc.cu). Coefficient planes

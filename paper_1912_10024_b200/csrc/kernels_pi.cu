@@ -180,14 +180,25 @@ __global__ void __launch_bounds__(kW2Warps * 32) k_pi_w2(PiWArgs A) {
     // phase 2: W^{ij}[x][y] = Σ_q ∇_jH_{as}[y][q] T_i[q][x]; row (t, i, j), column xy = x·Norb + y
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
-      double2 w[NO];
+      double2 w[NO], wm[NO];   // split accumulators: four independent FMA chains per complex element
 #pragma unroll
-      for (int x = 0; x < NO; ++x) w[x] = make_double2(0.0, 0.0);
+      for (int x = 0; x < NO; ++x) w[x] = wm[x] = make_double2(0.0, 0.0);
       const double2* ti = T + i * NNP;
 #pragma unroll
       for (int q = 0; q < NO; ++q)
 #pragma unroll
-        for (int x = 0; x < NO; ++x) cfma(w[x], hl[q], ti[q * NO + x]);
+        for (int x = 0; x < NO; ++x) {
+          const double2 b = ti[q * NO + x];
+          w[x].x = fma(hl[q].x, b.x, w[x].x);
+          wm[x].x = fma(hl[q].y, b.y, wm[x].x);
+          w[x].y = fma(hl[q].x, b.y, w[x].y);
+          wm[x].y = fma(hl[q].y, b.x, wm[x].y);
+        }
+#pragma unroll
+      for (int x = 0; x < NO; ++x) {
+        w[x].x -= wm[x].x;
+        w[x].y += wm[x].y;
+      }
       if (act) {
         const int row = t * 9 + i * 3 + hi;
 #pragma unroll

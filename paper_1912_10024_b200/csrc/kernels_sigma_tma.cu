@@ -1,16 +1,20 @@
 // kernels_sigma_tma.cu — Σ≷ D-contraction + sandwich (Eq. 3), warp-specialized
-// TMA / mbarrier pipeline for sm_100a (Norb <= 10).
+// TMA / mbarrier pipeline for sm_100a (Norb <= 12).
 //
-// Same GEMM as kernels_sigma.cu (rows (pair t, ij): 72 = 9 DMMA m-fragments; columns rc = Norb²;
-// K = (q, d) with a Hankel G_b operand), reorganized so that the FP64 tensor pipe never waits on
-// block-wide barriers or address arithmetic:
+// Reformulation (exact up to rounding): for a pair p = (a,s), b = nbr[a][s],
+//   Gt_p^{ij}(kz,E) = Σ_{q,d} C_p^{ij}(q,d) · G_b(kz-q+h, E+d)              (D-contraction, k_sigma)
+//   Σ_a(kz,E)      = scale · Σ_s Σ_i ∇_iH_{as} ( Σ_j Gt_p^{ij} ∇_jH_{br} )     (sandwich + neighbour sum)
+// with C_p^{ij}(q,-s_m) = Dc^X_{ij}(q,m), C_p^{ij}(q,+s_m) = Dc^Y_{ji}(q,m), 0 otherwise (R2, R3).
+// The contraction is a GEMM with rows (pair t, ij) — the ≤ 8 pairs sharing one source atom b, 72 rows = 9 DMMA
+// m-fragments — columns rc (the Norb² entries of G_b) and K = (q, d): the G operand is a Hankel window of G_b
+// rows E+d. The kernel is organized so that the FP64 tensor pipe never waits on block-wide barriers:
 //   warp 18          : producer. One elected lane issues, per stage, three bulk loads: the G_b rows
 //                      E-Dmax+d0 .. +KC straight from the caller's G window in the paper layout (a 4-D box of
 //                      one atom x KC energies; TMA zero-fills rows outside [0,NE): reading R7, and the padding
 //                      columns Norb²..NPS), the same rows of the Re+Im plane, and the 72 x KCP coefficient tile.
 //   warps 0..17      : consumers. Warp w owns m-fragment w%9 and half of the n-fragments; it waits on the
 //                      stage's `full` mbarrier, runs DMMA.8x8x4, and releases the stage on `empty`.
-// Epilogue (all warps): Gt -> smem, V^i = Σ_j Gt^{ij} ∇_jH_{br}, S = Σ_i ∇_iH_{as} V^i, Σ_a += scale·S.
+// Gt tiles go to the chunk's scratch; the sandwich kernels below add ∇H·Gt·∇H into Σ_a.
 #include "kernels_decl.cuh"
 #include "tma.cuh"
 
@@ -92,7 +96,8 @@ struct SigTmaCfg {
 #ifndef QT_SIG_STAGES
 #define QT_SIG_STAGES 4
 #endif
-  static constexpr int STAGES = QT_SIG_STAGES;
+  // Norb 11, 12 (NF = 16, 18): a stage is 61 KB, three fit next to each other
+  static constexpr int STAGES = NF > 13 ? 3 : QT_SIG_STAGES;
   static constexpr int G_STAGE = KC * NPS;   // complex elements
   static constexpr int S_STAGE = (KC * NPS / 2 + 7) & ~7;   // Re+Im plane of the G rows (doubles), complex units
   static constexpr int C_STAGE = kRows * KCP;
@@ -312,6 +317,9 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 #ifndef QT_SAND_W
 #define QT_SAND_W 12
 #endif
+#ifndef QT_SAND_SPLIT
+#define QT_SAND_SPLIT 1
+#endif
 #ifndef QT_SAND_S
 #define QT_SAND_S 14
 #endif
@@ -389,6 +397,13 @@ __global__ void __launch_bounds__((kSandWarps + 1) * 32) k_sigma_sand(SigmaArgs 
     C2 u[NO];
 #pragma unroll
     for (int v = 0; v < NO; ++v) u[v] = Cx<R>::zero();
+#if QT_SAND_SPLIT
+    // split accumulators: u = (Σ hr·gr − Σ hi·gi, Σ hr·gi + Σ hi·gr) with the four real sums in independent
+    // FMA chains (the two FMAs of one complex MAC no longer depend on each other)
+    C2 um[NO];
+#pragma unroll
+    for (int v = 0; v < NO; ++v) um[v] = Cx<R>::zero();
+#endif
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {   // (i, k) loops rolled: keeps the kernel inside the instruction cache
       const C2* gr = g + (i * 3 + j) * NNP;
@@ -397,9 +412,26 @@ __global__ void __launch_bounds__((kSandWarps + 1) * 32) k_sigma_sand(SigmaArgs 
       for (int k = 0; k < NO; ++k) {
         const C2 h = hl[k];
 #pragma unroll
-        for (int v = 0; v < NO; ++v) cfma(u[v], h, gr[k * NO + v]);
+        for (int v = 0; v < NO; ++v) {
+#if QT_SAND_SPLIT
+          const C2 b = gr[k * NO + v];
+          u[v].x = fma(h.x, b.x, u[v].x);
+          um[v].x = fma(h.y, b.y, um[v].x);
+          u[v].y = fma(h.x, b.y, u[v].y);
+          um[v].y = fma(h.y, b.x, um[v].y);
+#else
+          cfma(u[v], h, gr[k * NO + v]);
+#endif
+        }
       }
     }
+#if QT_SAND_SPLIT
+#pragma unroll
+    for (int v = 0; v < NO; ++v) {
+      u[v].x -= um[v].x;
+      u[v].y += um[v].y;
+    }
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);   // the slot's rows are in registers now
     C2 sv[NO];
@@ -544,7 +576,9 @@ cudaError_t launch_sigma_sand_det(const SigmaArgs& a, cudaStream_t st) {
     case 8: return launch_sand_det_no<8>(a, st);
     case 9: return launch_sand_det_no<9>(a, st);
     case 10: return launch_sand_det_no<10>(a, st);
-    default: return cudaErrorInvalidValue;   // Norb 11, 12 (cp.async kernel, atomics): rejected at plan time
+    case 11: return launch_sand_det_no<11>(a, st);
+    case 12: return launch_sand_det_no<12>(a, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 
@@ -637,7 +671,7 @@ cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t s
     case 8: return launch_sand_no<8>(a, nitems, st);
     case 9: return launch_sand_no<9>(a, nitems, st);
     case 10: return launch_sand_no<10>(a, nitems, st);
-    default: return cudaSuccess;   // Norb 11, 12: the cp.async kernel applies the sandwich itself
+    default: return cudaErrorInvalidValue;   // Norb 11, 12 (3·Norb > 32 lanes): the destination-ordered kernel
   }
 }
 
@@ -651,7 +685,9 @@ cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st) {
     case 8: return launch_sigma_tma_nf<8>(a, nitems, st);
     case 11: return launch_sigma_tma_nf<11>(a, nitems, st);
     case 13: return launch_sigma_tma_nf<13>(a, nitems, st);
-    default: return launch_sigma_cp(a, nitems, st);   // Norb 11, 12
+    case 16: return launch_sigma_tma_nf<16>(a, nitems, st);   // Norb 11
+    case 18: return launch_sigma_tma_nf<18>(a, nitems, st);   // Norb 12 (the paper's FinFET basis)
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -251,9 +251,9 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
   L->fp32 = d.precision == QT_PREC_FP32_MIXED;
   L->g = geom_of(&d, nbr, d.rank, reduce);
   const Geom& g = L->g;
-  if (strict && g.TE > 1 && d.Norb > 10) return QT_ERR_UNSUPPORTED;   // energy windows: TMA / tcgen05 kernels only
-  L->det = (d.flags & QT_FLAG_DETERMINISTIC) != 0;
-  if (strict && L->det && d.Norb > 10) return QT_ERR_UNSUPPORTED;     // the Norb 11-12 kernel sums with atomics
+  // Σ sandwich: the warp-per-energy kernel needs 3·Norb <= 32 lanes; Norb 11, 12 (and QT_FLAG_DETERMINISTIC) use the
+  // destination-ordered kernel, whose per-chunk destination lists are built below
+  L->det = (d.flags & QT_FLAG_DETERMINISTIC) != 0 || d.Norb > 10;
   L->reduce = reduce && g.TE > 1;
   L->Nwin = g.w_hi - g.w_lo;
   L->Nout = g.a_hi - g.a_lo;
@@ -360,7 +360,7 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
                                     : gt_per_item;
   L->NEp = std::max<int64_t>(32, (L->NEw + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
   L->Kp = (L->Dwin + 3 + 31) & ~int64_t(31);                      // delayed coefficient rows, whole 32-chunks
-  L->sig_tma = d.Norb <= 10;
+  L->sig_tma = true;   // every Norb <= 12 runs the TMA / mbarrier contraction
   L->ndc = (L->Dwin + 15) / 16;
   const size_t coef_item_t = L->fp32 ? (size_t)d.Nqz * 16 * kTcRows * L->Kp * sizeof(float)
                                      : (size_t)d.Nqz * L->ndc * kRows * kCoefKCP * sizeof(double2);
@@ -381,9 +381,8 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
       G.chunks.push_back(i1);
     }
   }
-  // Σ chunks. TMA path (Norb <= 10): per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] + its
-  // Gt scratch; cp.async path (Norb 11, 12): per pair coefficient rows. Workspace = [coef | Gt]. A chunk never
-  // mixes interior and halo sources.
+  // Σ chunks: per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] + its Gt scratch.
+  // Workspace = [coef | Gt]. A chunk never mixes interior and halo sources.
   {
     const size_t gt_item = L->sig_tma ? gt_per_item : 0;
     size_t coef_acc = 0, gt_acc = 0, coef_max = 0;
@@ -674,9 +673,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       ca.nitems = i1 - i0;
       ca.ndc = L.ndc;
       ca.Dwin = L.Dwin;
-      QT_LAUNCH(QT_K_SIGMA_COEF, L.fp32      ? launch_sigma_coef_tc(ca, (int)L.Kp, cs)
-                                 : L.sig_tma ? launch_sigma_coef_tiled(ca, cs)
-                                             : launch_sigma_coef(ca, cs));
+      QT_LAUNCH(QT_K_SIGMA_COEF, L.fp32 ? launch_sigma_coef_tc(ca, (int)L.Kp, cs) : launch_sigma_coef_tiled(ca, cs));
       QT_TRY(wait_halo(ch.g_halo));
       SigmaArgs sa;
       sa.G = (const double2*)(X == 0 ? GL : GG);

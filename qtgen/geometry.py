@@ -103,6 +103,8 @@ CONFIGS = {
     "small": dict(cells=(8, 2, 2), Nb=4, Norb=10, NE=256, Nw=16, Nkz=3),
     "cfg3":  dict(cells=(38, 4, 4), Nb=34, Norb=10, NE=176, Nw=70, Nkz=3),
     "cfg3_nb4": dict(cells=(38, 4, 4), Nb=4, Norb=10, NE=176, Nw=70, Nkz=3),
+    # the paper's own FinFET orbital count (Norb = 12; Table 2's OMEN row) on the cfg3 slice
+    "cfg3_norb12": dict(cells=(38, 4, 4), Nb=34, Norb=12, NE=176, Nw=70, Nkz=3),
     # profiling slice: cfg3's per-atom shape (Nb=34, NE=176, Nω=70, Nkz=3) on 384 atoms
     "prof":  dict(cells=(3, 4, 4), Nb=34, Norb=10, NE=176, Nw=70, Nkz=3),
     "cfg4":  dict(cells=(38, 4, 4), Nb=34, Norb=10, NE=706, Nw=70, Nkz=7),
