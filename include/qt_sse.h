@@ -61,7 +61,7 @@ extern "C" {
 typedef enum {
   QT_OK = 0,
   QT_ERR_INVALID_ARG = 1,   /* bad dims, neighbour table, grid, null/misaligned/aliased pointer          */
-  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12 (> 10 in FP32 mode or with TE > 1), Nω·shift_step > 128 (80)     */
+  QT_ERR_UNSUPPORTED = 2,   /* Norb > 12 (> 10 in FP32 mode), (Nω−1)·shift_step + 1 > 128 (80) shifts    */
   QT_ERR_OUT_OF_MEMORY = 3,
   QT_ERR_CUDA = 4,
   QT_ERR_NCCL = 5,
