@@ -4,7 +4,7 @@
  * The library evaluates, for X ∈ {<,>} and Y the other one:
  *   Σ^X_aa(kz,E)  — Eq. 3, PAPER.md P:355-365 (electron SSE, diagonal atom blocks)
  *   Π^X_ab(ω,qz)  — Eq. 4, PAPER.md P:366-375 (phonon SSE, self + N_b neighbour blocks)
- * from the tensors of PAPER.md P:386-397, with the readings R1-R19 of DESIGN.md §3:
+ * from the tensors of PAPER.md P:386-397, with the readings R1-R20 of DESIGN.md §3:
  *   Σ^X[kz][E][a] = scale_Σ · Σ_{s,qz,m} Σ_{i,j} ∇_iH_{ab} ·
  *        ( Dc^X_{ij}(qz,m) G^X_b(kz-qz, E-s_m) + Dc^Y_{ji}(qz,m) G^X_b(kz-qz, E+s_m) ) · ∇_jH_{ba}
  *   Dc^X_{ij}(qz,m) = D^X[qz][m][b][r+1] - D^X[qz][m][b][0] - D^X[qz][m][a][0] + D^X[qz][m][a][s+1]
@@ -80,8 +80,8 @@ typedef struct {
   int32_t shift0, shift_step;                  /* ħω_m/ΔE = shift0 + m·shift_step; shift0, shift_step ≥ 1     */
   qt_precision precision;                      /* QT_PREC_FP64, or QT_PREC_FP32_MIXED (Norb <= 10): both      */
                                                /* contractions on tcgen05 (kind::tf32, operands split hi+lo,  */
-                                               /* FP32 products and TMEM segments re-accumulated in FP64), the */
-                                               /* ∇H sandwiches in FP32; ≤1e-5 per block (SURVEY §8(f)      */
+                                               /* TMEM segments of 128 products summed in registers: Σ FP32, */
+                                               /* Π FP64), the ∇H sandwiches in FP32; ≤1e-5 per block (§8(f) */
                                                /* NEXT(1), §4.4)                           */
   qt_shard shard;                              /* QT_SHARD_NONE, or with nranks > 1 ATOM / ENERGY / 2D        */
   int32_t rank, nranks;
