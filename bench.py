@@ -281,6 +281,9 @@ def main():
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32 = QT_PREC_FP32_MIXED (reported separately: contractions on tcgen05 tf32x3)")
     ap.add_argument("--separate", action="store_true", help="qt_sse_sigma + qt_sse_pi instead of the fused call")
+    ap.add_argument("--fill-halo", action="store_true",
+                    help="generate the whole input window (halo included) in place instead of the owned block + NaN "
+                         "halo (no owned-block temporaries: for cfg5-sized windows; the exchange rewrites the same values)")
     ap.add_argument("--workload", default="sse", choices=["sse", "rgf"],
                     help="rgf = the GF-phase RGF solver (SURVEY §8(f) NEXT(4)); reported separately, 1 GPU")
     args = ap.parse_args()
@@ -342,20 +345,27 @@ def main():
     dH_full = torch.empty((p.Na, p.Nb, 3, p.Norb, p.Norb), dtype=c128, device=dev)
     # each rank generates only its OWNED block; the halo region is left as garbage (NaN) for the library's
     # exchange to fill inside every timed step
-    G_less.fill_(float("nan"))
-    G_gtr.fill_(float("nan"))
-    D_less.fill_(float("nan"))
-    D_gtr.fill_(float("nan"))
-    for t, tid in ((G_less, qtgen.ID_GL), (G_gtr, qtgen.ID_GG)):
-        own = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
-        qtgen.dev_G(p, tid, own, e_lo=e_lo, e_hi=e_hi, a_lo=a_lo, a_hi=a_hi)
-        t[:, e_lo - ew_lo:e_hi - ew_lo, a_lo - w_lo:a_hi - w_lo] = own
-        del own
-    for t, tid in ((D_less, qtgen.ID_DL), (D_gtr, qtgen.ID_DG)):
-        own = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
-        qtgen.dev_D(p, tid, own, nbr_dev, a_lo=a_lo, a_hi=a_hi)
-        t[:, :, a_lo - w_lo:a_hi - w_lo] = own
-        del own
+    if args.fill_halo:
+        qtgen.dev_G(p, qtgen.ID_GL, G_less, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_G(p, qtgen.ID_GG, G_gtr, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_D(p, qtgen.ID_DL, D_less, nbr_dev, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_D(p, qtgen.ID_DG, D_gtr, nbr_dev, a_lo=w_lo, a_hi=w_hi)
+    else:
+        G_less.fill_(float("nan"))
+        G_gtr.fill_(float("nan"))
+        D_less.fill_(float("nan"))
+        D_gtr.fill_(float("nan"))
+        for t, tid in ((G_less, qtgen.ID_GL), (G_gtr, qtgen.ID_GG)):
+            own = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
+            qtgen.dev_G(p, tid, own, e_lo=e_lo, e_hi=e_hi, a_lo=a_lo, a_hi=a_hi)
+            t[:, e_lo - ew_lo:e_hi - ew_lo, a_lo - w_lo:a_hi - w_lo] = own
+            del own
+        for t, tid in ((D_less, qtgen.ID_DL), (D_gtr, qtgen.ID_DG)):
+            own = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
+            qtgen.dev_D(p, tid, own, nbr_dev, a_lo=a_lo, a_hi=a_hi)
+            t[:, :, a_lo - w_lo:a_hi - w_lo] = own
+            del own
+    torch.cuda.empty_cache()
     if world == 1:
         assert not torch.isnan(G_less).any()
     qtgen.dev_dH(p, dH_full, nbr_dev)
