@@ -197,6 +197,27 @@ def test_deterministic_flag_cfg3_sampled():
         assert float((num[den > 0] / den[den > 0]).max()) <= TOL
 
 
+def test_calls_on_two_streams_are_ordered():
+    """qt_sse_sigma on one stream and qt_sse_pi on another share the plan's scratch: the plan orders them (each call
+    waits for the previous call's completion event when the stream changes)."""
+    p = micro(Na=14, Nb=12, Norb=3, NE=12, Nw=3, Nkz=3, fill=0.9, seed=5)
+    inp = inputs(p, seed=81)
+    t = to_dev(inp)
+    ref = gpu_run(p, inp)
+    plan = qt.Plan(p, workspace_limit=1)   # many chunks: long, overlapping-prone call sequences
+    sh = p.shapes()
+    out = {k: torch.empty(sh["G" if k[0] == "S" else "D"], dtype=torch.complex128, device="cuda")
+           for k in ("S_less", "S_gtr", "P_less", "P_gtr")}
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        plan.sigma(t["dH"], t["G_less"], t["G_gtr"], t["D_less"], t["D_gtr"], out["S_less"], out["S_gtr"], 1j, s1)
+        plan.pi(t["dH"], t["G_less"], t["G_gtr"], out["P_less"], out["P_gtr"], -1j, s2)
+    torch.cuda.synchronize()
+    plan.close()
+    for k in out:
+        assert rel_fro(out[k].cpu().numpy(), ref[k], AX) <= 1e-13
+
+
 def test_outputs_overwritten_not_accumulated():
     p = micro(**MICROS[1])
     inp = inputs(p, seed=5)
