@@ -41,7 +41,9 @@ struct SigmaArgs {
   int64_t Nwin, Nout, Nb, DWp, cp0, npairs_chunk, ntiles;
   int NE, Nkz, Nqz, h, Norb, NN, Dmax, Dwin, ndc;
   int rows;              // Gt rows per (item, kz, E) block: 72 (items of <= 8 pairs) or 128 (FP32 mode, <= 14)
-  int E0, NEo;           // energy sharding: outputs for window energies [E0, E0 + NEo) (NE = the G window)
+  int E0, NEo;           // outputs for window energies [E0, E0 + NEo) (NE = the G window; a sub-range of the rank's
+                         // energies when the scratch is split by energy)
+  int NEs, Es0;          // Σ tensor: NEs energies per kz; this launch's energies start at Σ energy Es0
   int gt_f32;            // Gt scratch holds float2 (FP32 mixed mode: k_sigma_tc -> FP32 sandwich)
   int gt_ld;             // Gt scratch row stride in elements: Norb² rounded up to a 16-byte multiple
   // QT_FLAG_DETERMINISTIC: destination lists of the chunk — entry = {a_out, first, count, -} into det_pairs
@@ -77,6 +79,7 @@ struct PiCArgs {
   int NWv, step;         // GEMM columns = every shift shift0 + c (c < NWv); column c is frequency m = c / step
                          // when c % step == 0 (shift_step > 1: the other columns are computed and dropped)
   int E0, NEo;           // energies of this rank's Π sum: window energies [E0, E0 + NEo)
+  int accumulate;        // add into Π (later energy sub-ranges of a chunk) instead of overwriting
 };
 
 struct PiSelfArgs {

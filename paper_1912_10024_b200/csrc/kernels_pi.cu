@@ -421,8 +421,15 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int c = c0 + k, m = c / A.step;
-              if (c < A.NWv && c == m * A.step)
-                A.Pi[((int64_t)qz * A.Nw + m) * A.Nout * (A.Nb + 1) * 9 + base] = cmul(A.scale, acc[f].value(k));
+              if (c < A.NWv && c == m * A.step) {
+                double2* o = A.Pi + ((int64_t)qz * A.Nw + m) * A.Nout * (A.Nb + 1) * 9 + base;
+                double2 v = cmul(A.scale, acc[f].value(k));
+                if (A.accumulate) {
+                  v.x += o->x;
+                  v.y += o->y;
+                }
+                *o = v;
+              }
             }
           }
         }

@@ -242,6 +242,7 @@ struct PiTcArgs {
   int64_t ntiles, Nout, Nb;
   int NE, Nkz, Nqz, h, Nw, shift0, NNp, nch;   // nch = K-chunks per kz
   int NWv, step;                                // shift columns c < NWv; column c is frequency c / step if c % step == 0
+  int accumulate;                               // add into Π (later energy sub-ranges) instead of overwriting
   int E0, NEo;                                  // this rank's energies: window [E0, E0 + NEo)
 };
 
@@ -387,9 +388,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
         for (int i = 0; i < kPCols; ++i) {
           const int c = cg * kPCols + i, m = c / A.step;
-          if (c < A.NWv && c == m * A.step)
-            A.Pi[((int64_t)qz * A.Nw + m) * mstride + base] =
-                make_double2(A.scale.x * ar[i] - A.scale.y * ai[i], A.scale.x * ai[i] + A.scale.y * ar[i]);
+          if (c < A.NWv && c == m * A.step) {
+            double2* o = A.Pi + ((int64_t)qz * A.Nw + m) * mstride + base;
+            double2 v = make_double2(A.scale.x * ar[i] - A.scale.y * ai[i], A.scale.x * ai[i] + A.scale.y * ar[i]);
+            if (A.accumulate) {
+              v.x += o->x;
+              v.y += o->y;
+            }
+            *o = v;
+          }
         }
       }
     }
@@ -448,6 +455,7 @@ cudaError_t launch_pi_contract_tc(const PiCArgs& a, const float* Wp, const float
   p.shift0 = a.shift0;
   p.NWv = a.NWv;
   p.step = a.step;
+  p.accumulate = a.accumulate;
   p.NNp = NNp;
   // chunks per kz: energies E < NE - shift0 have in-window terms (R7)
   p.E0 = a.E0;

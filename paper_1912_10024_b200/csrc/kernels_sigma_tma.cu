@@ -451,7 +451,7 @@ __global__ void __launch_bounds__((kSandWarps + 1) * 32) k_sigma_sand(SigmaArgs 
       if (lane < NO) {
         const double2 tot = make_double2((w.x + ax) + bx, (w.y + ay) + by);
         const double2 rr = cmul(A.scale, tot);
-        double* out = reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NEo + e) * A.Nout + pr.a) * NN + x * NO + y);
+        double* out = reinterpret_cast<double*>(A.Sig + (((int64_t)kz * A.NEs + A.Es0 + e) * A.Nout + pr.a) * NN + x * NO + y);
         atomicAdd(out, rr.x);
         atomicAdd(out + 1, rr.y);
       }
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kSandThreads) k_sigma_sand_det(SigmaArgs A) {
               if (y0 + y < NO) cfma(s[y], h, v[k * NO + y]);
           }
         }
-        double2* out = A.Sig + (((int64_t)kz * A.NEo + e0 + e) * A.Nout + ent.x) * NN + x * NO + y0;
+        double2* out = A.Sig + (((int64_t)kz * A.NEs + A.Es0 + e0 + e) * A.Nout + ent.x) * NN + x * NO + y0;
 #pragma unroll
         for (int y = 0; y < kSandY; ++y) {
           if (y0 + y < NO) {

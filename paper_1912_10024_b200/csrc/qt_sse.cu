@@ -68,6 +68,7 @@ struct Layout {
   std::vector<PiGroup> groups;
   int64_t n_interior_items = 0;
   int64_t sig_rows = kRows, ndc = 0, NNp = 0, Epad = 0, NEp = 0, Kp = 0;
+  int64_t sig_ec = 0, pi_ec = 0;   // energies per Σ / Π scratch sub-range (= NEo unless the workspace is small)
   size_t ws_bytes = 0, gt_offset = 0, part_bytes = 0;
   std::vector<HaloPeer> peers;
   size_t send_total = 0, recv_total = 0;
@@ -350,29 +351,42 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
   count_flops(&d, L->npairs, L->flops, g.e_lo, g.e_hi);
 
   // workspace (shared by the Σ coefficient tables + Gt scratch and the Π W scratch; calls are serialized)
-  const size_t coef_per_pair = (size_t)9 * d.Nqz * L->DWp * sizeof(double2);
   L->sig_rows = L->fp32 ? kTcRows : kRows;
-  const size_t gt_per_item = (size_t)d.Nkz * L->NEo * L->sig_rows * ((L->NN + 19) / 20) * 20 *
-                             (L->fp32 ? sizeof(float2) : sizeof(double2));
+  const size_t gt_e = (size_t)d.Nkz * L->sig_rows * ((L->NN + 19) / 20) * 20 *
+                      (L->fp32 ? sizeof(float2) : sizeof(double2));   // Gt scratch per item and energy
   L->NNp = (L->NN + 3) & ~int64_t(3);
   L->Epad = L->NEw + d.shift0 + 80 + 1;
-  const size_t w_per_item = L->fp32 ? (size_t)4 * kTcPiRows * d.Nkz * (((L->NEo * L->NNp + 31) / 32) * 32) * sizeof(float)
-                                    : gt_per_item;
+  // W scratch of one item for ne energies (FP32: split planes with each kz row padded to whole 32-chunks)
+  auto w_item = [&](int64_t ne) -> size_t {
+    return L->fp32 ? (size_t)4 * kTcPiRows * d.Nkz * (((ne * L->NNp + 31) / 32) * 32) * sizeof(float) : gt_e * ne;
+  };
   L->NEp = std::max<int64_t>(32, (L->NEw + 3) & ~int64_t(3));   // TMA boxes (32 wide) must lie inside the tensor
   L->Kp = (L->Dwin + 3 + 31) & ~int64_t(31);                      // delayed coefficient rows, whole 32-chunks
   L->sig_tma = true;   // every Norb <= 12 runs the TMA / mbarrier contraction
   L->ndc = (L->Dwin + 15) / 16;
   const size_t coef_item_t = L->fp32 ? (size_t)d.Nqz * 16 * kTcRows * L->Kp * sizeof(float)
                                      : (size_t)d.Nqz * L->ndc * kRows * kCoefKCP * sizeof(double2);
-  const size_t need_min = std::max(coef_per_pair * kMaxPairs, coef_item_t) + w_per_item + 512;
-  const size_t full = std::max((coef_per_pair * kMaxPairs + coef_item_t + w_per_item) * L->sig_items.size() + 512,
-                               w_per_item * L->pi_items.size());
+  const int64_t n_sig_items = (int64_t)L->sig_items.size(), n_pi_items = (int64_t)L->pi_items.size();
+  const size_t need_min = coef_item_t + std::max(gt_e, w_item(1)) + 512;
+  const size_t full = std::max((coef_item_t + gt_e * L->NEo) * n_sig_items + 512, w_item(L->NEo) * n_pi_items);
   size_t budget = std::max(ws_budget, need_min);
   L->ws_bytes = std::max<size_t>(std::min(budget, full), 256);
+  // Enough parallel work per launch: >= 2 waves of k_pi_contract CTAs (one per item and qz) and of sandwich CTAs
+  // (one per pair and kz). When the workspace cannot hold the scratch of that many items for all energies, the
+  // chunks are split by energy as well (Σ outputs are disjoint per energy; Π sub-ranges accumulate).
+  const int64_t waves = 2 * 148;
+  const int64_t pairs_per_item = L->fp32 ? kTcPiPairs : kMaxPairs;
+  const int64_t min_pi = std::min<int64_t>(std::max<int64_t>(1, n_pi_items), (waves + d.Nqz - 1) / d.Nqz);
+  const int64_t min_sig = std::min<int64_t>(std::max<int64_t>(1, n_sig_items),
+                                            (waves + d.Nkz * pairs_per_item - 1) / (d.Nkz * pairs_per_item));
+  L->pi_ec = L->NEo;
+  while (L->pi_ec > 1 && w_item(L->pi_ec) * min_pi > L->ws_bytes) L->pi_ec = (L->pi_ec + 1) / 2;
+  L->sig_ec = L->NEo;
+  while (L->sig_ec > 1 && (coef_item_t + gt_e * L->sig_ec) * min_sig + 512 > L->ws_bytes) L->sig_ec = (L->sig_ec + 1) / 2;
 
-  // Π chunks inside each group (each chunk's W scratch fits the workspace)
+  // Π chunks inside each group (each chunk's W scratch for pi_ec energies fits the workspace)
   {
-    const int64_t cap = std::max<int64_t>(1, (int64_t)(L->ws_bytes / w_per_item));
+    const int64_t cap = std::max<int64_t>(1, (int64_t)(L->ws_bytes / w_item(L->pi_ec)));
     for (size_t gi = 0; gi < L->groups.size(); ++gi) {
       PiGroup& G = L->groups[gi];
       const int64_t i0 = group_item0[gi], i1 = group_item0[gi + 1];
@@ -381,10 +395,10 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
       G.chunks.push_back(i1);
     }
   }
-  // Σ chunks: per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] + its Gt scratch.
-  // Workspace = [coef | Gt]. A chunk never mixes interior and halo sources.
+  // Σ chunks: per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] + its Gt scratch for sig_ec
+  // energies. Workspace = [coef | Gt]. A chunk never mixes interior and halo sources.
   {
-    const size_t gt_item = L->sig_tma ? gt_per_item : 0;
+    const size_t gt_item = gt_e * L->sig_ec;
     size_t coef_acc = 0, gt_acc = 0, coef_max = 0;
     SigChunk c;
     c.i0 = 0;
@@ -399,11 +413,11 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
       coef_acc = gt_acc = 0;
     };
     for (size_t i = 0; i < L->sig_items.size(); ++i) {
-      const size_t cu = L->sig_tma ? coef_item_t : (size_t)L->sig_items[i].npair * coef_per_pair;
+      const size_t cu = coef_item_t;
       if ((int64_t)i == L->n_interior_items && gt_acc + coef_acc > 0) close((int64_t)i);
       if (gt_acc > 0 && coef_acc + cu + gt_acc + gt_item + 256 > L->ws_bytes) close((int64_t)i);
       coef_acc += cu;
-      gt_acc += gt_item == 0 ? 1 : gt_item;
+      gt_acc += gt_item;
     }
     close((int64_t)L->sig_items.size());
     L->gt_offset = (coef_max + 255) & ~size_t(255);
@@ -696,6 +710,8 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       sa.NE = (int)L.NEw;
       sa.E0 = (int)L.E0;
       sa.NEo = (int)L.NEo;
+      sa.NEs = (int)L.NEo;
+      sa.Es0 = 0;
       sa.Nkz = (int)d.Nkz;
       sa.Nqz = (int)d.Nqz;
       sa.h = (int)L.h;
@@ -711,16 +727,21 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       sa.det_atoms = p->d_det_atoms ? p->d_det_atoms + ch.det_off : nullptr;
       sa.det_pairs = p->d_det_pairs;
       sa.n_det = ch.det_n;
-      if (L.fp32) {
-        QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : L.gtp_elems()), L.NEp,
-                                              reinterpret_cast<const float*>(p->ws), (int)L.Kp, i1 - i0, cs));
-      } else {
-        QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
-      }
-      if (L.det) {
-        QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand_det(sa, cs));
-      } else {
-        QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
+      for (int64_t e0 = 0; e0 < L.NEo; e0 += L.sig_ec) {   // energy sub-ranges of the Gt scratch (usually one)
+        sa.E0 = (int)(L.E0 + e0);
+        sa.NEo = (int)std::min<int64_t>(L.sig_ec, L.NEo - e0);
+        sa.Es0 = (int)e0;
+        if (L.fp32) {
+          QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : L.gtp_elems()), L.NEp,
+                                                reinterpret_cast<const float*>(p->ws), (int)L.Kp, i1 - i0, cs));
+        } else {
+          QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
+        }
+        if (L.det) {
+          QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand_det(sa, cs));
+        } else {
+          QT_LAUNCH(QT_K_SIGMA_SAND, launch_sigma_sand(sa, i1 - i0, cs));
+        }
       }
     }
   }
@@ -758,6 +779,8 @@ qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* G
         const int64_t i0 = G.chunks[c], i1 = G.chunks[c + 1];
         if (i1 <= i0) continue;
         const int64_t pp0 = L.pi_items[i0].pair0;
+        for (int64_t e0 = 0; e0 < L.NEo; e0 += L.pi_ec) {   // energy sub-ranges of the W scratch (usually one)
+        const int64_t ne = std::min<int64_t>(L.pi_ec, L.NEo - e0);
         PiWArgs wa;
         wa.GY = GY;
         wa.dH = (const double2*)dH;
@@ -771,8 +794,8 @@ qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* G
         wa.Nwin = L.Nwin;
         wa.Nb = d.Nb;
         wa.NE = (int)L.NEw;
-        wa.E0 = (int)L.E0;
-        wa.NEo = (int)L.NEo;
+        wa.E0 = (int)(L.E0 + e0);
+        wa.NEo = (int)ne;
         wa.Nkz = (int)d.Nkz;
         wa.Norb = (int)d.Norb;
         wa.NN = (int)L.NN;
@@ -796,8 +819,9 @@ qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* G
         ca.Nout = nga;
         ca.Nb = d.Nb;
         ca.NE = (int)L.NEw;
-        ca.E0 = (int)L.E0;
-        ca.NEo = (int)L.NEo;
+        ca.E0 = (int)(L.E0 + e0);
+        ca.NEo = (int)ne;
+        ca.accumulate = e0 > 0 ? 1 : 0;
         ca.Nkz = (int)d.Nkz;
         ca.Nqz = (int)d.Nqz;
         ca.h = (int)L.h;
@@ -812,6 +836,7 @@ qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* G
                                                             (int)L.NNp, i1 - i0, cs));
         } else {
           QT_LAUNCH(QT_K_PI_CONTRACT, launch_pi_contract(ca, i1 - i0, cs));
+        }
         }
       }
       PiSelfArgs sa;
