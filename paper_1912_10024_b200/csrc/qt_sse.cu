@@ -533,6 +533,8 @@ struct qt_sse_plan_s {
   // host-execute staging
   void* h_dev = nullptr;
   size_t h_dev_bytes = 0;
+  cudaStream_t xstream = nullptr;   // copy-back stream of qt_sse_execute_host
+  cudaEvent_t ev_out[4] = {nullptr, nullptr, nullptr, nullptr};   // Σ^<, Σ^>, Π^<, Π^> complete
   // communication
   void* comm = nullptr;         // all ranks
   void* comm_e = nullptr;       // the TE ranks of this atom slab (Π reduction)
@@ -642,7 +644,8 @@ qt_status relayout_sigma(qt_sse_plan_s* p, const void* GL, const void* GG, int64
 // Σ^X (Eq. 3) over the Σ chunks; with `halo` set the stream waits for it (and re-lays-out the halo part of
 // G) before the first chunk that reads halo data.
 qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void* GG, const void* DL, const void* DG,
-                    double sre, double sim, void* SL, void* SG, cudaStream_t cs, cudaEvent_t halo, bool* halo_done) {
+                    double sre, double sim, void* SL, void* SG, cudaStream_t cs, cudaEvent_t halo, bool* halo_done,
+                    cudaEvent_t* done_x = nullptr) {
   const Layout& L = p->L;
   const qt_sse_desc& d = L.d;
   const size_t sig_bytes = (size_t)d.Nkz * L.NEo * L.Nout * L.NN * sizeof(double2);
@@ -744,6 +747,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
         }
       }
     }
+    if (done_x) QT_CUDA(cudaEventRecord(done_x[X], cs));   // Σ^X complete (qt_sse_execute_host copies it back)
   }
   return QT_OK;
 }
@@ -752,7 +756,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
 // communicator) an ncclReduce of the group's partial sums to its owner on the communication stream, while
 // the compute stream continues with the next group (two partial buffers).
 qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* GG, double sre, double sim, void* PL,
-                 void* PG, cudaStream_t cs) {
+                 void* PG, cudaStream_t cs, cudaEvent_t* done_x = nullptr) {
   const Layout& L = p->L;
   const qt_sse_desc& d = L.d;
   int nb = 0;   // partial buffer toggle
@@ -859,6 +863,7 @@ qt_status run_pi(qt_sse_plan_s* p, const void* dH, const void* GL, const void* G
         p->red_pending[buf] = true;
       }
     }
+    if (done_x && !L.reduce) QT_CUDA(cudaEventRecord(done_x[X], cs));   // Π^X complete (no pending reduction)
   }
   for (int b = 0; b < 2; ++b)
     if (p->red_pending[b]) {
@@ -1037,7 +1042,11 @@ extern "C" void qt_sse_destroy(qt_sse_plan_t p) {
   cudaFree(p->recvbuf);
   nccl_comm_destroy(p->comm_e);
   nccl_comm_destroy(p->comm);
+  if (p->xstream) cudaStreamSynchronize(p->xstream);
   cudaFree(p->h_dev);
+  if (p->xstream) cudaStreamDestroy(p->xstream);
+  for (cudaEvent_t e : p->ev_out)
+    if (e) cudaEventDestroy(e);
   cudaEvent_t evs[] = {p->ev_in, p->ev_halo, p->ev_part[0], p->ev_part[1], p->ev_red[0], p->ev_red[1], p->ev_done};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
@@ -1146,9 +1155,19 @@ extern "C" qt_status qt_sse_pi(qt_sse_plan_t p, const void* dH, const void* GL, 
   return call_end(p, cs);
 }
 
+static qt_status sigma_pi_impl(qt_sse_plan_t p, const void* dH, void* GL, void* GG, void* DL, void* DG, double ssre,
+                               double ssim, double psre, double psim, void* SL, void* SG, void* PL, void* PG, void* stream,
+                               cudaEvent_t* sig_done, cudaEvent_t* pi_done);
+
 extern "C" qt_status qt_sse_sigma_pi(qt_sse_plan_t p, const void* dH, void* GL, void* GG, void* DL, void* DG,
                                      double ssre, double ssim, double psre, double psim, void* SL, void* SG, void* PL,
                                      void* PG, void* stream) {
+  return sigma_pi_impl(p, dH, GL, GG, DL, DG, ssre, ssim, psre, psim, SL, SG, PL, PG, stream, nullptr, nullptr);
+}
+
+static qt_status sigma_pi_impl(qt_sse_plan_t p, const void* dH, void* GL, void* GG, void* DL, void* DG, double ssre,
+                               double ssim, double psre, double psim, void* SL, void* SG, void* PL, void* PG, void* stream,
+                               cudaEvent_t* sig_done, cudaEvent_t* pi_done) {
   if (!p) return QT_ERR_INVALID_ARG;
   QT_TRY(check_ptrs({dH, GL, GG, DL, DG}, {SL, SG, PL, PG}));
   cudaStream_t cs = (cudaStream_t)stream;
@@ -1168,12 +1187,12 @@ extern "C" qt_status qt_sse_sigma_pi(qt_sse_plan_t p, const void* dH, void* GL, 
   } else {
     QT_TRY(relayout_sigma(p, GL, GG, 0, L.Nwin, cs));
   }
-  QT_TRY(run_sigma(p, dH, GL, GG, DL, DG, ssre, ssim, SL, SG, cs, halo, &halo_done));
+  QT_TRY(run_sigma(p, dH, GL, GG, DL, DG, ssre, ssim, SL, SG, cs, halo, &halo_done, sig_done));
   if (!halo_done) {   // no Σ chunk read the halo (e.g. no pairs): Π still needs it
     QT_CUDA(cudaStreamWaitEvent(cs, halo, 0));
     QT_TRY(relayout_sigma(p, GL, GG, 0, L.Nwin, cs));
   }
-  QT_TRY(run_pi(p, dH, GL, GG, psre, psim, PL, PG, cs));
+  QT_TRY(run_pi(p, dH, GL, GG, psre, psim, PL, PG, cs, pi_done));
   return call_end(p, cs);
 }
 
@@ -1206,12 +1225,30 @@ extern "C" qt_status qt_sse_execute_host(qt_sse_plan_t p, const void* dH, const 
   QT_CUDA(cudaMemcpyAsync(dGG, GG, b_G, cudaMemcpyHostToDevice, cs));
   QT_CUDA(cudaMemcpyAsync(dDL, DL, b_D, cudaMemcpyHostToDevice, cs));
   QT_CUDA(cudaMemcpyAsync(dDG, DG, b_D, cudaMemcpyHostToDevice, cs));
-  QT_TRY(qt_sse_sigma_pi(p, ddH, dGL, dGG, dDL, dDG, ssre, ssim, psre, psim, dSL, dSG, dPL, dPG, stream));
-  QT_CUDA(cudaMemcpyAsync(SL, dSL, b_S, cudaMemcpyDeviceToHost, cs));
-  QT_CUDA(cudaMemcpyAsync(SG, dSG, b_S, cudaMemcpyDeviceToHost, cs));
-  QT_CUDA(cudaMemcpyAsync(PL, dPL, b_P, cudaMemcpyDeviceToHost, cs));
+  // Σ^<, Σ^> and (without a pending Π reduction) Π^< are copied back on a second stream as soon as each is complete,
+  // overlapped with the remaining compute; Π^> (and reduced Π) after the call
+  if (!p->xstream) {
+    QT_CUDA(cudaStreamCreateWithFlags(&p->xstream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : p->ev_out) QT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t* sig_done = p->ev_out;
+  cudaEvent_t* pi_done = p->ev_out + 2;
+  QT_TRY(sigma_pi_impl(p, ddH, dGL, dGG, dDL, dDG, ssre, ssim, psre, psim, dSL, dSG, dPL, dPG, stream, sig_done, pi_done));
+  void* hS[2] = {SL, SG};
+  const char* dS[2] = {dSL, dSG};
+  for (int x = 0; x < 2; ++x) {
+    QT_CUDA(cudaStreamWaitEvent(p->xstream, sig_done[x], 0));
+    QT_CUDA(cudaMemcpyAsync(hS[x], dS[x], b_S, cudaMemcpyDeviceToHost, p->xstream));
+  }
+  if (!L.reduce) {
+    QT_CUDA(cudaStreamWaitEvent(p->xstream, pi_done[0], 0));
+    QT_CUDA(cudaMemcpyAsync(PL, dPL, b_P, cudaMemcpyDeviceToHost, p->xstream));
+  } else {
+    QT_CUDA(cudaMemcpyAsync(PL, dPL, b_P, cudaMemcpyDeviceToHost, cs));
+  }
   QT_CUDA(cudaMemcpyAsync(PG, dPG, b_P, cudaMemcpyDeviceToHost, cs));
   QT_CUDA(cudaStreamSynchronize(cs));
+  QT_CUDA(cudaStreamSynchronize(p->xstream));
   QT_TRY(nccl_check(p));
   return QT_OK;
 }
