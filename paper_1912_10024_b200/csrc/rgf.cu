@@ -243,41 +243,53 @@ qt_status solve_group(qt_rgf_plan_s* q, const Grp& g, const double2* Ad, const d
   double2* T[7];
   for (int k = 0; k < 7; ++k) T[k] = q->tmp + (k * P + g.p0) * blk;   // the group's slice of each temporary
   const int n_i = (int)bs;
-  // ---------------- forward pass: left-connected g^R_n (into GR), g^<_n (GL), g^>_n (GG)
-  for (int64_t n = 0; n < nb; ++n) {
-    double2* M = T[0];
-    RG_TRY(copy(q, g, M, blk, Ad + n * blk, sD));
+  // ---------------- forward pass: left-connected g^R_n (into GR), g^<_n (GL), g^>_n (GG).
+  // Schedule: the inversion of M_{n+1} (per-point LU + solve on the lanes) runs concurrently with the eight GEMMs
+  // of g^<_n, g^>_n on the group stream; only M_{n+1} itself (two GEMMs) waits for g^R_n.
+  auto build_M = [&](int64_t n) -> qt_status {   // M_n = A_nn − A_{n,n-1} g^R_{n-1} A_{n-1,n} into T[0]
+    RG_TRY(copy(q, g, T[0], blk, Ad + n * blk, sD));
     if (n > 0) {
-      // T1 = A_{n,n-1} g^R_{n-1};  M = A_nn − T1 A_{n-1,n}
       RG_TRY(gemm(q, g, Al + (n - 1) * blk, sO, false, GR + (n - 1) * blk, sD, false, T[1], blk, 1.0, 0.0));
-      RG_TRY(gemm(q, g, T[1], blk, false, Au + (n - 1) * blk, sO, false, M, blk, -1.0, 1.0));
+      RG_TRY(gemm(q, g, T[1], blk, false, Au + (n - 1) * blk, sO, false, T[0], blk, -1.0, 1.0));
     }
-    // g^R_n = M^{-1}: per point, LU of M_p (in place) and a solve against the identity written into block n of GR,
-    // fanned out over the group's lanes
-    {
-      const int64_t tot = np * blk;
-      k_set_identity<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(GR + n * blk, sD, n_i, np);
-      RG_TRY(cu(cudaGetLastError()));
-      qt::count_launches(1);
-      cudaEvent_t fork = g.l0 == 0 ? q->ev_fork : q->ev_gdone[1];   // any free event of this group
-      RG_TRY(cu(cudaEventRecord(fork, st)));
-      for (int l = g.l0; l < g.l0 + g.nl; ++l) RG_TRY(cu(cudaStreamWaitEvent(q->ls[l], fork, 0)));
-      for (int64_t p = 0; p < np; ++p) {
-        const int l = g.l0 + (int)(p % g.nl);
-        cuDoubleComplex* Mp = reinterpret_cast<cuDoubleComplex*>(M + p * blk);
-        int* piv = q->piv + (g.p0 + p) * bs;
-        if (cusolverDnZgetrf(q->sh[l], n_i, n_i, Mp, n_i, reinterpret_cast<cuDoubleComplex*>(q->lwork) + (size_t)l * q->lwork_elems,
-                             piv, q->info + n * P + g.p0 + p) != CUSOLVER_STATUS_SUCCESS)
-          return QT_ERR_CUDA;
-        if (cusolverDnZgetrs(q->sh[l], CUBLAS_OP_N, n_i, n_i, Mp, n_i, piv,
-                             reinterpret_cast<cuDoubleComplex*>(GR + p * sD + n * blk), n_i,
-                             q->info + nb * P + g.p0 + p) != CUSOLVER_STATUS_SUCCESS)
-          return QT_ERR_CUDA;
-      }
-      for (int l = g.l0; l < g.l0 + g.nl; ++l) {
-        RG_TRY(cu(cudaEventRecord(q->ev_join[l], q->ls[l])));
-        RG_TRY(cu(cudaStreamWaitEvent(st, q->ev_join[l], 0)));
-      }
+    return QT_OK;
+  };
+  auto fork_inverse = [&](int64_t n) -> qt_status {   // g^R_n = M_n^{-1} on the lanes (identity written first)
+    const int64_t tot = np * blk;
+    k_set_identity<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(GR + n * blk, sD, n_i, np);
+    RG_TRY(cu(cudaGetLastError()));
+    qt::count_launches(1);
+    cudaEvent_t fork = g.l0 == 0 ? q->ev_fork : q->ev_gdone[1];
+    RG_TRY(cu(cudaEventRecord(fork, st)));
+    for (int l = g.l0; l < g.l0 + g.nl; ++l) RG_TRY(cu(cudaStreamWaitEvent(q->ls[l], fork, 0)));
+    for (int64_t p = 0; p < np; ++p) {
+      const int l = g.l0 + (int)(p % g.nl);
+      cuDoubleComplex* Mp = reinterpret_cast<cuDoubleComplex*>(T[0] + p * blk);
+      int* piv = q->piv + (g.p0 + p) * bs;
+      if (cusolverDnZgetrf(q->sh[l], n_i, n_i, Mp, n_i, reinterpret_cast<cuDoubleComplex*>(q->lwork) + (size_t)l * q->lwork_elems,
+                           piv, q->info + n * P + g.p0 + p) != CUSOLVER_STATUS_SUCCESS)
+        return QT_ERR_CUDA;
+      if (cusolverDnZgetrs(q->sh[l], CUBLAS_OP_N, n_i, n_i, Mp, n_i, piv,
+                           reinterpret_cast<cuDoubleComplex*>(GR + p * sD + n * blk), n_i,
+                           q->info + nb * P + g.p0 + p) != CUSOLVER_STATUS_SUCCESS)
+        return QT_ERR_CUDA;
+    }
+    for (int l = g.l0; l < g.l0 + g.nl; ++l) RG_TRY(cu(cudaEventRecord(q->ev_join[l], q->ls[l])));
+    return QT_OK;
+  };
+  auto join_inverse = [&]() -> qt_status {
+    for (int l = g.l0; l < g.l0 + g.nl; ++l) RG_TRY(cu(cudaStreamWaitEvent(st, q->ev_join[l], 0)));
+    return QT_OK;
+  };
+  RG_TRY(build_M(0));
+  RG_TRY(fork_inverse(0));
+  RG_TRY(join_inverse());
+  for (int64_t n = 0; n < nb; ++n) {
+    // M_{n+1} needs g^R_n (joined); its inversion overlaps the lesser/greater GEMMs of block n below. T[0] (M)
+    // is free again: the lanes finished with M_n at the join.
+    if (n + 1 < nb) {
+      RG_TRY(build_M(n + 1));
+      RG_TRY(fork_inverse(n + 1));
     }
     const double2* S[2] = {Sl, Sg};
     double2* G[2] = {GL, GG};
@@ -293,6 +305,7 @@ qt_status solve_group(qt_rgf_plan_s* q, const Grp& g, const double2* Ad, const d
       RG_TRY(gemm(q, g, GR + n * blk, sD, false, Sx, blk, false, T[3], blk, 1.0, 0.0));
       RG_TRY(gemm(q, g, T[3], blk, false, GR + n * blk, sD, true, G[x] + n * blk, sD, 1.0, 0.0));
     }
+    if (n + 1 < nb) RG_TRY(join_inverse());
   }
   // ---------------- backward pass: G_{nb-1} = g_{nb-1}; block n <- block n+1
   const dim3 tb(32, 8), tg((unsigned)((bs + 31) / 32), (unsigned)((bs + 31) / 32), (unsigned)np);
