@@ -92,6 +92,9 @@ constexpr int kEB = 4;
 
 cudaError_t launch_sigma_coef_tiled(const CoefArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
+// energy-pair form of the Σ contraction for items of >= 4 pairs (kernels_sigma_pair.cu)
+bool sigma_pair_supported(int Norb);
+cudaError_t launch_sigma_pair(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_sand(const SigmaArgs& a, int64_t nitems, cudaStream_t st);
 cudaError_t launch_sigma_sand_det(const SigmaArgs& a, cudaStream_t st);   // QT_FLAG_DETERMINISTIC
 // FP32 mixed-precision Σ contraction (tcgen05 kind::tf32; kernels_sigma_tc.cu). Coefficient planes

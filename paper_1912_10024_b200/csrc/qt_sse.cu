@@ -15,6 +15,10 @@
 
 #include "kernels_decl.cuh"
 
+#ifndef QT_SIG_PAIR
+#define QT_SIG_PAIR 1
+#endif
+
 using namespace qt;
 
 static std::atomic<uint64_t> g_launches{0};
@@ -44,6 +48,7 @@ struct PiGroup {            // Π output group: atoms [lo, hi) of the owned slab
 struct SigChunk {
   int64_t i0 = 0, i1 = 0;
   int64_t det_off = 0, det_n = 0;   // QT_FLAG_DETERMINISTIC: the chunk's destination-atom entries
+  int64_t nfull = 0;                 // leading items of >= 4 pairs (k_sigma_pair in pair mode)
   bool coef_halo = false;   // the coefficient tables read D of halo atoms
   bool g_halo = false;      // the contraction reads G entries of the halo
 };
@@ -54,6 +59,7 @@ struct Layout {
   int64_t NN = 0, h = 0, Dmax = 0, Dwin = 0, DWp = 0, NWv = 0, NWP = 0;
   int64_t Nwin = 0, Nout = 0, NEw = 0, NEo = 0, E0 = 0;
   bool fp32 = false, sig_tma = true, reduce = false;
+  bool sig_pair_mode = false;   // items of >= 4 pairs on the energy-pair contraction (k_sigma_pair)
   std::vector<int32_t> nbr_win;
   std::vector<SigItem> sig_items;
   std::vector<SigPair> sig_pairs;
@@ -300,6 +306,29 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
   L->n_interior_items = (int64_t)L->sig_items.size();
   for (int64_t b = g.w_lo; b < g.w_hi; ++b)
     if (b < g.a_lo || b >= g.a_hi) add_source(b);
+  // Within the interior and the halo sources, items of >= 4 pairs first (the energy-pair contraction kernel takes
+  // them; smaller items keep k_sigma's multi-energy tiles), then the pair list rebuilt in item order so every
+  // chunk's pairs stay contiguous.
+  L->sig_pair_mode = !L->fp32 && sigma_pair_supported((int)d.Norb) && QT_SIG_PAIR;
+  if (L->sig_pair_mode) {
+    auto full_first = [](const SigItem& x) { return x.npair >= 4; };
+    std::stable_partition(L->sig_items.begin(), L->sig_items.begin() + L->n_interior_items, full_first);
+    std::stable_partition(L->sig_items.begin() + L->n_interior_items, L->sig_items.end(), full_first);
+    std::vector<SigPair> pairs;
+    std::vector<int32_t> pair_item;
+    pairs.reserve(L->sig_pairs.size());
+    for (size_t i = 0; i < L->sig_items.size(); ++i) {
+      SigItem& it = L->sig_items[i];
+      const int32_t p0 = (int32_t)pairs.size();
+      for (int t = 0; t < it.npair; ++t) {
+        pairs.push_back(L->sig_pairs[it.pair0 + t]);
+        pair_item.push_back((int32_t)i);
+      }
+      it.pair0 = p0;
+    }
+    L->sig_pairs.swap(pairs);
+    L->sig_pair_item.swap(pair_item);
+  }
 
   // Π groups: one per output owner (sub-slabs of the owned atoms when the partial sums are reduced)
   if (L->reduce) {
@@ -404,6 +433,9 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
     c.i0 = 0;
     auto close = [&](int64_t i) {
       c.i1 = i;
+      c.nfull = 0;
+      if (L->sig_pair_mode)
+        while (c.i0 + c.nfull < c.i1 && L->sig_items[c.i0 + c.nfull].npair >= 4) ++c.nfull;
       const bool halo_src = c.i0 >= L->n_interior_items;
       c.coef_halo = halo_src && g.Ta > 1;
       c.g_halo = halo_src || g.TE > 1;
@@ -737,6 +769,15 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
         if (L.fp32) {
           QT_LAUNCH(QT_K_SIGMA, launch_sigma_tc(sa, p->ws_gtp + (X == 0 ? 0 : L.gtp_elems()), L.NEp,
                                                 reinterpret_cast<const float*>(p->ws), (int)L.Kp, i1 - i0, cs));
+        } else if (L.sig_pair_mode) {
+          // items [i0, i0 + nfull): energy-pair tiles; the rest: k_sigma (Gt scratch offset by nfull items)
+          if (ch.nfull > 0) QT_LAUNCH(QT_K_SIGMA, launch_sigma_pair(sa, ch.nfull, cs));
+          if (i1 - i0 > ch.nfull) {
+            SigmaArgs sb = sa;
+            sb.items = sa.items + ch.nfull;
+            sb.Gt = sa.Gt + (int64_t)ch.nfull * d.Nkz * sa.NEo * sa.rows * sa.gt_ld;
+            QT_LAUNCH(QT_K_SIGMA, launch_sigma(sb, i1 - i0 - ch.nfull, cs));
+          }
         } else {
           QT_LAUNCH(QT_K_SIGMA, launch_sigma(sa, i1 - i0, cs));
         }
