@@ -775,6 +775,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
           if (i1 - i0 > ch.nfull) {
             SigmaArgs sb = sa;
             sb.items = sa.items + ch.nfull;
+            sb.coef = sa.coef + (int64_t)ch.nfull * d.Nqz * L.ndc * kRows * kCoefKCP;   // tiles per chunk item
             sb.Gt = sa.Gt + (int64_t)ch.nfull * d.Nkz * sa.NEo * sa.rows * sa.gt_ld;
             QT_LAUNCH(QT_K_SIGMA, launch_sigma(sb, i1 - i0 - ch.nfull, cs));
           }
