@@ -31,7 +31,10 @@ struct SigPairCfg {
   static constexpr int KC = 16;
   static constexpr int ROWS = KC + 1;                 // G rows per stage: energy E + 1 reads one row further
   static constexpr int KCP = kCoefKCP;
-  static constexpr int STAGES = 4;
+#ifndef QT_PAIR_STAGES
+#define QT_PAIR_STAGES 4
+#endif
+  static constexpr int STAGES = QT_PAIR_STAGES;
   static constexpr int G_STAGE = (ROWS * NPSG + 7) & ~7;            // complex
   static constexpr int S_STAGE = ((ROWS * NPSS + 1) / 2 + 7) & ~7;  // complex units of the double plane
   static constexpr int C_STAGE = kRows * KCP;
