@@ -284,6 +284,8 @@ def main():
     ap.add_argument("--fill-halo", action="store_true",
                     help="generate the whole input window (halo included) in place instead of the owned block + NaN "
                          "halo (no owned-block temporaries: for cfg5-sized windows; the exchange rewrites the same values)")
+    ap.add_argument("--inputs", default="random", choices=["random", "physical"],
+                    help="value envelope of the synthetic inputs (include/qt_gen.h); the cost does not depend on it")
     ap.add_argument("--workload", default="sse", choices=["sse", "rgf"],
                     help="rgf = the GF-phase RGF solver (SURVEY §8(f) NEXT(4)); reported separately, 1 GPU")
     args = ap.parse_args()
@@ -302,6 +304,7 @@ def main():
 
     import qtgen
     p = qtgen.problem(args.config)
+    gmode = qtgen.PHYSICAL if args.inputs == "physical" else qtgen.RANDOM
 
     if args.impl == "reference":
         return run_reference(args, p, rank, world, out_stream)
@@ -346,10 +349,10 @@ def main():
     # each rank generates only its OWNED block; the halo region is left as garbage (NaN) for the library's
     # exchange to fill inside every timed step
     if args.fill_halo:
-        qtgen.dev_G(p, qtgen.ID_GL, G_less, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
-        qtgen.dev_G(p, qtgen.ID_GG, G_gtr, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
-        qtgen.dev_D(p, qtgen.ID_DL, D_less, nbr_dev, a_lo=w_lo, a_hi=w_hi)
-        qtgen.dev_D(p, qtgen.ID_DG, D_gtr, nbr_dev, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_G(p, qtgen.ID_GL, G_less, gmode, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_G(p, qtgen.ID_GG, G_gtr, gmode, e_lo=ew_lo, e_hi=ew_hi, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_D(p, qtgen.ID_DL, D_less, nbr_dev, gmode, a_lo=w_lo, a_hi=w_hi)
+        qtgen.dev_D(p, qtgen.ID_DG, D_gtr, nbr_dev, gmode, a_lo=w_lo, a_hi=w_hi)
     else:
         G_less.fill_(float("nan"))
         G_gtr.fill_(float("nan"))
@@ -357,18 +360,18 @@ def main():
         D_gtr.fill_(float("nan"))
         for t, tid in ((G_less, qtgen.ID_GL), (G_gtr, qtgen.ID_GG)):
             own = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
-            qtgen.dev_G(p, tid, own, e_lo=e_lo, e_hi=e_hi, a_lo=a_lo, a_hi=a_hi)
+            qtgen.dev_G(p, tid, own, gmode, e_lo=e_lo, e_hi=e_hi, a_lo=a_lo, a_hi=a_hi)
             t[:, e_lo - ew_lo:e_hi - ew_lo, a_lo - w_lo:a_hi - w_lo] = own
             del own
         for t, tid in ((D_less, qtgen.ID_DL), (D_gtr, qtgen.ID_DG)):
             own = torch.empty((p.Nqz, p.Nw, nout, p.Nb + 1, 3, 3), dtype=c128, device=dev)
-            qtgen.dev_D(p, tid, own, nbr_dev, a_lo=a_lo, a_hi=a_hi)
+            qtgen.dev_D(p, tid, own, nbr_dev, gmode, a_lo=a_lo, a_hi=a_hi)
             t[:, :, a_lo - w_lo:a_hi - w_lo] = own
             del own
     torch.cuda.empty_cache()
     if world == 1:
         assert not torch.isnan(G_less).any()
-    qtgen.dev_dH(p, dH_full, nbr_dev)
+    qtgen.dev_dH(p, dH_full, nbr_dev, gmode)
     dH = dH_full[w_lo:w_hi].contiguous()
     del dH_full
     S_less = torch.empty((p.Nkz, e_hi - e_lo, nout, p.Norb, p.Norb), dtype=c128, device=dev)
@@ -504,7 +507,7 @@ def main():
     # ---- CPU oracle baseline (rank 0, N=1 only): stratified bounded sample of the same workload
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        host = hin if hin is not None else qtgen.host_inputs(p)
+        host = hin if hin is not None else qtgen.host_inputs(p, gmode)
         hnp = {k: (v.numpy() if hasattr(v, "numpy") else v) for k, v in host.items()}
         os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
         fs, dt, ns, npi, t_full, strata = stratified_oracle(p, hnp, args.cpu_seconds)
@@ -523,7 +526,7 @@ def main():
                "scaling": "strong", "vs_baseline": None,
                "dtype": "f64" if not fp32 else "f32-mixed (Σ and Π contractions tf32x3 on tcgen05, FP32 sandwiches; "
                                                "FP64 inputs/outputs, FP64 re-accumulation)",
-               "data": "synthetic",
+               "data": "synthetic" if gmode == qtgen.RANDOM else "synthetic (PHYSICAL envelope, include/qt_gen.h)",
                "config": {"workload": f"{args.config}: Si FinFET slice Na={p.Na}, Nb={p.Nb}, Norb={p.Norb}, "
                                       f"NE={p.NE}, Nω={p.Nw}, Nkz=Nqz={p.Nkz}",
                           "flops_per_step": flops_step,

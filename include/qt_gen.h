@@ -18,7 +18,22 @@
  * Complex element with flat index f takes re = x(2f), im = x(2f+1).
  *
  * Modes (QTGEN_*): RANDOM, INTEGER, DELTA (D only: neighbour slots = I3/2 at
- * (qz = floor(Nqz/2), m = delta_m), everything else 0; pin P3).
+ * (qz = floor(Nqz/2), m = delta_m), everything else 0; pin P3), PHYSICAL (the
+ * wide-dynamic-range envelope of SURVEY.md §8(d) "Modes", for the FP32 mode's
+ * accuracy):
+ *   G<(E) = i·f(E)·A,  G>(E) = -i·g(E)·A,  A = X X† / Norb  (Hermitian PSD),
+ *   X the block's random draws of tensor ID_GL (X_rk = complex draw at flat
+ *   index r·Norb + k; the same X for G< and G>, so both share one A),
+ *   f(E) = 1 / (1 + 2^t), g(E) = 1 / (1 + 2^-t), t = floor(40·e / NE) - 20
+ *   (a Fermi-like ladder over the energy grid: f spans 1 .. 2^-19, g = 1 - f
+ *   up to rounding, computed without cancellation);
+ *   ∇H: random draws scaled by the neighbour shell of the slot the draw is
+ *   owned by: slots 0-3 ×1, 4-15 ×0.3, 16-27 ×0.1, 28+ ×0.03 (diamond shells
+ *   of 4 / 12 / 12 / 6 neighbours, qtgen/geometry.py);
+ *   D: as RANDOM.
+ * Every PHYSICAL value is formed in a fixed order of IEEE-rounded +, ×, ÷
+ * (no contraction; ldexp exact), so host and device agree bit for bit. A_cr is
+ * conj(A_rc) exactly, so G stays exactly anti-Hermitian.
  *
  * Layouts (row-major, complex128 interleaved re,im):
  *   G  [Nkz][NE][Na][Norb][Norb]
@@ -35,7 +50,7 @@
 extern "C" {
 #endif
 
-enum { QTGEN_RANDOM = 0, QTGEN_INTEGER = 1, QTGEN_DELTA = 2, QTGEN_ZERO = 3 };
+enum { QTGEN_RANDOM = 0, QTGEN_INTEGER = 1, QTGEN_DELTA = 2, QTGEN_ZERO = 3, QTGEN_PHYSICAL = 4 };
 enum { QTGEN_ID_DH = 1, QTGEN_ID_GL = 2, QTGEN_ID_GG = 3, QTGEN_ID_DL = 4, QTGEN_ID_DG = 5 };
 
 /* ---- host (qtgen/libqtgen_host.so, OpenMP) ---- */

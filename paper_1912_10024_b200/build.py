@@ -79,7 +79,7 @@ TARGETS = {
         srcs=[ROOT / "qtgen" / "gen_host.c"],
         deps=[ROOT / "include" / "qt_gen.h"],
         cmd=lambda srcs, out: ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
-                               f"-I{ROOT / 'include'}", *map(str, srcs), "-o", str(out)],
+                               f"-I{ROOT / 'include'}", *map(str, srcs), "-o", str(out), "-lm"],
     ),
     "oracle": dict(
         out=ROOT / "oracle" / "liboracle.so",

@@ -15,7 +15,7 @@ from .geometry import CONFIGS, neighbor_table, random_graph, reverse_slots  # no
 
 _HERE = Path(__file__).resolve().parent
 SEED = 191210024
-RANDOM, INTEGER, DELTA, ZERO = 0, 1, 2, 3
+RANDOM, INTEGER, DELTA, ZERO, PHYSICAL = 0, 1, 2, 3, 4
 ID_DH, ID_GL, ID_GG, ID_DL, ID_DG = 1, 2, 3, 4, 5
 
 _i64, _u64, _int, _vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p

@@ -21,6 +21,15 @@ __device__ __forceinline__ int rev_slot(const int32_t* nbr, int64_t Nb, int64_t 
   return -1;
 }
 
+// PHYSICAL envelope (see qt_gen.h); same expressions as gen_host.c, every operation explicitly rounded
+__device__ __forceinline__ double occupation(int id, int64_t e, int64_t NE) {
+  const int t = (int)((40 * e) / NE) - 20;
+  return __ddiv_rn(1.0, __dadd_rn(1.0, ldexp(1.0, id == QTGEN_ID_GL ? t : -t)));
+}
+__device__ __forceinline__ double shell_scale(int64_t slot) {
+  return slot < 4 ? 1.0 : slot < 16 ? 0.3 : slot < 28 ? 0.1 : 0.03;
+}
+
 __global__ void k_gen_G(uint64_t seed, int id, int mode, int64_t NE, int64_t Na, int64_t Norb,
                         int64_t e_lo, int64_t ne, int64_t a_lo, int64_t na, int64_t total, double2* out) {
   const int64_t nn = Norb * Norb;
@@ -30,6 +39,22 @@ __global__ void k_gen_G(uint64_t seed, int id, int mode, int64_t NE, int64_t Na,
     if (mode == QTGEN_ZERO) { out[t] = make_double2(0.0, 0.0); continue; }
     int64_t r = rc / Norb, c = rc % Norb;
     uint64_t base = (uint64_t)(((k * NE + e) * Na + a) * nn);
+    if (mode == QTGEN_PHYSICAL) {
+      double are = 0.0, aim = 0.0;
+      for (int64_t kk = 0; kk < Norb; ++kk) {
+        uint64_t fx = base + (uint64_t)(r * Norb + kk), fy = base + (uint64_t)(c * Norb + kk);
+        double xr = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fx), xi = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fx + 1);
+        double yr = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fy), yi = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fy + 1);
+        are = __dadd_rn(are, __dadd_rn(__dmul_rn(xr, yr), __dmul_rn(xi, yi)));
+        aim = __dadd_rn(aim, __dsub_rn(__dmul_rn(xi, yr), __dmul_rn(xr, yi)));
+      }
+      are = __ddiv_rn(are, (double)Norb);
+      aim = __ddiv_rn(aim, (double)Norb);
+      const double occ = occupation(id, e, NE);
+      out[t] = id == QTGEN_ID_GL ? make_double2(-__dmul_rn(occ, aim), __dmul_rn(occ, are))
+                                 : make_double2(__dmul_rn(occ, aim), -__dmul_rn(occ, are));
+      continue;
+    }
     uint64_t f_rc = base + (uint64_t)(r * Norb + c), f_cr = base + (uint64_t)(c * Norb + r);
     double xr_rc = draw(seed, id, mode, 2 * f_rc), xi_rc = draw(seed, id, mode, 2 * f_rc + 1);
     double xr_cr = draw(seed, id, mode, 2 * f_cr), xi_cr = draw(seed, id, mode, 2 * f_cr + 1);
@@ -82,11 +107,13 @@ __global__ void k_gen_dH(uint64_t seed, int id, int mode, int64_t Na, int64_t Nb
     if (mode != QTGEN_ZERO && b >= 0) {
       if (a < b) {
         uint64_t f = (uint64_t)(((a * Nb + s) * 3 + i) * nn) + xy;
-        v.x = draw(seed, id, mode, 2 * f); v.y = draw(seed, id, mode, 2 * f + 1);
+        const double sc = mode == QTGEN_PHYSICAL ? shell_scale(s) : 1.0;
+        v.x = __dmul_rn(sc, draw(seed, id, mode, 2 * f)); v.y = __dmul_rn(sc, draw(seed, id, mode, 2 * f + 1));
       } else {
         int r = rev_slot(nbr, Nb, b, a);
         uint64_t f = (uint64_t)(((b * Nb + r) * 3 + i) * nn) + y * Norb + x;
-        v.x = draw(seed, id, mode, 2 * f); v.y = -draw(seed, id, mode, 2 * f + 1);
+        const double sc = mode == QTGEN_PHYSICAL ? shell_scale(r) : 1.0;
+        v.x = __dmul_rn(sc, draw(seed, id, mode, 2 * f)); v.y = -__dmul_rn(sc, draw(seed, id, mode, 2 * f + 1));
       }
     }
     out[t] = v;

@@ -3,6 +3,7 @@
  * gen_dev.cu implements the same generator on the device; tests check they
  * agree bit-for-bit. Build: gcc -O2 -fopenmp -ffp-contract=off -shared -fPIC. */
 #include "qt_gen.h"
+#include <math.h>
 #include <stddef.h>
 
 static inline uint64_t sm64(uint64_t z) {
@@ -22,6 +23,15 @@ static inline int rev_slot(const int32_t* nbr, int64_t Nb, int64_t b, int64_t a)
   return -1;
 }
 
+/* PHYSICAL envelope (see qt_gen.h): occupation factor of energy e for tensor id (f for G<, g for G>) */
+static inline double occupation(int id, int64_t e, int64_t NE) {
+  const int t = (int)((40 * e) / NE) - 20;
+  return 1.0 / (1.0 + ldexp(1.0, id == QTGEN_ID_GL ? t : -t));
+}
+static inline double shell_scale(int64_t slot) {
+  return slot < 4 ? 1.0 : slot < 16 ? 0.3 : slot < 28 ? 0.1 : 0.03;
+}
+
 void qtgen_host_G(uint64_t seed, int id, int mode, int64_t Nkz, int64_t NE, int64_t Na, int64_t Norb,
                   int64_t e_lo, int64_t e_hi, int64_t a_lo, int64_t a_hi, double* out) {
   const int64_t ne = e_hi - e_lo, na = a_hi - a_lo, nn = Norb * Norb;
@@ -32,6 +42,30 @@ void qtgen_host_G(uint64_t seed, int id, int mode, int64_t Nkz, int64_t NE, int6
     double* o = out + 2 * nn * q;
     if (mode == QTGEN_ZERO) { for (int64_t t = 0; t < 2 * nn; ++t) o[t] = 0.0; continue; }
     uint64_t base = (uint64_t)(((k * NE + e) * Na + a) * nn);
+    if (mode == QTGEN_PHYSICAL) {
+      const double occ = occupation(id, e, NE);
+      for (int64_t r = 0; r < Norb; ++r)
+        for (int64_t c = 0; c < Norb; ++c) {
+          double are = 0.0, aim = 0.0;   /* A_rc = sum_k X_rk conj(X_ck) */
+          for (int64_t kk = 0; kk < Norb; ++kk) {
+            uint64_t fx = base + (uint64_t)(r * Norb + kk), fy = base + (uint64_t)(c * Norb + kk);
+            double xr = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fx), xi = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fx + 1);
+            double yr = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fy), yi = draw(seed, QTGEN_ID_GL, QTGEN_RANDOM, 2 * fy + 1);
+            are = are + (xr * yr + xi * yi);
+            aim = aim + (xi * yr - xr * yi);
+          }
+          are = are / (double)Norb;
+          aim = aim / (double)Norb;
+          if (id == QTGEN_ID_GL) { /* i f A */
+            o[2 * (r * Norb + c)] = -(occ * aim);
+            o[2 * (r * Norb + c) + 1] = occ * are;
+          } else {                 /* -i g A */
+            o[2 * (r * Norb + c)] = occ * aim;
+            o[2 * (r * Norb + c) + 1] = -(occ * are);
+          }
+        }
+      continue;
+    }
     for (int64_t r = 0; r < Norb; ++r)
       for (int64_t c = 0; c < Norb; ++c) {
         uint64_t f_rc = base + (uint64_t)(r * Norb + c), f_cr = base + (uint64_t)(c * Norb + r);
@@ -101,15 +135,20 @@ void qtgen_host_dH(uint64_t seed, int id, int mode, int64_t Na, int64_t Nb, int6
     if (b < 0) continue;
     if (a < b) {
       uint64_t base = (uint64_t)(((a * Nb + s) * 3 + i) * nn);
-      for (int64_t t = 0; t < nn; ++t) { o[2 * t] = draw(seed, id, mode, 2 * (base + t)); o[2 * t + 1] = draw(seed, id, mode, 2 * (base + t) + 1); }
+      const double sc = mode == QTGEN_PHYSICAL ? shell_scale(s) : 1.0;
+      for (int64_t t = 0; t < nn; ++t) {
+        o[2 * t] = sc * draw(seed, id, mode, 2 * (base + t));
+        o[2 * t + 1] = sc * draw(seed, id, mode, 2 * (base + t) + 1);
+      }
     } else { /* dH_{a,b} = (dH_{b,a})^dagger */
       int r = rev_slot(nbr, Nb, b, a);
       uint64_t base = (uint64_t)(((b * Nb + r) * 3 + i) * nn);
+      const double sc = mode == QTGEN_PHYSICAL ? shell_scale(r) : 1.0;
       for (int64_t x = 0; x < Norb; ++x)
         for (int64_t y = 0; y < Norb; ++y) {
           uint64_t f = base + y * Norb + x;
-          o[2 * (x * Norb + y)] = draw(seed, id, mode, 2 * f);
-          o[2 * (x * Norb + y) + 1] = -draw(seed, id, mode, 2 * f + 1);
+          o[2 * (x * Norb + y)] = sc * draw(seed, id, mode, 2 * f);
+          o[2 * (x * Norb + y) + 1] = -(sc * draw(seed, id, mode, 2 * f + 1));
         }
     }
   }

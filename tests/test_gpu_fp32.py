@@ -107,6 +107,36 @@ def test_fp32_unsupported_norb():
         qt.Plan(p, precision=FP32)
 
 
+@pytest.mark.parametrize("cfg", range(len(MICROS)))
+def test_fp32_micro_physical(cfg):
+    """FP32 mode on the wide-dynamic-range PHYSICAL envelope (qt_gen.h): the per-block bar still holds when
+    G≷ magnitudes span 2^20 across the energies a Σ / Π block sums over."""
+    p = micro(**MICROS[cfg])
+    check(p, inputs(p, mode=qtgen.PHYSICAL, seed=650 + cfg))
+
+
+def test_fp32_prof_physical_sampled():
+    """PHYSICAL envelope at the cfg3 per-atom shape (Nb = 34 with ∇H shells 1 / 0.3 / 0.1 / 0.03), FP32 mode:
+    sampled Σ (half at the low- and high-energy ends of the occupation ladder) and Π blocks at 1e-5."""
+    p = qtgen.problem("prof")
+    inp = qtgen.host_inputs(p, qtgen.PHYSICAL)
+    out = _run(p, inp, 1j, -1j)
+    rng = np.random.default_rng(9)
+    n = 64
+    es = np.concatenate([rng.integers(0, 20, n // 4), rng.integers(p.NE - 20, p.NE, n // 4),
+                         rng.integers(0, p.NE, n - n // 2)])
+    sb = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nkz, n), es, rng.integers(0, p.Na, n)], 1)
+    S = (out["S_less"], out["S_gtr"])
+    err_s = rel_fro(np.stack([S[x][k, e, a] for x, k, e, a in sb]), oracle.sigma_blocks(p, inp, sb, 1j), AX)
+    a_s = rng.integers(0, p.Na, n)
+    pb = np.stack([rng.integers(0, 2, n), rng.integers(0, p.Nqz, n), rng.integers(0, p.Nw, n), a_s,
+                   [rng.choice(np.concatenate([[0], 1 + np.nonzero(p.nbr[x] >= 0)[0]])) for x in a_s]], 1)
+    P = (out["P_less"], out["P_gtr"])
+    err_p = rel_fro(np.stack([P[x][q, m, a, s] for x, q, m, a, s in pb]), oracle.pi_blocks(p, inp, pb, -1j), AX)
+    print(f"prof PHYSICAL FP32 mode: max per-block rel. Frobenius error Σ {err_s:.2e}, Π {err_p:.2e}")
+    assert err_s <= TOL_FP32 and err_p <= TOL_FP32, (err_s, err_p)
+
+
 def test_fp32_small_config_sampled():
     p = qtgen.problem("small")
     inp = qtgen.host_inputs(p, qtgen.RANDOM)

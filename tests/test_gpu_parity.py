@@ -50,7 +50,7 @@ def check_full(p, inp, ss=1j, ps=-1j, exact=False, **kw):
 
 
 # ------------------------------------------------------------------ generator: device == host, bit for bit
-@pytest.mark.parametrize("mode", [qtgen.RANDOM, qtgen.INTEGER, qtgen.DELTA])
+@pytest.mark.parametrize("mode", [qtgen.RANDOM, qtgen.INTEGER, qtgen.DELTA, qtgen.PHYSICAL])
 def test_device_generator_matches_host(mode):
     for p in (qtgen.problem("tiny"), micro(**MICROS[2])):
         h = qtgen.host_inputs(p, mode if mode != qtgen.DELTA else qtgen.RANDOM,
@@ -72,6 +72,13 @@ def test_parity_micro(cfg):
     p = micro(**MICROS[cfg])
     check_full(p, inputs(p, seed=300 + cfg))
     check_full(p, inputs(p, mode=qtgen.INTEGER, seed=400 + cfg), ss=1.0, ps=1j, exact=True)
+
+
+@pytest.mark.parametrize("cfg", range(len(MICROS)))
+def test_parity_micro_physical(cfg):
+    """The wide-dynamic-range PHYSICAL envelope (qt_gen.h; G≷ spanning 2^20 in magnitude across energies)."""
+    p = micro(**MICROS[cfg])
+    check_full(p, inputs(p, mode=qtgen.PHYSICAL, seed=350 + cfg))
 
 
 def test_parity_tiny_config():
@@ -295,6 +302,11 @@ def test_small_config_sampled_random():
 
 def test_small_config_sampled_integer():
     _sampled_parity(qtgen.problem("small"), qtgen.INTEGER, 96, 96, exact=True)
+
+
+def test_prof_sampled_physical():
+    """PHYSICAL envelope at the cfg3 per-atom shape (Nb = 34, four ∇H shells, Norb 10, NE 176, Nω 70)."""
+    _sampled_parity(qtgen.problem("prof"), qtgen.PHYSICAL, 64, 64, exact=False)
 
 
 @pytest.mark.slow
