@@ -447,7 +447,10 @@ def main():
     if tf.exists():
         prof_traffic = json.loads(tf.read_text()).get(args.config, {}).get("k_sigma")
     if not fp32:
-        roofline = {"bound": "tensor", "kernel": "k_sigma (Σ D-contraction, DMMA.8x8x4 FP64)",
+        kname = ("k_sigma_pair + k_sigma (Σ D-contraction: energy-pair tiles for items of >= 4 pairs, multi-energy "
+                 "tiles for the rest; DMMA.8x8x4 FP64; both timed as one kind)" if 9 <= p.Norb <= 11
+                 else "k_sigma (Σ D-contraction, DMMA.8x8x4 FP64)")
+        roofline = {"bound": "tensor", "kernel": kname,
                     "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
                     "frac": round(achieved / peak, 4), "traffic": prof_traffic,
                     "flops_basis": "algorithmic: 8 real flops per complex MAC, in-window valid-pair work only",
