@@ -169,6 +169,26 @@ def test_parity_isolated_atoms_and_many_pairs():
     assert (p.nbr >= 0).sum(1).max() > 8
 
 
+@pytest.mark.parametrize("Norb,NE,Nw,shift0,step,Nkz,seed", [(9, 13, 3, 1, 1, 3, 2), (10, 21, 5, 2, 1, 2, 3),
+                                                             (11, 17, 4, 1, 2, 1, 2), (10, 8, 4, 1, 1, 4, 3),
+                                                             (11, 23, 7, 3, 1, 2, 3), (9, 12, 2, 1, 3, 2, 2)])
+def test_parity_energy_pair_tiles(Norb, NE, Nw, shift0, step, Nkz, seed):
+    """k_sigma_pair (FP64, Norb 9-11): source atoms of 5..12 pairs give items of 4..8 pairs on the energy-pair
+    tiles and 1..3-pair remainders on k_sigma in the same chunk (the coefficient / Gt offsets between the two
+    launches); odd and even NE (the last pair's E+1 past the window), shift0 / shift_step > 1, Nkz 1..4; the
+    separate and fused calls, many chunks with energy sub-ranges (workspace_limit = 1), the deterministic
+    neighbour sum; random inputs at 1e-12 and integer inputs bit-exact."""
+    nbr = qtgen.geometry.random_graph(16, 13, 0.6, seed)
+    deg = (nbr >= 0).sum(1)
+    assert (deg >= 4).any() and ((deg % 8 > 0) & (deg % 8 < 4)).any()
+    p = Problem(nbr, Norb, NE, Nw, Nkz, shift0=shift0, shift_step=step, name="pair")
+    check_full(p, inputs(p, seed=900 + Norb))
+    check_full(p, inputs(p, mode=qtgen.INTEGER, seed=910 + Norb), ss=1.0, ps=1j, exact=True, fused=True)
+    check_full(p, inputs(p, seed=920 + Norb), fused=True, workspace_limit=1)
+    check_full(p, inputs(p, mode=qtgen.INTEGER, seed=930 + Norb), ss=1j, ps=1.0, exact=True,
+               flags=qt.QT_FLAG_DETERMINISTIC, workspace_limit=1)
+
+
 @pytest.mark.parametrize("prec", [qt.QT_PREC_FP64, qt.QT_PREC_FP32_MIXED])
 def test_deterministic_flag_bitwise_reproducible(prec):
     """QT_FLAG_DETERMINISTIC: the Σ neighbour sum runs in one fixed order (no floating-point atomics), so two runs
