@@ -108,6 +108,8 @@ typedef struct {
   int32_t Ta, TE, ta, te;   /* rank grid and this rank's coordinates                                    */
   double reduce_bytes;      /* bytes this rank sends in the Π reduction per qt_sse_pi call              */
   double mem_bytes;         /* device bytes per rank: caller tensors (window inputs, outputs) + plan    */
+  double flops_sigma_pair;  /* the part of flops_sigma's D-contraction run by the energy-pair kernel
+                               (k_sigma_pair: FP64, Norb 9..11, items of >= 4 pairs); 0 otherwise      */
 } qt_sse_info;
 
 /* Validates desc + neighbours, builds the work lists, allocates the workspace. With an NCCL unique id and
@@ -178,7 +180,8 @@ uint64_t qt_sse_launch_count(void);
  * returns, per kernel kind (QT_K_*), the summed milliseconds and launch counts since the
  * last reset, then clears them. */
 enum { QT_K_SIGMA_COEF = 0, QT_K_SIGMA = 1, QT_K_PI_W = 2, QT_K_PI_CONTRACT = 3, QT_K_PI_SELF = 4,
-       QT_K_RELAYOUT = 5, QT_K_HALO = 6, QT_K_SIGMA_SAND = 7, QT_K_NKINDS = 8 };
+       QT_K_RELAYOUT = 5, QT_K_HALO = 6, QT_K_SIGMA_SAND = 7, QT_K_SIGMA_PAIR = 8, QT_K_NKINDS = 9 };
+/* QT_K_SIGMA = k_sigma (multi-energy tiles) or k_sigma_tc (FP32 mode); QT_K_SIGMA_PAIR = k_sigma_pair. */
 qt_status qt_sse_timing_enable(qt_sse_plan_t plan, int enable);
 qt_status qt_sse_timing_read(qt_sse_plan_t plan, double ms[QT_K_NKINDS], int64_t launches[QT_K_NKINDS]);
 

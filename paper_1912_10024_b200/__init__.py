@@ -25,7 +25,7 @@ EXPORTED = ["qt_sse_plan", "qt_sse_sigma", "qt_sse_pi", "qt_sse_execute_host", "
             "qt_sse_shard_info", "qt_sse_sigma_pi"]
 EXPORTED_RGF = ["qt_rgf_plan", "qt_rgf_solve", "qt_rgf_check_info", "qt_rgf_count_flops", "qt_rgf_destroy"]
 KERNEL_KINDS = ["k_sigma_coef", "k_sigma", "k_pi_w", "k_pi_contract", "k_pi_self", "k_relayout", "k_halo_pack",
-                "k_sigma_sand"]
+                "k_sigma_sand", "k_sigma_pair"]
 
 
 class Desc(ctypes.Structure):
@@ -44,7 +44,7 @@ class Info(ctypes.Structure):
                 ("e_lo", ctypes.c_int64), ("e_hi", ctypes.c_int64), ("ew_lo", ctypes.c_int64), ("ew_hi", ctypes.c_int64),
                 ("pa_lo", ctypes.c_int64), ("pa_hi", ctypes.c_int64), ("Ta", ctypes.c_int32), ("TE", ctypes.c_int32),
                 ("ta", ctypes.c_int32), ("te", ctypes.c_int32), ("reduce_bytes", ctypes.c_double),
-                ("mem_bytes", ctypes.c_double)]
+                ("mem_bytes", ctypes.c_double), ("flops_sigma_pair", ctypes.c_double)]
 
 
 class RgfDesc(ctypes.Structure):

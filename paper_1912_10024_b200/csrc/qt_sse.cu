@@ -423,6 +423,28 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
       for (int64_t i = i0 + cap; i < i1; i += cap) G.chunks.push_back(i);
       G.chunks.push_back(i1);
     }
+    // Inside each chunk, items of more pairs first (k_pi_contract / sandwich CTAs are issued in item order: the
+    // long CTAs start in the first waves and the short remainder items fill the tail), then the pair list rebuilt
+    // in item order (each chunk's pairs stay one contiguous range).
+    for (const PiGroup& G : L->groups)
+      for (size_t k = 0; k + 1 < G.chunks.size(); ++k)
+        std::stable_sort(L->pi_items.begin() + G.chunks[k], L->pi_items.begin() + G.chunks[k + 1],
+                         [](const PiItem& x, const PiItem& y) { return x.npair > y.npair; });
+    std::vector<PiPair> pairs;
+    std::vector<int32_t> pair_item;
+    pairs.reserve(L->pi_pairs.size());
+    pair_item.reserve(L->pi_pairs.size());
+    for (size_t i = 0; i < L->pi_items.size(); ++i) {
+      PiItem& it = L->pi_items[i];
+      const int32_t p0 = (int32_t)pairs.size();
+      for (int t = 0; t < it.npair; ++t) {
+        pairs.push_back(L->pi_pairs[it.pair0 + t]);
+        pair_item.push_back((int32_t)i);
+      }
+      it.pair0 = p0;
+    }
+    L->pi_pairs.swap(pairs);
+    L->pi_pair_item.swap(pair_item);
   }
   // Σ chunks: per item a tiled coefficient block [q][16-shift chunk][72][kCoefKCP] + its Gt scratch for sig_ec
   // energies. Workspace = [coef | Gt]. A chunk never mixes interior and halo sources.
@@ -771,7 +793,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
                                                 reinterpret_cast<const float*>(p->ws), (int)L.Kp, i1 - i0, cs));
         } else if (L.sig_pair_mode) {
           // items [i0, i0 + nfull): energy-pair tiles; the rest: k_sigma (Gt scratch offset by nfull items)
-          if (ch.nfull > 0) QT_LAUNCH(QT_K_SIGMA, launch_sigma_pair(sa, ch.nfull, cs));
+          if (ch.nfull > 0) QT_LAUNCH(QT_K_SIGMA_PAIR, launch_sigma_pair(sa, ch.nfull, cs));
           if (i1 - i0 > ch.nfull) {
             SigmaArgs sb = sa;
             sb.items = sa.items + ch.nfull;
@@ -1041,6 +1063,11 @@ static void fill_info(const Layout& L, size_t ws_total, qt_sse_info* o) {
   o->te = g.te;
   o->reduce_bytes = L.reduce_bytes;
   o->mem_bytes = footprint(L);
+  int64_t np_pair = 0;
+  if (L.sig_pair_mode)
+    for (const SigItem& it : L.sig_items)
+      if (it.npair >= 4) np_pair += it.npair;
+  o->flops_sigma_pair = L.sig_pairs.empty() ? 0.0 : L.flops[0] * (double)np_pair / (double)L.sig_pairs.size();
 }
 
 extern "C" qt_status qt_sse_shard_info(const qt_sse_desc* desc, const int32_t* nbr, qt_sse_info* o) {
