@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 #ifndef QT_SAND_S
 #define QT_SAND_S 14
 #endif
+#ifndef QT_SAND_PF
+#define QT_SAND_PF 0
+#endif
 constexpr int kSandWarps = QT_SAND_W;   // consumer warps per CTA (energies e ≡ w mod kSandWarps)
 constexpr int kSandSlots = QT_SAND_S;   // Gt ring shared by the warps: kSandSlots - kSandWarps energies prefetched
 
@@ -380,6 +383,8 @@ __global__ void __launch_bounds__((kSandWarps + 1) * 32) k_sigma_sand(SigmaArgs 
         if (e >= kSandSlots) mbar_wait(&empty[slot], ((e / kSandSlots) - 1) & 1);
         mbar_arrive_expect_tx(&full[slot], 9 * Cf::ROWB);
         const C2* src = gsrc + (int64_t)e * A.rows * ld;
+        if (QT_SAND_PF > 0 && e + QT_SAND_PF < A.NEo)   // the pair's 9 rows are contiguous: one L2 prefetch
+          bulk_prefetch_l2(src + (int64_t)QT_SAND_PF * A.rows * ld, 9 * Cf::ROWB);
         for (int r = 0; r < 9; ++r)
           bulk_load(ring + slot * Cf::SLOT + r * NNP, src + r * ld, Cf::ROWB, &full[slot]);
       }
