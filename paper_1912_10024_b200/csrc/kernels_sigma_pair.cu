@@ -9,6 +9,11 @@
 // column quarter); each quarter's columns come from one TMA box of KC + 1 rows x its rc range. Everything
 // else — producer warp, 18 consumer warps, Gauss-3M DMMA, 4-stage mbarrier ring, role tables, k-step trimming
 // to the energy window (R7), Gt scratch layout — is k_sigma's.
+//
+// Items of 1..3 pairs fill only F = ceil(9n/8) = 2..4 of the 9 m-fragments; like k_sigma's multi-energy tiles
+// they take ept = 9/F consecutive energy PAIRS per tile (m-fragment group g = mi / F serves energies E + 2g and
+// E + 2g + 1: shared-memory rows k + 2g + e of one taller TMA box of KC + 2·ept − 1 rows; tiles of the other
+// energy pairs are empty), so every item of a chunk runs here and k_sigma is not launched in pair mode.
 #include "kernels_decl.cuh"
 #include "tma.cuh"
 
@@ -35,11 +40,16 @@ struct SigPairCfg {
 #define QT_PAIR_STAGES 4
 #endif
   static constexpr int STAGES = QT_PAIR_STAGES;
-  static constexpr int G_STAGE = (ROWS * NPSG + 7) & ~7;            // complex
-  static constexpr int S_STAGE = ((ROWS * NPSS + 1) / 2 + 7) & ~7;  // complex units of the double plane
+  static constexpr int EPT_MAX = 4;                  // energy pairs per tile for items of 1 pair (F = 2)
+  static constexpr int ROWS_M = KC + 2 * EPT_MAX - 1; // G rows per stage of a multi-energy-pair tile
+  static constexpr int G_STAGE = (ROWS_M * NPSG + 7) & ~7;            // complex (room for the taller box)
+  static constexpr int S_STAGE = ((ROWS_M * NPSS + 1) / 2 + 7) & ~7;  // complex units of the double plane
   static constexpr int C_STAGE = kRows * KCP;
   static constexpr int STAGE = G_STAGE + S_STAGE + C_STAGE;
   static constexpr uint32_t STAGE_BYTES = ROWS * NPSG * 16 + ROWS * NPSS * 8 + C_STAGE * 16;
+  __host__ __device__ static constexpr uint32_t stage_bytes_m(int F) {
+    return ROWS_M * NPSG * 16 + ROWS_M * NPSS * 8 + F * 8 * KCP * 16;
+  }
   static constexpr int PIPE = STAGES * STAGE;
   static constexpr int NCONS = 18;
   static constexpr int THREADS = (NCONS + 1) * 32;
@@ -70,7 +80,7 @@ __device__ __forceinline__ void sigma_pair_stage(C3Acc* acc, const double2* gs, 
 
 struct PairTile {
   SigItem item;
-  int E, kz, Q, il, dc_lo, nchunk, nst, lo, hi;
+  int E, kz, Q, il, dc_lo, nchunk, nst, lo, hi, F, ept;
 };
 
 template <int KC>
@@ -83,17 +93,23 @@ __device__ __forceinline__ PairTile pair_tile(const SigmaArgs& A, int64_t t) {
   T.kz = (int)((t / NP) % A.Nkz);
   T.il = (int)(t / ((int64_t)NP * A.Nkz));
   T.item = A.items[T.il];
-  T.lo = max(0, A.Dmax - (T.E + 1));          // union of the windows of E and E + 1 (R7)
+  // items of n <= 3 pairs: F = ceil(9n/8) m-fragments, ept = 9/F energy pairs per tile (tiles of the other
+  // energy pairs of the group are empty)
+  T.F = (9 * T.item.npair + 7) / 8;
+  T.ept = T.item.npair >= 4 ? 1 : 9 / T.F;
+  const bool skip = ((T.E - A.E0) / 2) % T.ept != 0;
+  T.lo = max(0, A.Dmax - (T.E + 2 * T.ept - 1));   // union of the windows of E .. E + 2·ept − 1 (R7)
   T.hi = min(A.Dwin, A.Dmax - T.E + A.NE);
   T.dc_lo = T.lo / KC;
   T.nchunk = (T.hi + KC - 1) / KC - T.dc_lo;
-  T.nst = A.Nqz * T.nchunk;
+  T.nst = skip ? 0 : A.Nqz * T.nchunk;
   return T;
 }
 
 template <int NN>
 __global__ void __launch_bounds__(SigPairCfg<NN>::THREADS, 1)
-    k_sigma_pair(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmS, SigmaArgs A) {
+    k_sigma_pair(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmS,
+                 const __grid_constant__ CUtensorMap tmGm, const __grid_constant__ CUtensorMap tmSm, SigmaArgs A) {
   using C = SigPairCfg<NN>;
   extern __shared__ uint8_t smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw + ((-smem_u32(smem_raw)) & 127u));
@@ -114,6 +130,8 @@ __global__ void __launch_bounds__(SigPairCfg<NN>::THREADS, 1)
     if (lane == 0) {
       prefetch_tmap(&tmG);
       prefetch_tmap(&tmS);
+      prefetch_tmap(&tmGm);
+      prefetch_tmap(&tmSm);
       uint32_t g = 0;
       for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
         const PairTile T = pair_tile<C::KC>(A, t);
@@ -122,15 +140,16 @@ __global__ void __launch_bounds__(SigPairCfg<NN>::THREADS, 1)
         for (int st = 0; st < T.nst; ++st, ++g) {
           const uint32_t slot = g % C::STAGES;
           if (g >= C::STAGES) mbar_wait(&empty[slot], ((g / C::STAGES) - 1) & 1);
-          mbar_arrive_expect_tx(&full[slot], C::STAGE_BYTES);
+          const bool multi = T.ept > 1;
+          mbar_arrive_expect_tx(&full[slot], multi ? C::stage_bytes_m(T.F) : C::STAGE_BYTES);
           const int dc = T.dc_lo + c;
           const int kp = (int)imod(T.kz - q + A.h, A.Nkz);          // kz - qz (R4, R5)
           double2* gs = smem + slot * C::STAGE;
           const int r0 = T.E - A.Dmax + dc * C::KC;
-          tma_load_4d(gs, &tmG, 2 * rq0, T.item.b_in, r0, kp, &full[slot]);
-          tma_load_4d(gs + C::G_STAGE, &tmS, rq0, r0, kp, T.item.b_in, &full[slot]);
+          tma_load_4d(gs, multi ? &tmGm : &tmG, 2 * rq0, T.item.b_in, r0, kp, &full[slot]);
+          tma_load_4d(gs + C::G_STAGE, multi ? &tmSm : &tmS, rq0, r0, kp, T.item.b_in, &full[slot]);
           bulk_load(gs + C::G_STAGE + C::S_STAGE, A.coef + (((int64_t)T.il * A.Nqz + q) * A.ndc + dc) * C::C_STAGE,
-                    C::C_STAGE * 16, &full[slot]);
+                    (multi ? T.F * 8 : kRows) * C::KCP * 16, &full[slot]);
           if (++c == T.nchunk) {
             c = 0;
             ++q;
@@ -155,12 +174,13 @@ __global__ void __launch_bounds__(SigPairCfg<NN>::THREADS, 1)
     const int n0 = split_b ? nfq / 2 + 1 : (nfq + 1) / 2;
     const int nfw = qq ? nfq - n0 : n0;
     const int f0 = qq ? n0 : 0;
-    const int row = mi * 8 + (lane >> 2);
-    const bool active = mi * 8 < 9 * T.item.npair && nfw > 0;
+    const int eg = mi / T.F, ml = mi - eg * T.F;     // energy pair E + 2·eg, m-fragment ml of the item's rows
+    const int row = ml * 8 + (lane >> 2);
+    const bool active = eg < T.ept && T.E + 2 * eg - A.E0 < A.NEo && ml * 8 < 9 * T.item.npair && nfw > 0;
     // this lane's B element: column 8·f + (lane>>2) -> rc offset 4·f + (lane>>3), energy e = (lane>>2) & 1
     const int n = lane >> 2, e = n & 1;
-    const int boffg = ((lane & 3) + e) * C::NPSG + (n >> 1) + 4 * f0;
-    const int boffs = ((lane & 3) + e) * C::NPSS + (n >> 1) + 4 * f0;
+    const int boffg = ((lane & 3) + e + 2 * eg) * C::NPSG + (n >> 1) + 4 * f0;
+    const int boffs = ((lane & 3) + e + 2 * eg) * C::NPSS + (n >> 1) + 4 * f0;
     C3Acc acc[C::TMAXW];
 #pragma unroll
     for (int f = 0; f < C::TMAXW; ++f) acc[f] = C3Acc{};
@@ -188,8 +208,9 @@ __global__ void __launch_bounds__(SigPairCfg<NN>::THREADS, 1)
     }
     if (active && row < 9 * T.item.npair) {
       // accumulator pair = columns 2·rc + {0, 1} = (rc, E) and (rc, E + 1)
-      double2* out0 = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NEo + T.E - A.E0) * A.rows + row) * A.gt_ld;
-      const bool second = T.E + 1 - A.E0 < A.NEo;
+      const int Eg = T.E + 2 * eg;
+      double2* out0 = A.Gt + ((((int64_t)T.il * A.Nkz + T.kz) * A.NEo + Eg - A.E0) * A.rows + row) * A.gt_ld;
+      const bool second = Eg + 1 - A.E0 < A.NEo;
       double2* out1 = out0 + (int64_t)A.rows * A.gt_ld;
 #pragma unroll
       for (int f = 0; f < C::TMAXW; ++f) {
@@ -210,21 +231,24 @@ static cudaError_t launch_sigma_pair_nn(const SigmaArgs& a, int64_t nitems, cuda
   using C = SigPairCfg<NN>;
   cudaError_t ea = cudaFuncSetAttribute(k_sigma_pair<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (ea != cudaSuccess) return ea;
-  CUtensorMap tmG, tmS;
-  {   // G^X window in the paper layout [Nkz][NE][Nwin][NN]: box = KC + 1 energies of one atom, one quarter's rc range
-    const uint64_t dims[4] = {2ull * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
-    const uint64_t strides[3] = {(uint64_t)NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
-    const uint32_t box[4] = {2 * C::NPSG, 1, C::ROWS, 1};
-    cudaError_t e = make_tmap_f64(&tmG, a.G, 4, dims, strides, box);
-    if (e != cudaSuccess) return e;
-  }
-  {
-    const uint64_t NS = (NN + 1) & ~1ull;
-    const uint64_t dims[4] = {(uint64_t)NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
-    const uint64_t strides[3] = {NS * 8, (uint64_t)a.NE * NS * 8, (uint64_t)a.Nkz * a.NE * NS * 8};
-    const uint32_t box[4] = {C::NPSS, C::ROWS, 1, 1};
-    cudaError_t e = make_tmap_f64(&tmS, a.Gsum, 4, dims, strides, box);
-    if (e != cudaSuccess) return e;
+  CUtensorMap tmG, tmS, tmGm, tmSm;
+  for (int m = 0; m < 2; ++m) {
+    const uint32_t rows = m ? C::ROWS_M : C::ROWS;
+    {   // G^X window in the paper layout [Nkz][NE][Nwin][NN]: box = `rows` energies of one atom, one quarter's rc range
+      const uint64_t dims[4] = {2ull * NN, (uint64_t)a.Nwin, (uint64_t)a.NE, (uint64_t)a.Nkz};
+      const uint64_t strides[3] = {(uint64_t)NN * 16, (uint64_t)a.Nwin * NN * 16, (uint64_t)a.NE * a.Nwin * NN * 16};
+      const uint32_t box[4] = {2 * C::NPSG, 1, rows, 1};
+      cudaError_t e = make_tmap_f64(m ? &tmGm : &tmG, a.G, 4, dims, strides, box);
+      if (e != cudaSuccess) return e;
+    }
+    {
+      const uint64_t NS = (NN + 1) & ~1ull;
+      const uint64_t dims[4] = {(uint64_t)NN, (uint64_t)a.NE, (uint64_t)a.Nkz, (uint64_t)a.Nwin};
+      const uint64_t strides[3] = {NS * 8, (uint64_t)a.NE * NS * 8, (uint64_t)a.Nkz * a.NE * NS * 8};
+      const uint32_t box[4] = {C::NPSS, rows, 1, 1};
+      cudaError_t e = make_tmap_f64(m ? &tmSm : &tmS, a.Gsum, 4, dims, strides, box);
+      if (e != cudaSuccess) return e;
+    }
   }
   SigmaArgs b = a;
   b.ntiles = nitems * ((a.NEo + 1) / 2) * a.Nkz * 4;
@@ -233,7 +257,7 @@ static cudaError_t launch_sigma_pair_nn(const SigmaArgs& a, int64_t nitems, cuda
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(b.ntiles, nsm);
-  k_sigma_pair<NN><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmS, b);
+  k_sigma_pair<NN><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tmG, tmS, tmGm, tmSm, b);
   return cudaGetLastError();
 }
 

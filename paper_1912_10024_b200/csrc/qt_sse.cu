@@ -18,6 +18,12 @@
 #ifndef QT_SIG_PAIR
 #define QT_SIG_PAIR 1
 #endif
+// smallest item (pairs) the energy-pair kernel takes in pair mode; 1 = every item (its multi-energy-pair tiles
+// for items of 1..3 pairs), 4 = items of 1..3 pairs on k_sigma's multi-energy tiles
+#ifndef QT_PAIR_MIN
+#define QT_PAIR_MIN 1
+#endif
+constexpr int kPairMinPairs = QT_PAIR_MIN;
 
 using namespace qt;
 
@@ -306,9 +312,9 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
   L->n_interior_items = (int64_t)L->sig_items.size();
   for (int64_t b = g.w_lo; b < g.w_hi; ++b)
     if (b < g.a_lo || b >= g.a_hi) add_source(b);
-  // Within the interior and the halo sources, items of >= 4 pairs first (the energy-pair contraction kernel takes
-  // them; smaller items keep k_sigma's multi-energy tiles), then the pair list rebuilt in item order so every
-  // chunk's pairs stay contiguous.
+  // Within the interior and the halo sources, items of >= 4 pairs first (full-height tiles before the
+  // multi-energy-pair tiles of the small items; with QT_PAIR_MIN = 4 the small items run k_sigma instead), then
+  // the pair list rebuilt in item order so every chunk's pairs stay contiguous.
   L->sig_pair_mode = !L->fp32 && sigma_pair_supported((int)d.Norb) && QT_SIG_PAIR;
   if (L->sig_pair_mode) {
     auto full_first = [](const SigItem& x) { return x.npair >= 4; };
@@ -457,7 +463,7 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
       c.i1 = i;
       c.nfull = 0;
       if (L->sig_pair_mode)
-        while (c.i0 + c.nfull < c.i1 && L->sig_items[c.i0 + c.nfull].npair >= 4) ++c.nfull;
+        while (c.i0 + c.nfull < c.i1 && L->sig_items[c.i0 + c.nfull].npair >= kPairMinPairs) ++c.nfull;
       const bool halo_src = c.i0 >= L->n_interior_items;
       c.coef_halo = halo_src && g.Ta > 1;
       c.g_halo = halo_src || g.TE > 1;
@@ -1066,7 +1072,7 @@ static void fill_info(const Layout& L, size_t ws_total, qt_sse_info* o) {
   int64_t np_pair = 0;
   if (L.sig_pair_mode)
     for (const SigItem& it : L.sig_items)
-      if (it.npair >= 4) np_pair += it.npair;
+      if (it.npair >= kPairMinPairs) np_pair += it.npair;
   o->flops_sigma_pair = L.sig_pairs.empty() ? 0.0 : L.flops[0] * (double)np_pair / (double)L.sig_pairs.size();
 }
 
