@@ -11,3 +11,7 @@ for v in cur pairmin4; do
   echo "== $v"; python tools/kt.py prof; python tools/kt.py cfg3
   cp /tmp/libqtsse.cur.so paper_1912_10024_b200/libqtsse.so
 done
+# one full capture of the FP32-mode Σ sandwich (profiling slice) for its stall breakdown
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sigma_sand" -c 1 -o gpurun_out/r02m_k_sigma_sand_fp32 \
+    python tools/kt.py prof fp32 > gpurun_out/r02m_ncu_sand32.log 2>&1
+echo "ncu rc=$?"
