@@ -216,10 +216,16 @@ __global__ void __launch_bounds__(kW2Warps * 32) k_pi_w2(PiWArgs A) {
 // Stage = (kz, E0..E0+EC-1, xy0..xy0+XC-1): the W tile [EC][72][XC] (one contiguous 1-D bulk copy) and the G_a window
 // rows E0+s_0 .. E0+EC-1+s_{NWP-1} (4-D TMA box; rows >= NE zero-filled: reading R7). Warp 18 produces;
 // warps 0..17 consume (warp w: m-fragment w%9 of the rows (t,ij), half of the m-column fragments).
+#ifndef QT_PI_EC
+#define QT_PI_EC 1
+#endif
+#ifndef QT_PI_STAGES
+#define QT_PI_STAGES 3
+#endif
 struct PiCfg {
   static constexpr int XC = 20;      // xy per stage: 5 DMMA k-steps; row stride 80 words ≡ 16 (mod 32)
-  static constexpr int EC = 1;       // energies per stage
-  static constexpr int STAGES = 3;
+  static constexpr int EC = QT_PI_EC;   // energies per stage
+  static constexpr int STAGES = QT_PI_STAGES;   // (two for Nω windows > 88 shifts: PiTma::STAGES)
   static constexpr int W_STAGE = EC * kRows * XC;
   static constexpr int NCONS = 18;
   static constexpr int THREADS = (NCONS + 1) * 32;
@@ -234,7 +240,11 @@ struct PiTma {
   static constexpr int STAGE = PiCfg::W_STAGE + G_STAGE + GS_STAGE;
   static constexpr uint32_t STAGE_BYTES = (PiCfg::W_STAGE + GROWS * PiCfg::XC) * 16 + GROWS * PiCfg::XC * 8;
   static constexpr int NF0 = (NFM + 1) / 2, NF1 = NFM / 2;
-  static constexpr size_t SMEM = (size_t)PiCfg::STAGES * STAGE * 16 + 2 * PiCfg::STAGES * 8 + 128;
+  // three stages of (W tile + G window + Re+Im) fit up to 11 column fragments (88 shifts); wider windows take two
+  static constexpr int STAGES = (size_t)PiCfg::STAGES * STAGE * 16 + 2 * PiCfg::STAGES * 8 + 128 <= 227 * 1024
+                                    ? PiCfg::STAGES : 2;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE * 16 + 2 * STAGES * 8 + 128;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 // Complex k-step over N column fragments with Gauss's 3-multiplication form: per fragment
@@ -257,14 +267,14 @@ __device__ __forceinline__ void pi_kstep(C3Acc* acc, double2 a, double as, const
 // without any are skipped.
 template <int NFW, int STRIDE = 0>   // STRIDE > 0: compile-time fragment stride (immediate smem offsets)
 __device__ __forceinline__ void pi_stage(C3Acc* acc, const double2* ws, const double2* gs,
-                                         const double* gss, int rem, int f0, int stride_rt, int nfa) {
+                                         const double* gss, int rem, int nel, int f0, int stride_rt, int nfa) {
   static_assert(NFW > 0, "empty fragment range");
   using C = PiCfg;
   const int stride = STRIDE > 0 ? STRIDE : stride_rt;
   const int fs = stride * 8 * C::XC;
 #pragma unroll
   for (int el = 0; el < C::EC; ++el) {
-    const int ncol = (rem - el + 7) >> 3;                        // column fragments with columns < rem - el
+    const int ncol = el < nel ? (rem - el + 7) >> 3 : 0;         // column fragments with columns < rem - el
     const int nfe = min(nfa, max(0, (ncol - f0 + stride - 1) / stride));
     const double2* w = ws + el * kRows * C::XC;
     const double2* g = gs + el * C::XC;
@@ -299,8 +309,8 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   using T = PiTma<NFM>;
   extern __shared__ uint8_t smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw + ((-smem_u32(smem_raw)) & 127u));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * T::STAGE);
-  uint64_t* empty = full + C::STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::STAGES * T::STAGE);
+  uint64_t* empty = full + T::STAGES;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t blk = blockIdx.x;
@@ -315,7 +325,7 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
   const int nst = A.Nkz * nxc * nec;
 
   if (tid == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < T::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCONS);
     }
@@ -356,8 +366,8 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
       prefetch_tmap(&tmGS);
       int kz = 0, xc = 0, ec = 0;
       for (int st = 0; st < nst; ++st) {
-        const int slot = st % C::STAGES;
-        if (st >= C::STAGES) mbar_wait(&empty[slot], ((st / C::STAGES) - 1) & 1);
+        const int slot = st % T::STAGES;
+        if (st >= T::STAGES) mbar_wait(&empty[slot], ((st / T::STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[slot], T::STAGE_BYTES);
         double2* ws = smem + slot * T::STAGE;
         const int k2 = (int)imod(kz + qz - A.h, A.Nkz);   // kz + qz (R5)
@@ -379,8 +389,8 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
     const bool active = warp < C::NCONS && mi < Fr && nfa > 0;
     int ec = 0;
     for (int st = 0; st < nst; ++st) {
-      const int slot = st % C::STAGES;
-      mbar_wait(&full[slot], (st / C::STAGES) & 1);
+      const int slot = st % T::STAGES;
+      mbar_wait(&full[slot], (st / T::STAGES) & 1);
       if (active) {
         const int aoff = (mi * 8 + (lane >> 2)) * C::XC + (lane & 3);
         const int boff = (f0 * 8 + (lane >> 2)) * C::XC + (lane & 3);
@@ -389,19 +399,20 @@ __global__ void __launch_bounds__(PiCfg::THREADS, 1)
         const double2* gs = st0 + C::W_STAGE + boff;
         const double* gss = reinterpret_cast<const double*>(st0 + C::W_STAGE + T::G_STAGE) + boff;
         const int rem = A.NE - A.E0 - ec * C::EC - A.shift0;
+        const int nel = e_end - ec * C::EC;                     // energies of this stage inside the chunk's range
         // compile-time fragment counts for the common cases (full-speed unrolled path), guarded otherwise
         if (Wp == 2 && nfa == T::NF0) {
-          pi_stage<T::NF0, 2>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+          pi_stage<T::NF0, 2>(acc, ws, gs, gss, rem, nel, f0, Wp, nfa);
         } else if (Wp == 2 && nfa == T::NF0 - 1) {
-          if constexpr (T::NF0 > 1) pi_stage<(T::NF0 > 1 ? T::NF0 - 1 : 1), 2>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+          if constexpr (T::NF0 > 1) pi_stage<(T::NF0 > 1 ? T::NF0 - 1 : 1), 2>(acc, ws, gs, gss, rem, nel, f0, Wp, nfa);
         } else if (nfa == 1) {
-          pi_stage<1>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+          pi_stage<1>(acc, ws, gs, gss, rem, nel, f0, Wp, nfa);
         } else if (nfa == 2) {
-          if constexpr (T::NF0 >= 2) pi_stage<2>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+          if constexpr (T::NF0 >= 2) pi_stage<2>(acc, ws, gs, gss, rem, nel, f0, Wp, nfa);
         } else if (nfa == 3) {
-          if constexpr (T::NF0 >= 3) pi_stage<3>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+          if constexpr (T::NF0 >= 3) pi_stage<3>(acc, ws, gs, gss, rem, nel, f0, Wp, nfa);
         } else {
-          pi_stage<T::NF0>(acc, ws, gs, gss, rem, f0, Wp, nfa);
+          pi_stage<T::NF0>(acc, ws, gs, gss, rem, nel, f0, Wp, nfa);
         }
       }
       __syncwarp();

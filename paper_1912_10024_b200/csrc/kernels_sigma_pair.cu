@@ -81,6 +81,7 @@ __device__ __forceinline__ void sigma_pair_stage(C3Acc* acc, const double2* gs, 
 struct PairTile {
   SigItem item;
   int E, kz, Q, il, dc_lo, nchunk, nst, lo, hi, F, ept;
+  bool skip;   // energy pair served by its group's first tile
 };
 
 template <int KC>
@@ -97,12 +98,12 @@ __device__ __forceinline__ PairTile pair_tile(const SigmaArgs& A, int64_t t) {
   // energy pairs of the group are empty)
   T.F = (9 * T.item.npair + 7) / 8;
   T.ept = T.item.npair >= 4 ? 1 : 9 / T.F;
-  const bool skip = ((T.E - A.E0) / 2) % T.ept != 0;
+  T.skip = ((T.E - A.E0) / 2) % T.ept != 0;
   T.lo = max(0, A.Dmax - (T.E + 2 * T.ept - 1));   // union of the windows of E .. E + 2·ept − 1 (R7)
   T.hi = min(A.Dwin, A.Dmax - T.E + A.NE);
   T.dc_lo = T.lo / KC;
   T.nchunk = (T.hi + KC - 1) / KC - T.dc_lo;
-  T.nst = skip ? 0 : A.Nqz * T.nchunk;
+  T.nst = T.skip ? 0 : A.Nqz * T.nchunk;
   return T;
 }
 
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(SigPairCfg<NN>::THREADS, 1)
   uint32_t g = 0;
   for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
     const PairTile T = pair_tile<C::KC>(A, t);
+    if (T.skip) continue;   // (no stages, and its energies' Gt is written by the group's first tile)
     const int nfq = C::qfrags(T.Q), fq0 = C::qfirst(T.Q);
     const bool split_b = (nfq % 2 == 0) && nfq / 2 + 1 == C::TMAXW;
     const int role = split_b ? roleB : roleA;

@@ -326,25 +326,38 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 #ifndef QT_SAND_PF
 #define QT_SAND_PF 0
 #endif
-constexpr int kSandWarps = QT_SAND_W;   // consumer warps per CTA (energies e ≡ w mod kSandWarps)
-constexpr int kSandSlots = QT_SAND_S;   // Gt ring shared by the warps: kSandSlots - kSandWarps energies prefetched
+// FP32 Gt (the mixed mode): half the bytes per slot, so the ring can be deeper
+#ifndef QT_SAND_WF
+#define QT_SAND_WF 12
+#endif
+#ifndef QT_SAND_SF
+#define QT_SAND_SF 14
+#endif
 
 template <int NO, class R>
 struct SandCfg {
   using C2 = typename Cx<R>::T;
+  static constexpr bool F32 = sizeof(R) == 4;
   static constexpr int NN = NO * NO;
   static constexpr int NNE = (int)(((size_t)NN * sizeof(C2) + 15) / 16 * 16 / sizeof(C2));   // row, 16-byte multiple
   static constexpr int NNP = NNE + 16 / (int)sizeof(C2);   // padded slot row: j = 0,1,2 rows on distinct banks
   static constexpr uint32_t ROWB = (uint32_t)(NNE * sizeof(C2));   // bytes copied per row (the scratch's gt_ld)
   static constexpr int SLOT = 9 * NNP;         // C2 per slot (rows (i,j) of one energy)
   static constexpr int HSZ = 3 * NNP;          // C2 per ∇H triple
-  static constexpr size_t SMEM = ((size_t)kSandSlots * SLOT + 2 * HSZ) * sizeof(C2) + 2 * kSandSlots * 8;
+  static constexpr int WARPS = F32 ? QT_SAND_WF : QT_SAND_W;   // consumer warps per CTA (energies e ≡ w mod WARPS)
+  // Gt ring: SLOTS - WARPS energies prefetched (the FP32 ring as deep as 220 KB allows, up to QT_SAND_SF)
+  static constexpr int SLOTS_FIT = (int)((220 * 1024 - 2 * HSZ * sizeof(C2)) / (SLOT * sizeof(C2) + 16));
+  static constexpr int SLOTS = F32 ? (QT_SAND_SF < SLOTS_FIT ? QT_SAND_SF : SLOTS_FIT) : QT_SAND_S;
+  static_assert(SLOTS > WARPS, "ring deeper than the consumer warps");
+  static constexpr size_t SMEM = ((size_t)SLOTS * SLOT + 2 * HSZ) * sizeof(C2) + 2 * SLOTS * 8;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
   static_assert(3 * NO <= 32, "lanes (j, x)");
 };
 
 template <int NO, class R>
-__global__ void __launch_bounds__((kSandWarps + 1) * 32) k_sigma_sand(SigmaArgs A) {
+__global__ void __launch_bounds__((SandCfg<NO, R>::WARPS + 1) * 32) k_sigma_sand(SigmaArgs A) {
   using Cf = SandCfg<NO, R>;
+  constexpr int kSandWarps = Cf::WARPS, kSandSlots = Cf::SLOTS;
   using C2 = typename Cf::C2;
   constexpr int NN = Cf::NN, NNP = Cf::NNP;
   extern __shared__ __align__(128) double2 sand_raw[];
@@ -654,7 +667,7 @@ static cudaError_t launch_sand_nr(const SigmaArgs& a, int64_t /*nitems*/, cudaSt
   using Cf = SandCfg<NO, R>;
   cudaError_t e = cudaFuncSetAttribute(k_sigma_sand<NO, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
   if (e != cudaSuccess) return e;
-  k_sigma_sand<NO, R><<<(unsigned)(a.npairs_chunk * a.Nkz), (kSandWarps + 1) * 32, Cf::SMEM, st>>>(a);
+  k_sigma_sand<NO, R><<<(unsigned)(a.npairs_chunk * a.Nkz), (Cf::WARPS + 1) * 32, Cf::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 // FP64 Gt scratch (72-row items) or, in the FP32 mixed mode (128-row items), FP32 Gt and an FP32 sandwich

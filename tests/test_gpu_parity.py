@@ -134,6 +134,16 @@ def test_parity_window_sweep(Nw, NE, shift0, Nkz):
     check_full(p, inputs(p, mode=qtgen.INTEGER, seed=Nw), ss=1.0, ps=1.0, exact=True)
 
 
+@pytest.mark.parametrize("Norb,Nw,NE,step", [(2, 128, 150, 1), (10, 100, 110, 1), (3, 43, 100, 3), (9, 89, 100, 1)])
+def test_parity_wide_window(Norb, Nw, NE, step):
+    """Shift windows up to the supported maximum ((Nω−1)·shift_step + 1 = 128, qt_sse.h): Π's correlation tile
+    then has 12..16 column fragments (two pipeline stages instead of three) and Σ's K up to 257 shifts."""
+    nbr = qtgen.geometry.random_graph(6, 5, 0.8, Norb)
+    p = Problem(nbr, Norb, NE, Nw, 2, shift_step=step, name="wide")
+    check_full(p, inputs(p, seed=960 + Norb))
+    check_full(p, inputs(p, mode=qtgen.INTEGER, seed=970 + Norb), ss=1.0, ps=1j, exact=True, fused=True)
+
+
 @pytest.mark.parametrize("step,shift0,Nw,NE", [(2, 1, 4, 20), (3, 2, 5, 30), (2, 3, 7, 12)])
 @pytest.mark.parametrize("prec", [qt.QT_PREC_FP64, qt.QT_PREC_FP32_MIXED])
 def test_parity_shift_step(step, shift0, Nw, NE, prec):
