@@ -394,12 +394,17 @@ __global__ void __launch_bounds__((SandCfg<NO, R>::WARPS + 1) * 32) k_sigma_sand
       for (int e = 0; e < A.NEo; ++e) {
         const int slot = e % kSandSlots;
         if (e >= kSandSlots) mbar_wait(&empty[slot], ((e / kSandSlots) - 1) & 1);
-        mbar_arrive_expect_tx(&full[slot], 9 * Cf::ROWB);
         const C2* src = gsrc + (int64_t)e * A.rows * ld;
         if (QT_SAND_PF > 0 && e + QT_SAND_PF < A.NEo)   // the pair's 9 rows are contiguous: one L2 prefetch
-          bulk_prefetch_l2(src + (int64_t)QT_SAND_PF * A.rows * ld, 9 * Cf::ROWB);
-        for (int r = 0; r < 9; ++r)
-          bulk_load(ring + slot * Cf::SLOT + r * NNP, src + r * ld, Cf::ROWB, &full[slot]);
+          bulk_prefetch_l2(src + (int64_t)QT_SAND_PF * A.rows * ld, 9 * ld * (uint32_t)sizeof(C2));
+        if (ld == NNP) {   // scratch rows already padded like the slot: one copy (the per-copy cost dominates)
+          mbar_arrive_expect_tx(&full[slot], 9 * NNP * (uint32_t)sizeof(C2));
+          bulk_load(ring + slot * Cf::SLOT, src, 9 * NNP * (uint32_t)sizeof(C2), &full[slot]);
+        } else {
+          mbar_arrive_expect_tx(&full[slot], 9 * Cf::ROWB);
+          for (int r = 0; r < 9; ++r)
+            bulk_load(ring + slot * Cf::SLOT + r * NNP, src + r * ld, Cf::ROWB, &full[slot]);
+        }
       }
     }
     return;

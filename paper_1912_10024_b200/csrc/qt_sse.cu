@@ -80,6 +80,7 @@ struct Layout {
   std::vector<PiGroup> groups;
   int64_t n_interior_items = 0;
   int64_t sig_rows = kRows, ndc = 0, NNp = 0, Epad = 0, NEp = 0, Kp = 0;
+  int64_t gt_ld = 0;   // Gt scratch row stride (elements)
   int64_t sig_ec = 0, pi_ec = 0;   // energies per Σ / Π scratch sub-range (= NEo unless the workspace is small)
   size_t ws_bytes = 0, gt_offset = 0, part_bytes = 0;
   std::vector<HaloPeer> peers;
@@ -387,8 +388,11 @@ qt_status build_layout(const qt_sse_desc* desc, const int32_t* nbr, bool reduce,
 
   // workspace (shared by the Σ coefficient tables + Gt scratch and the Π W scratch; calls are serialized)
   L->sig_rows = L->fp32 ? kTcRows : kRows;
-  const size_t gt_e = (size_t)d.Nkz * L->sig_rows * ((L->NN + 19) / 20) * 20 *
-                      (L->fp32 ? sizeof(float2) : sizeof(double2));   // Gt scratch per item and energy
+  // Gt row stride = the Σ sandwich's padded shared-memory row (Norb² rounded to 16 bytes + 16 bytes), so one bulk
+  // copy moves a pair's 9 rows of an energy into its ring slot with the bank-conflict padding in place
+  L->gt_ld = L->fp32 ? ((L->NN + 1) & ~int64_t(1)) + 2 : L->NN + 1;
+  const size_t gt_e = (size_t)d.Nkz * L->sig_rows * std::max<int64_t>((L->NN + 19) / 20 * 20, L->gt_ld) *
+                      (L->fp32 ? sizeof(float2) : sizeof(double2));   // Gt (and Π W) scratch per item and energy
   L->NNp = (L->NN + 3) & ~int64_t(3);
   L->Epad = L->NEw + d.shift0 + 80 + 1;
   // W scratch of one item for ne energies (FP32: split planes with each kz row padded to whole 32-chunks)
@@ -785,7 +789,7 @@ qt_status run_sigma(qt_sse_plan_s* p, const void* dH, const void* GL, const void
       sa.Dwin = (int)L.Dwin;
       sa.rows = (int)L.sig_rows;
       sa.gt_f32 = L.fp32 ? 1 : 0;
-      sa.gt_ld = L.fp32 ? (int)((L.NN + 1) & ~int64_t(1)) : (int)L.NN;
+      sa.gt_ld = (int)L.gt_ld;
       sa.ntiles = 0;
       sa.det_atoms = p->d_det_atoms ? p->d_det_atoms + ch.det_off : nullptr;
       sa.det_pairs = p->d_det_pairs;
