@@ -326,6 +326,10 @@ __global__ void __launch_bounds__(SigTmaCfg<NF>::THREADS, 1)
 #ifndef QT_SAND_PF
 #define QT_SAND_PF 0
 #endif
+#ifndef QT_SAND_KU
+#define QT_SAND_KU 2
+#endif
+constexpr int kSandKU = QT_SAND_KU;   // unroll of the sandwich's k loop (loads of the next k in flight)
 // FP32 Gt (the mixed mode): half the bytes per slot, so the ring can be deeper
 #ifndef QT_SAND_WF
 #define QT_SAND_WF 12
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__((SandCfg<NO, R>::WARPS + 1) * 32) k_sigma_sand
     for (int i = 0; i < 3; ++i) {   // (i, k) loops rolled: keeps the kernel inside the instruction cache
       const C2* gr = g + (i * 3 + j) * NNP;
       const C2* hl = Hl + i * NNP + x * NO;
-#pragma unroll 2
+#pragma unroll kSandKU
       for (int k = 0; k < NO; ++k) {
         const C2 h = hl[k];
 #pragma unroll

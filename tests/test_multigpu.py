@@ -1,6 +1,8 @@
 """Multi-GPU parity over real NCCL (halo exchange inside qt_sse_sigma_pi, Π reduction to sub-slab owners): runs
 tests/mgpu_worker.py under torchrun on 2 (or 4) GPUs, skipped when fewer are visible. The same sharded kernels
 are covered on ONE GPU by tests/test_gpu_loopback.py."""
+import os
+import signal
 import socket
 import subprocess
 import sys
@@ -27,9 +29,22 @@ def _run(n, args):
     root = Path(__file__).resolve().parent.parent
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", str(root / "tests" / "mgpu_worker.py"), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "mgpu ok" in r.stdout
+    # own process group: on a timeout torchrun AND its workers are stopped (an orphaned worker spinning on a GPU
+    # would slow or break every later case on that GPU)
+    pr = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=root,
+                          start_new_session=True)
+    try:
+        out, err = pr.communicate(timeout=420)
+    except subprocess.TimeoutExpired:
+        os.killpg(pr.pid, signal.SIGTERM)
+        try:
+            out, err = pr.communicate(timeout=30)
+        except subprocess.TimeoutExpired:
+            os.killpg(pr.pid, signal.SIGKILL)
+            out, err = pr.communicate()
+        pytest.fail("multi-GPU worker timed out\n" + out[-3000:] + err[-3000:])
+    assert pr.returncode == 0, out[-3000:] + err[-3000:]
+    assert "mgpu ok" in out
 
 
 @pytest.mark.parametrize("cfg,mode,prec,shard,call", [
