@@ -169,6 +169,22 @@ def test_per_rank_flops_partition_the_total(nranks):
             assert all(infos[r]["e_hi"] == infos[r + 1]["e_lo"] for r in range(nranks - 1))
 
 
+def test_energy_pair_kernel_flop_share():
+    """qt_sse_shard_info.flops_sigma_pair: in FP64 pair mode (Norb 9..11) every Σ item runs on k_sigma_pair, so its
+    share is the whole Σ D-contraction (rank shares included); FP32 mode and Norb outside 9..11 report 0."""
+    import paper_1912_10024_b200 as qt
+    for name, share in (("small", 1.0), ("prof", 1.0), ("tiny", 0.0)):   # tiny: Norb 4
+        p = qtgen.problem(name)
+        contr = qt.count_flops(p)["sigma_contraction"]
+        i = qt.shard_info(p, 0, 1)
+        assert abs(i["flops_sigma_pair"] - share * contr) <= 1e-9 * contr, (name, i["flops_sigma_pair"], contr)
+        assert qt.shard_info(p, 0, 1, precision=qt.QT_PREC_FP32_MIXED)["flops_sigma_pair"] == 0.0
+    p = qtgen.problem("prof")
+    parts = [qt.shard_info(p, r, 3)["flops_sigma_pair"] for r in range(3)]
+    tot = qt.count_flops(p)["sigma_contraction"]
+    assert abs(sum(parts) - tot) <= 1e-9 * tot
+
+
 def _gworker(rank, world, ga, port, result_q):
     """Ta x TE grid (the paper's 2-D tiling): the oracle on this rank's window (atom window x energy
     window) reproduces its owned Σ block; Π of the rank is its partial sum over its OWN energies (emulated here by
