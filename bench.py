@@ -446,8 +446,8 @@ def main():
     if pair_n > 0:
         dom, dom_ms, dom_n = "k_sigma_pair", pair_ms, pair_n
         dom_flops = info["flops_sigma_pair"]
-        kname = ("k_sigma_pair (Σ D-contraction on energy-pair tiles: items of >= 4 pairs, "
-                 f"{100 * dom_flops / max(contr_step, 1):.1f}% of the contraction flops; DMMA.8x8x4 FP64)")
+        kname = ("k_sigma_pair (Σ D-contraction on energy-pair tiles, multi-energy-pair tiles for items of 1-3 "
+                 f"pairs: {100 * dom_flops / max(contr_step, 1):.1f}% of the contraction flops; DMMA.8x8x4 FP64)")
     else:
         dom, (dom_ms, dom_n) = "k_sigma", kern["k_sigma"]
         dom_flops = contr_step
